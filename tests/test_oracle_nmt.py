@@ -1,0 +1,97 @@
+"""Pins for oracle/nmt.py: full training-step loss and gradients."""
+import numpy as np
+import torch
+
+from oracle import nmt as O
+from synth.configs import C1, SMALL_NMT
+from synth.data import nmt_params, nmt_batch
+
+
+def _f64(p):
+    return {k: np.asarray(v, np.float64) for k, v in p.items()}
+
+
+def test_zero_weights_closed_form():
+    """All weights/biases 0 => h = a = 0, logits = 0 => loss = ln V; dbo = mean(softmax - onehot)."""
+    cfg = C1
+    P = {k: np.zeros_like(v, dtype=np.float64) for k, v in nmt_params(0, cfg).items()}
+    b = nmt_batch(1, cfg, lengths="random")
+    r = O.step(P, b, cfg)
+    assert abs(r["loss"] - np.log(cfg.V)) < 1e-14
+    counts = np.bincount(b["tgt_out"].reshape(-1), minlength=cfg.V)
+    expect = (1.0 / cfg.V) - counts / (cfg.B * cfg.Td)
+    assert np.abs(r["grads"]["out.bo"] - expect).max() < 1e-15
+    assert np.all(r["grads"]["out.Wo"] == 0)
+
+
+def test_fd_sampled_gradients_c1():
+    cfg = C1
+    P = _f64(nmt_params(3, cfg))
+    b = nmt_batch(4, cfg, lengths="random")
+    G = O.step(P, b, cfg)["grads"]
+    g = np.random.default_rng(0)
+    eps = 1e-6
+    for name, val in P.items():
+        flat = val.reshape(-1)
+        idxs = g.choice(flat.size, size=min(4, flat.size), replace=False)
+        if name.startswith("emb"):   # pick rows that are actually used
+            toks = b["src"] if name == "emb_src" else b["tgt_in"]
+            row = int(toks.reshape(-1)[0])
+            idxs = np.array([row * val.shape[1] + j for j in range(3)])
+        for i in idxs:
+            Pp = {k: v.copy() for k, v in P.items()}
+            Pm = {k: v.copy() for k, v in P.items()}
+            Pp[name].reshape(-1)[i] += eps
+            Pm[name].reshape(-1)[i] -= eps
+            num = (O.step(Pp, b, cfg, False)["loss"] - O.step(Pm, b, cfg, False)["loss"]) / (2 * eps)
+            ana = G[name].reshape(-1)[i]
+            assert abs(num - ana) <= 1e-7 + 1e-6 * abs(num), (name, i, num, ana)
+
+
+def _torch_nmt_loss(P, b, cfg):
+    """Same model written with torch.nn.LSTM / LSTMCell + autograd (library routines)."""
+    T = {k: torch.from_numpy(v).requires_grad_(True) for k, v in P.items()}
+    B, H, E = cfg.B, cfg.H, cfg.E
+    x = T["emb_src"][torch.from_numpy(b["src"])].transpose(0, 1)
+    for l in range(cfg.enc_layers):
+        m = torch.nn.LSTM(x.shape[2], H).double()
+        x, _ = torch.func.functional_call(m, {"weight_ih_l0": T[f"enc{l}.Wx"], "weight_hh_l0": T[f"enc{l}.Wh"],
+                                              "bias_ih_l0": T[f"enc{l}.b"], "bias_hh_l0": torch.zeros(4 * H, dtype=torch.float64)}, (x,))
+    Hs = x.transpose(0, 1)
+    Kp = Hs @ T["att.Wk"].T
+    valid = torch.arange(cfg.Ts)[None, :] < torch.from_numpy(b["src_len"]).long()[:, None]
+    cells = [torch.nn.LSTMCell(E + H if l == 0 else H, H).double() for l in range(cfg.dec_layers)]
+    h = [torch.zeros(B, H, dtype=torch.float64) for _ in cells]
+    c = [torch.zeros(B, H, dtype=torch.float64) for _ in cells]
+    a = torch.zeros(B, H, dtype=torch.float64)
+    loss = 0
+    for t in range(cfg.Td):
+        inp = torch.cat([T["emb_tgt"][torch.from_numpy(b["tgt_in"][:, t])], a], dim=1)
+        for l, cell in enumerate(cells):
+            h[l], c[l] = torch.func.functional_call(cell, {"weight_ih": T[f"dec{l}.Wx"], "weight_hh": T[f"dec{l}.Wh"],
+                                                          "bias_ih": T[f"dec{l}.b"], "bias_hh": torch.zeros(4 * H, dtype=torch.float64)},
+                                                    (inp, (h[l], c[l])))
+            inp = h[l]
+        q = inp
+        qp = q @ T["att.Wq"].T + T["att.bq"]
+        sc = torch.tanh(qp[:, None, :] + Kp) @ T["att.v"]
+        alpha = torch.softmax(sc.masked_fill(~valid, float("-inf")), dim=1)
+        ctx = torch.einsum("bs,bsk->bk", alpha, Hs)
+        a = torch.tanh(ctx @ T["att.Wcc"].T + q @ T["att.Wch"].T)
+        logits = a @ T["out.Wo"].T + T["out.bo"]
+        loss = loss + torch.nn.functional.cross_entropy(logits, torch.from_numpy(b["tgt_out"][:, t]), reduction="sum")
+    loss = loss / (B * cfg.Td)
+    loss.backward()
+    return loss.item(), {k: v.grad.numpy() for k, v in T.items()}
+
+
+def test_torch_autograd_crosscheck_small_nmt():
+    cfg = SMALL_NMT
+    P = _f64(nmt_params(5, cfg))
+    b = nmt_batch(6, cfg, lengths="random")
+    r = O.step(P, b, cfg)
+    tl, tg = _torch_nmt_loss(P, b, cfg)
+    assert abs(r["loss"] - tl) < 1e-12
+    for k in P:
+        scale = max(np.abs(tg[k]).max(), 1e-30)
+        assert np.abs(r["grads"][k] - tg[k]).max() / scale < 1e-10, k
