@@ -1,0 +1,212 @@
+/* echo.h — C ABI of libecho.so, the B200 (sm_100a) hot path of Echo
+ * (Zheng et al., arXiv 1805.08899; /root/reference/PAPER.md).
+ *
+ * Echo recomputes "the feature maps of the attention and RNN layers rather
+ * than stashing them persistently in the GPU memory" and fuses
+ * the recomputation into the backward pass (Echo-dagger).
+ * This library provides the cheap non-FC parts of that path as fused kernels;
+ * the fully-connected contractions around them (Eq. 1) are
+ * done by the caller (cuBLAS) and are outside this library by design.
+ *
+ * Conventions for every compute entry point
+ *   - All tensor pointers are DEVICE pointers, row-major, densely packed unless
+ *     a stride is given.  The CALLER owns every buffer; the library never
+ *     allocates or frees device memory, never synchronises, keeps no device
+ *     state and is re-entrant.
+ *   - "storage dtype" s is fp32 or bf16 (echo_dtype); all math and
+ *     accumulation are fp32.  Tensors documented "fp32" are fp32 in both.
+ *   - Every value the STASH mode stores is rounded to s once, at production;
+ *     both modes read the rounded value (rounding contract, DESIGN.md a4), so
+ *     STASH and RECOMPUTE gradients are bit-identical.
+ *   - Vectorised 128-bit access: every pointer must be 16-byte aligned and the
+ *     innermost extents (H, A, Hk, L) multiples of 8, else ECHO_ERR_INVALID.
+ *   - Kernels are launched on `stream` (a cudaStream_t passed as void*).
+ *     Launch-configuration errors are reported synchronously (cudaGetLastError
+ *     after the launch -> ECHO_ERR_CUDA); asynchronous faults surface at the
+ *     caller's next synchronisation.  Safe to record in a CUDA graph.
+ *   - On any non-OK return nothing has been launched (validation happens
+ *     first) except for ECHO_ERR_CUDA; echo_last_error() returns a
+ *     thread-local message describing the last failure.
+ */
+#ifndef ECHO_H_
+#define ECHO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ECHO_ABI_VERSION 1
+
+typedef enum {
+  ECHO_OK = 0,
+  ECHO_ERR_INVALID = 1,     /* bad argument / parse / validation            */
+  ECHO_ERR_GRAPH = 2,       /* estimator pipeline error (cycle, bad op)      */
+  ECHO_ERR_CAPACITY = 3,    /* size cap (shared memory tile, report buffer) */
+  ECHO_ERR_MISMATCH = 4,    /* debug self-verification failed                */
+  ECHO_ERR_CUDA = 5,        /* CUDA launch error                             */
+  ECHO_ERR_UNSUPPORTED = 6
+} echo_status;
+
+typedef enum { ECHO_FP32 = 0, ECHO_BF16 = 1 } echo_dtype;   /* storage dtype s */
+typedef enum { ECHO_STASH = 0, ECHO_RECOMPUTE = 1 } echo_mode;
+
+const char* echo_last_error(void);
+int echo_abi_version(void);
+
+/* ===================================================================== LSTM
+ * PAPER.md §2, lines 101-112 (Fig. 1): the cell's FC outputs (Eq. 1) enter the
+ * non-linear block f (slicing + element-wise ops) which outputs h_t, c_t.
+ * Gate order along the 4H axis: i | f | g | o (contiguous H blocks).
+ *   i = sigma(A_i), f = sigma(A_f), g = tanh(A_g), o = sigma(A_o)
+ *   c_t = f * c_{t-1} + i * g ;  h_t = o * tanh(c_t)
+ * Feature maps (Echo plan, DESIGN.md table T3): both modes stash the gates
+ * [B,4H]; STASH additionally keeps c_t (fp32), tanh(c_t) and h_t; RECOMPUTE
+ * regenerates c (echo_lstm_cscan) and tanh(c), h (echo_lstm_bwd) in the
+ * backward pass.  Time order is the caller's processing order (a reverse-
+ * direction layer simply processes t = T-1..0).
+ */
+typedef struct {
+  int32_t B;          /* batch rows, > 0                    */
+  int32_t H;          /* hidden width, > 0, multiple of 8   */
+  int32_t dtype;      /* echo_dtype                          */
+  int32_t mode;       /* echo_mode                           */
+} echo_lstm_desc;
+
+/* a1 — forward pointwise step.
+ *  gx_t    [B,4H] s   x_t W_x^T (+ b) (+ h_{t-1} W_h^T when gh_t == NULL)
+ *  gh_t    [B,4H] s   h_{t-1} W_h^T, or NULL if already accumulated into gx_t
+ *  bias    [4H]  fp32 or NULL if folded into gx_t
+ *  c_prev  [B,H] fp32 c_{t-1}
+ *  gates_t [B,4H] s   OUT i|f|g|o (the stash in both modes); may alias gx_t
+ *  c_out   [B,H] fp32 OUT c_t (must not alias c_prev)
+ *  tc_t    [B,H] s    OUT tanh(c_t): required in STASH, must be NULL in RECOMPUTE
+ *  h_out   [B,H] s    OUT h_t                                                   */
+echo_status echo_lstm_fwd(const echo_lstm_desc* d, const void* gx_t, const void* gh_t,
+                          const float* bias, const float* c_prev, void* gates_t,
+                          float* c_out, void* tc_t, void* h_out, void* stream);
+
+/* a2 — cell-state regeneration scan (RECOMPUTE backward prologue, run once per
+ * layer before the reverse time loop).  Re-executes the mirrored c-chain from
+ * the stashed gates and c_0 (Fig. 4 step 4; recomputation path
+ * Fig. 8(c)), with the exact device function of a1.
+ *  gates [T,B,4H] s   stashed gates in processing order
+ *  c0    [B,H] fp32
+ *  c_ws  [T,B,H] fp32 OUT c_1..c_T (transient workspace owned by the caller) */
+echo_status echo_lstm_cscan(const echo_lstm_desc* d, int32_t T, const void* gates,
+                            const float* c0, float* c_ws, void* stream);
+
+/* a3 — backward step with fused recomputation (Echo-dagger fusion).
+ *  gates_t [B,4H] s    stashed i|f|g|o
+ *  c_prev  [B,H] fp32  c_{t-1} (c_0, the STASH c buffer, or the a2 workspace)
+ *  c_t     [B,H] fp32  RECOMPUTE: c_t from a2; STASH: NULL
+ *  tc_t    [B,H] s     STASH: stashed tanh(c_t); RECOMPUTE: NULL
+ *  dh_t    [B,H] fp32  total dLoss/dh_t (from above + recurrent)
+ *  dc      [B,H] fp32  IN dLoss/dc_t carried from t+1; OUT dLoss/dc_{t-1}
+ *  dA_t    [B,4H] s    OUT dLoss/dA_t (pre-activations); may alias gates_t
+ *  h_regen [B,H] s     RECOMPUTE: OUT regenerated h_t (for the caller's dW GEMMs) or NULL;
+ *                      STASH: must be NULL                                           */
+echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_t, const float* c_prev,
+                          const float* c_t, const void* tc_t, const float* dh_t, float* dc,
+                          void* dA_t, void* h_regen, void* stream);
+
+/* ===================================================================== MLP attention
+ * PAPER.md §2 lines 129-133 and Fig. 7 (the scoring function as
+ * broadcast-add + tanh):  for each row b and source position s < len_b
+ *   E_s = tanh(qp_b + Kp_{b,s})   score_s = E_s . v   alpha = softmax_s(score)
+ *   ctx_b = sum_s alpha_s Hs_{b,s}
+ * One query per row (the NMT decoder calls this once per target step).
+ * Feature maps (Echo plan, DESIGN.md table T4): STASH keeps E [B,Ts,A] s and
+ * alpha [B,Ts] fp32 (and the caller keeps ctx); RECOMPUTE keeps nothing and
+ * echo_attn_bwd regenerates E, scores, alpha and ctx.
+ */
+typedef struct {
+  int32_t B, Ts, A, Hk;   /* > 0; A, Hk multiples of 8; Ts <= 4096                  */
+  int32_t dtype;          /* echo_dtype                                              */
+  int32_t mode;           /* echo_mode                                               */
+  int64_t kp_stride_b;    /* element stride of Kp (and dKp) between rows b (Ts*A for [B,Ts,A], A for [Ts,B,A]) */
+  int64_t kp_stride_s;    /* element stride of Kp (and dKp) between positions s (A, or B*A)                 */
+  int64_t hs_stride_b;    /* element stride of Hs (and dHs) between rows b (Ts*Hk or Hk)                    */
+  int64_t hs_stride_s;    /* element stride of Hs (and dHs) between positions s (Hk or B*Hk)                */
+} echo_attn_desc;
+
+/* a5 — forward.
+ *  qp [B,A] s, Kp strided [B,Ts,A] s, v [A] s, Hs strided [B,Ts,Hk] s, src_len [B] int32 in
+ *  [1,Ts] or NULL (= Ts), ctx [B,Hk] s OUT, E_st [B,Ts,A] s OUT (STASH) / NULL,
+ *  alpha_st [B,Ts] fp32 OUT (STASH) / NULL.  Masked positions get alpha = 0.      */
+echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
+                          const void* Hs, const int32_t* src_len, void* ctx, void* E_st,
+                          float* alpha_st, void* stream);
+
+/* a6 — backward with fused recomputation.
+ *  E_st, alpha_st   STASH inputs from a5 (NULL in RECOMPUTE)
+ *  dctx   [B,Hk] fp32    dLoss/dctx
+ *  dqp    [B,A] fp32     OUT dLoss/dqp (overwritten)
+ *  dKp    [B,Ts,A] fp32  ACCUMULATED (+=) dLoss/dKp, same strides as Kp
+ *  dHs    [B,Ts,Hk] fp32 ACCUMULATED (+=) dLoss/dHs, same strides as Hs
+ *  dv_part [B,A] fp32    ACCUMULATED (+=) per-row partials of dLoss/dv; reduce
+ *                        with echo_attn_dv_reduce (fixed order, no atomics)
+ *  ctx_regen [B,Hk] s    OUT regenerated ctx (RECOMPUTE; bit-identical to a5's) or NULL */
+echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
+                          const void* Hs, const int32_t* src_len, const void* E_st,
+                          const float* alpha_st, const float* dctx, float* dqp, float* dKp,
+                          float* dHs, float* dv_part, void* ctx_regen, void* stream);
+
+/* dv[a] (+)= sum_b dv_part[b,a] in ascending b (deterministic).  accumulate != 0 adds to dv. */
+echo_status echo_attn_dv_reduce(int32_t B, int32_t A, const float* dv_part, float* dv,
+                                int32_t accumulate, void* stream);
+
+/* ===================================================================== dot-product softmax + dropout
+ * Transformer attention probabilities (§6.3.2): P =
+ * softmax(scale * S) per row, P_d = P * m / (1 - p) with keep-mask m.  Echo
+ * recomputes P in the backward pass and stores the dropout feature map as a
+ * 1-bit mask (Alg. 1 line 18).
+ * m is Philox4x32-10: element n (row-major) uses counter offset + n/4 and key
+ * seed, word n%4; keep iff (word >> 8) >= floor(p * 2^24)  (R19).
+ */
+typedef struct {
+  int32_t R, L;           /* rows, row length (L multiple of 8, <= 2048)   */
+  int32_t dtype, mode;
+  float scale;            /* applied to S before the softmax               */
+  float dropout_p;        /* in [0, 1)                                     */
+  uint64_t seed, offset;  /* Philox key and counter base                   */
+} echo_dot_desc;
+
+/* a7 forward.  S [R,L] s (caller's Q K^T), Pd [R,L] s OUT (feeds the caller's PV GEMM),
+ *  P_st [R,L] s OUT (STASH) / NULL, mask: STASH byte mask [R,L] uint8 OUT;
+ *  RECOMPUTE bit mask [R, L/8] uint8 OUT (bit j%8 of byte j/8).                        */
+echo_status echo_dot_softmax_fwd(const echo_dot_desc* d, const void* S, void* Pd, void* P_st,
+                                 uint8_t* mask, void* stream);
+
+/* a7 backward.  dPd [R,L] s = dLoss/dP_d.  STASH: reads P_st + byte mask (S may be NULL);
+ *  RECOMPUTE: reads S + bit mask and regenerates P.  dS [R,L] s OUT = dLoss/dS (may alias dPd);
+ *  Pd_regen [R,L] s OUT (RECOMPUTE; for the caller's dV GEMM) or NULL.                */
+echo_status echo_dot_softmax_bwd(const echo_dot_desc* d, const void* S, const void* P_st,
+                                 const uint8_t* mask, const void* dPd, void* dS, void* Pd_regen,
+                                 void* stream);
+
+/* ===================================================================== footprint estimator
+ * Host-only, integer, deterministic.  Runs the adjusted pass pipeline of
+ * Fig. 14: Gradient -> InferShape&Type -> EdgeUseRef ->
+ * Echo (Algorithm 1) -> DeadNodeElimination
+ * -> InferShape&Type -> liveness planning, and reports per-edge decisions and
+ * exact byte totals.
+ *  graph_json   NUL-terminated graph document (schema in DESIGN.md "Graph
+ *               document": {version:1, placeholders:[...], nodes:[...], outputs:[...]})
+ *  config_json  NUL-terminated strategy config {strategy: "baseline"|"mirror"|"echo",
+ *               compute_heavy_ops, binarizable_ops, enable_dead_node,
+ *               enable_binarization, flop_threshold, weight_multiplier}; NULL = echo defaults
+ *  report_json  caller buffer for the NUL-terminated report; may be NULL to query
+ *  report_len   IN capacity of report_json; OUT bytes needed (including the NUL).
+ *               Returns ECHO_ERR_CAPACITY (with *report_len set) if too small.
+ * Errors: ECHO_ERR_INVALID (parse / schema / unknown op / arity / shape),
+ *         ECHO_ERR_GRAPH (cycle or pipeline failure).                              */
+echo_status echo_footprint_estimate(const char* graph_json, const char* config_json,
+                                    char* report_json, size_t* report_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECHO_H_ */

@@ -1,0 +1,161 @@
+"""Thin ctypes binding of libecho.so (include/echo.h).  Argument marshalling only.
+
+Every function here has the C name and the C argument order; tensors are
+passed as torch tensors (device pointers via .data_ptr(), None -> NULL) and the
+stream defaults to torch's current CUDA stream.  No computation happens in
+Python: a missing library or a non-OK status raises immediately (there is no
+CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libecho.so")
+
+ECHO_OK, ECHO_ERR_INVALID, ECHO_ERR_GRAPH, ECHO_ERR_CAPACITY, ECHO_ERR_MISMATCH, ECHO_ERR_CUDA, ECHO_ERR_UNSUPPORTED = range(7)
+FP32, BF16 = 0, 1
+STASH, RECOMPUTE = 0, 1
+
+EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_cscan", "echo_lstm_bwd",
+            "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
+            "echo_dot_softmax_bwd", "echo_footprint_estimate")
+
+
+class EchoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"libecho status {status}: {msg}")
+        self.status = status
+
+
+class LstmDesc(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("dtype", ctypes.c_int32), ("mode", ctypes.c_int32)]
+
+
+class AttnDesc(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("Ts", ctypes.c_int32), ("A", ctypes.c_int32), ("Hk", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("kp_stride_b", ctypes.c_int64), ("kp_stride_s", ctypes.c_int64),
+                ("hs_stride_b", ctypes.c_int64), ("hs_stride_s", ctypes.c_int64)]
+
+
+class DotDesc(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_int32), ("L", ctypes.c_int32), ("dtype", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("scale", ctypes.c_float), ("dropout_p", ctypes.c_float),
+                ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libecho.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libecho.so not found at {path}; run `python -m paper_1805_08899_b200.build`")
+    lib = ctypes.CDLL(path)
+    vp, i32, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64
+    lib.echo_last_error.restype = ctypes.c_char_p
+    lib.echo_abi_version.restype = ctypes.c_int
+    sigs = {
+        "echo_lstm_fwd": [ctypes.POINTER(LstmDesc)] + [vp] * 9,
+        "echo_lstm_cscan": [ctypes.POINTER(LstmDesc), i32, vp, vp, vp, vp],
+        "echo_lstm_bwd": [ctypes.POINTER(LstmDesc)] + [vp] * 9,
+        "echo_attn_fwd": [ctypes.POINTER(AttnDesc)] + [vp] * 9,
+        "echo_attn_bwd": [ctypes.POINTER(AttnDesc)] + [vp] * 14,
+        "echo_attn_dv_reduce": [i32, i32, vp, vp, i32, vp],
+        "echo_dot_softmax_fwd": [ctypes.POINTER(DotDesc)] + [vp] * 5,
+        "echo_dot_softmax_bwd": [ctypes.POINTER(DotDesc)] + [vp] * 7,
+        "echo_footprint_estimate": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)],
+    }
+    for name, args in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _p(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is not None:
+        return stream if isinstance(stream, int) else stream.cuda_stream
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _check(status):
+    if status != ECHO_OK:
+        raise EchoError(status, load().echo_last_error().decode())
+
+
+def echo_abi_version() -> int:
+    return load().echo_abi_version()
+
+
+def echo_last_error() -> str:
+    return load().echo_last_error().decode()
+
+
+# ---------------------------------------------------------------- LSTM
+def echo_lstm_fwd(d, gx_t, gh_t, bias, c_prev, gates_t, c_out, tc_t, h_out, stream=None):
+    _check(load().echo_lstm_fwd(ctypes.byref(d), _p(gx_t), _p(gh_t), _p(bias), _p(c_prev), _p(gates_t), _p(c_out),
+                                _p(tc_t), _p(h_out), _stream(stream)))
+
+
+def echo_lstm_cscan(d, T, gates, c0, c_ws, stream=None):
+    _check(load().echo_lstm_cscan(ctypes.byref(d), int(T), _p(gates), _p(c0), _p(c_ws), _stream(stream)))
+
+
+def echo_lstm_bwd(d, gates_t, c_prev, c_t, tc_t, dh_t, dc, dA_t, h_regen, stream=None):
+    _check(load().echo_lstm_bwd(ctypes.byref(d), _p(gates_t), _p(c_prev), _p(c_t), _p(tc_t), _p(dh_t), _p(dc),
+                                _p(dA_t), _p(h_regen), _stream(stream)))
+
+
+# ---------------------------------------------------------------- MLP attention
+def echo_attn_fwd(d, qp, Kp, v, Hs, src_len, ctx, E_st, alpha_st, stream=None):
+    _check(load().echo_attn_fwd(ctypes.byref(d), _p(qp), _p(Kp), _p(v), _p(Hs), _p(src_len), _p(ctx), _p(E_st),
+                                _p(alpha_st), _stream(stream)))
+
+
+def echo_attn_bwd(d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part, ctx_regen, stream=None):
+    _check(load().echo_attn_bwd(ctypes.byref(d), _p(qp), _p(Kp), _p(v), _p(Hs), _p(src_len), _p(E_st), _p(alpha_st),
+                                _p(dctx), _p(dqp), _p(dKp), _p(dHs), _p(dv_part), _p(ctx_regen), _stream(stream)))
+
+
+def echo_attn_dv_reduce(B, A, dv_part, dv, accumulate, stream=None):
+    _check(load().echo_attn_dv_reduce(int(B), int(A), _p(dv_part), _p(dv), int(accumulate), _stream(stream)))
+
+
+# ---------------------------------------------------------------- dot softmax + dropout
+def echo_dot_softmax_fwd(d, S, Pd, P_st, mask, stream=None):
+    _check(load().echo_dot_softmax_fwd(ctypes.byref(d), _p(S), _p(Pd), _p(P_st), _p(mask), _stream(stream)))
+
+
+def echo_dot_softmax_bwd(d, S, P_st, mask, dPd, dS, Pd_regen, stream=None):
+    _check(load().echo_dot_softmax_bwd(ctypes.byref(d), _p(S), _p(P_st), _p(mask), _p(dPd), _p(dS), _p(Pd_regen),
+                                       _stream(stream)))
+
+
+# ---------------------------------------------------------------- footprint estimator (host)
+def echo_footprint_estimate(graph_json: str, config_json: str | None = None) -> str:
+    lib = load()
+    g = graph_json.encode()
+    c = config_json.encode() if config_json is not None else None
+    n = ctypes.c_size_t(0)
+    st = lib.echo_footprint_estimate(g, c, None, ctypes.byref(n))
+    if st not in (ECHO_OK, ECHO_ERR_CAPACITY):
+        _check(st)
+    buf = ctypes.create_string_buffer(n.value)
+    _check(lib.echo_footprint_estimate(g, c, buf, ctypes.byref(n)))
+    return buf.value.decode()

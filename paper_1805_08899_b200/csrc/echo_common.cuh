@@ -1,0 +1,113 @@
+// echo_common.cuh — shared device helpers for libecho (sm_100a).
+//
+// Storage-type abstraction (fp32 / bf16 storage, fp32 math), 128-bit vector
+// load/store, the rounding contract (DESIGN.md a4: round once at production,
+// every consumer reads the rounded value) and status plumbing.
+//
+// Bit-identity between STASH and RECOMPUTE rests on the device functions in
+// this file and in the kernels being *the same code with the same operation
+// order*; every floating-point step that could be contracted or reassociated
+// is written with explicit round-to-nearest intrinsics (__fmaf_rn, __fmul_rn,
+// __fadd_rn, __fdiv_rn), so nvcc cannot contract the two paths differently.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/echo.h"
+
+namespace echo {
+
+// ------------------------------------------------------------------ status plumbing
+void set_error(const char* fmt, ...);
+echo_status fail(echo_status s, const char* fmt, ...);
+echo_status check_launch(const char* what);
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------------ storage types
+template <typename T> struct St;
+template <> struct St<float> {
+  static constexpr int VEC = 4;                      // elements per 16-byte vector
+  __device__ static __forceinline__ float round(float x) { return x; }
+};
+template <> struct St<__nv_bfloat16> {
+  static constexpr int VEC = 8;
+  __device__ static __forceinline__ float round(float x) {
+    return __bfloat162float(__float2bfloat16_rn(x));
+  }
+};
+
+// 16-byte vector load of storage T -> VEC floats
+__device__ __forceinline__ void ld16(const float* p, float (&o)[4]) {
+  float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void ld16(const __nv_bfloat16* p, float (&o)[8]) {
+  uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x; o[2 * i + 1] = f.y;
+  }
+}
+// streaming (read-once) variant: bypass L1 allocation
+__device__ __forceinline__ void ld16_stream(const float* p, float (&o)[4]) {
+  float4 v = __ldcs(reinterpret_cast<const float4*>(p));
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void ld16_stream(const __nv_bfloat16* p, float (&o)[8]) {
+  uint4 v = __ldcs(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x; o[2 * i + 1] = f.y;
+  }
+}
+// store VEC floats (already rounded to T) as storage T
+__device__ __forceinline__ void st16(float* p, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void st16(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+// fp32 arrays of N = 4 or 8 floats (c, dc, dh are always fp32)
+template <int N>
+__device__ __forceinline__ void ldf(const float* p, float (&o)[N]) {
+#pragma unroll
+  for (int k = 0; k < N; k += 4) {
+    float4 v = *reinterpret_cast<const float4*>(p + k);
+    o[k] = v.x; o[k + 1] = v.y; o[k + 2] = v.z; o[k + 3] = v.w;
+  }
+}
+template <int N>
+__device__ __forceinline__ void stf(float* p, const float (&v)[N]) {
+#pragma unroll
+  for (int k = 0; k < N; k += 4) *reinterpret_cast<float4*>(p + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+}
+
+// ------------------------------------------------------------------ math (IEEE, no fast-math)
+__device__ __forceinline__ float sigmoidf_(float x) {
+  return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+}
+
+// warp-wide sum with a fixed xor tree (deterministic, identical in every kernel)
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace echo

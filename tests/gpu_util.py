@@ -1,0 +1,37 @@
+"""Helpers for GPU parity tests (test infrastructure)."""
+import numpy as np
+import torch
+
+TOL = {"fp32": 1e-4, "bf16": 2e-2}     # north_star: max relative error (reading R14: inf-norm relative)
+
+
+def dev(x, storage="fp32", dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    if dtype is not None:
+        return t.to(device="cuda", dtype=dtype)
+    if t.dtype in (torch.int64, torch.int32):
+        return t.cuda()
+    return t.to(device="cuda", dtype=torch.bfloat16 if storage == "bf16" else torch.float32)
+
+
+def host(t):
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+def relerr(x, y):
+    """max_i |x_i - y_i| / max_i |y_i|  (reading R14)."""
+    x = np.asarray(x, np.float64)
+    y = np.asarray(y, np.float64)
+    den = np.abs(y).max()
+    return float(np.abs(x - y).max() / (den if den > 0 else 1.0))
+
+
+def assert_close(x, y, storage, what=""):
+    e = relerr(x, y)
+    assert e <= TOL[storage], f"{what}: rel err {e:.3e} > {TOL[storage]}"
+    return e
+
+
+def bits_equal(a, b):
+    return torch.equal(a.contiguous().view(torch.uint8) if a.dtype != torch.bool else a,
+                       b.contiguous().view(torch.uint8) if b.dtype != torch.bool else b)

@@ -1,0 +1,115 @@
+"""GPU parity of MLP attention (a5/a6) and dot softmax+dropout (a7) vs the fp64 oracle,
+plus STASH == RECOMPUTE bit-identity."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention as OA
+from oracle import dot_softmax as OD
+from synth.data import mlp_attn_inputs, dot_softmax_inputs
+from tests.gpu_util import dev, host, assert_close, bits_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def _abi():
+    from paper_1805_08899_b200 import abi
+    abi.load()
+    return abi
+
+
+def _run_attn(abi, d, storage, mode, layout):
+    B, Ts, A = d["Kp"].shape
+    Hk = d["Hs"].shape[2]
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    if layout == "bsk":
+        Kp, Hs = dev(d["Kp"], storage), dev(d["Hs"], storage)
+        desc = abi.AttnDesc(B, Ts, A, Hk, dt, mode, Ts * A, A, Ts * Hk, Hk)
+    else:  # s-major [Ts, B, *] as produced by the encoder
+        Kp = dev(d["Kp"].transpose(1, 0, 2), storage)
+        Hs = dev(d["Hs"].transpose(1, 0, 2), storage)
+        desc = abi.AttnDesc(B, Ts, A, Hk, dt, mode, A, B * A, Hk, B * Hk)
+    qp, v = dev(d["qp"], storage), dev(d["v"], storage)
+    sl = torch.from_numpy(d["src_len"]).cuda()
+    ctx = torch.empty(B, Hk, device="cuda", dtype=qp.dtype)
+    E = torch.empty(B, Ts, A, device="cuda", dtype=qp.dtype) if mode == abi.STASH else None
+    al = torch.empty(B, Ts, device="cuda") if mode == abi.STASH else None
+    abi.echo_attn_fwd(desc, qp, Kp, v, Hs, sl, ctx, E, al)
+    dctx = dev(d["dctx"], dtype=torch.float32)
+    dqp = torch.empty(B, A, device="cuda")
+    dKp = torch.zeros_like(Kp, dtype=torch.float32)
+    dHs = torch.zeros_like(Hs, dtype=torch.float32)
+    dvp = torch.zeros(B, A, device="cuda")
+    creg = torch.empty_like(ctx) if mode == abi.RECOMPUTE else None
+    abi.echo_attn_bwd(desc, qp, Kp, v, Hs, sl, E, al, dctx, dqp, dKp, dHs, dvp, creg)
+    dv = torch.empty(A, device="cuda")
+    abi.echo_attn_dv_reduce(B, A, dvp, dv, 0)
+    if layout != "bsk":
+        dKp = dKp.transpose(0, 1)
+        dHs = dHs.transpose(0, 1)
+    return {"ctx": ctx, "E": E, "alpha": al, "dqp": dqp, "dKp": dKp.contiguous(), "dHs": dHs.contiguous(), "dv": dv,
+            "ctx_regen": creg}
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("B,Ts,A,Hk,layout", [(2, 4, 16, 16, "bsk"), (5, 37, 64, 48, "bsk"), (7, 29, 40, 88, "sbk"),
+                                               (128, 50, 512, 512, "sbk"), (3, 700, 256, 64, "bsk")])
+def test_attention_parity_and_bit_identity(storage, B, Ts, A, Hk, layout, cuda_dev):
+    abi = _abi()
+    d = mlp_attn_inputs(31, B, Ts, A, Hk, storage, lengths="random")
+    ref = OA.backward(*(np.asarray(d[k], np.float64) for k in ("qp", "Kp", "v", "Hs", "dctx")), src_len=d["src_len"])
+    res = {m: _run_attn(abi, d, storage, m, layout) for m in (abi.STASH, abi.RECOMPUTE)}
+    for m, r in res.items():
+        assert_close(host(r["ctx"]), ref["ctx"], storage, "ctx")
+        for k in ("dqp", "dKp", "dHs", "dv"):
+            assert_close(host(r[k]), ref[k], storage, k)
+    s, r = res[abi.STASH], res[abi.RECOMPUTE]
+    assert_close(host(s["alpha"]), ref["alpha"], storage, "alpha")
+    assert_close(host(s["E"]), ref["E"], storage, "E")
+    assert bits_equal(r["ctx_regen"], r["ctx"])
+    assert bits_equal(s["ctx"], r["ctx"])
+    for k in ("dqp", "dKp", "dHs", "dv"):
+        assert bits_equal(s[k], r[k]), k
+
+
+def test_attention_masked_rows_untouched(cuda_dev):
+    abi = _abi()
+    d = mlp_attn_inputs(5, 4, 9, 16, 16, lengths="random")
+    d["src_len"][:] = [9, 1, 3, 5]
+    r = _run_attn(abi, d, "fp32", abi.RECOMPUTE, "bsk")
+    for b, n in enumerate(d["src_len"]):
+        assert torch.all(r["dKp"][b, n:] == 0) and torch.all(r["dHs"][b, n:] == 0)
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("R,L,p", [(13, 264, 0.1), (64, 256, 0.1), (5, 8, 0.0), (9, 1032, 0.3), (2048, 256, 0.1)])
+def test_dot_softmax_dropout(storage, R, L, p, cuda_dev):
+    abi = _abi()
+    d = dot_softmax_inputs(41, R, L, storage)
+    seed, off, scale = 0x1234_5678_9ABC, 1000, 1.0 / np.sqrt(64)
+    keep = OD.dropout_keep_mask(seed, off, R * L, p).reshape(R, L)
+    ref = OD.backward(np.asarray(d["S"], np.float64), scale, keep, p, np.asarray(d["dPd"], np.float64))
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    S, dPd = dev(d["S"], storage), dev(d["dPd"], storage)
+    out = {}
+    for m in (abi.STASH, abi.RECOMPUTE):
+        desc = abi.DotDesc(R, L, dt, m, scale, p, seed, off)
+        Pd = torch.empty_like(S)
+        P = torch.empty_like(S) if m == abi.STASH else None
+        mask = torch.empty(R * L if m == abi.STASH else R * L // 8, dtype=torch.uint8, device="cuda")
+        abi.echo_dot_softmax_fwd(desc, S, Pd, P, mask)
+        dS = torch.empty_like(S)
+        Pdr = torch.empty_like(S) if m == abi.RECOMPUTE else None
+        abi.echo_dot_softmax_bwd(desc, S if m == abi.RECOMPUTE else None, P, mask, dPd, dS, Pdr)
+        out[m] = (Pd, mask, dS, Pdr, P)
+        assert_close(host(Pd), ref["Pd"], storage, "Pd")
+        assert_close(host(dS), ref["dS"], storage, "dS")
+    # the keep-mask is integer work: bit-exact against the oracle's Philox
+    sm = out[abi.STASH][1].cpu().numpy().reshape(R, L).astype(bool)
+    assert np.array_equal(sm, keep)
+    bm = np.unpackbits(out[abi.RECOMPUTE][1].cpu().numpy(), bitorder="little").reshape(R, L).astype(bool)
+    assert np.array_equal(bm, keep)
+    assert bits_equal(out[abi.STASH][0], out[abi.RECOMPUTE][0])
+    assert bits_equal(out[abi.STASH][2], out[abi.RECOMPUTE][2])
+    assert bits_equal(out[abi.RECOMPUTE][3], out[abi.RECOMPUTE][0])
+    assert_close(host(out[abi.STASH][4]), ref["P"], storage, "P")
