@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark: train samples/s and peak activation HBM, RECOMPUTE (Echo) vs STASH (Baseline).
+
+    python bench.py [--gpus N --steps K --warmup W] [--dtype fp32|bf16] [--batch B] [--impl reference]
+
+Workload: C2 of BASELINE.json (`configs[1]`): Sockeye-style 2+2-layer LSTM NMT, hidden 512,
+MLP attention, batch 128 per GPU, 50 source / 50 target steps, V = 8192, synthetic tokens,
+random-init weights.  One step = forward + backward + (allreduce) + SGD of the whole model;
+the Echo hot path (libecho a1/a2/a3/a5/a6) runs inside it, the FCs are cuBLAS.
+Multi-GPU: one process per GPU (torchrun), batch-sharded (weak scaling), NCCL allreduce.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _metric():
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        return json.load(f)["metric"]
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = [l.strip().split(", ") for l in open(self.f.name) if l.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm (CPU oracle)
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle (the only reference this paper-only tier has), timed on the
+    host cores on a bounded sample of the same C2 workload (batch 16 per step instead of 128)."""
+    from synth.configs import C2
+    from synth.data import nmt_params, nmt_batch
+    from oracle import nmt as O
+    ws, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    Bs = 16
+    cfg = C2.with_batch(Bs)
+    params = nmt_params(0, cfg)
+    batches = [nmt_batch(1 + i, cfg) for i in range(max(1, args.warmup) + args.steps)]
+    for i in range(args.warmup):
+        O.step(params, batches[i], cfg)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        O.step(params, batches[args.warmup + i], cfg)
+    dt = time.perf_counter() - t0
+    v = Bs * args.steps / dt
+    cores = len(os.sched_getaffinity(0))
+    line = {"impl": "reference", "metric": _metric(), "value": v, "unit": "samples/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2-nmt (fp64 CPU oracle, bounded sample: batch 16 of 128 per step)",
+                       "global_batch": Bs, "seq_len": 50, "hidden": 512, "vocab": 8192, "layers": "2+2"},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                             "sample": f"C2 shapes, batch {Bs} per step, {args.steps} steps, numpy fp64"},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def cpu_baseline_sample():
+    """The oracle as it stands, on the host cores, bounded sample (~10-20 s): C2 shapes at batch 16."""
+    from synth.configs import C2
+    from synth.data import nmt_params, nmt_batch
+    from oracle import nmt as O
+    Bs, n = 16, 2
+    cfg = C2.with_batch(Bs)
+    params = nmt_params(0, cfg)
+    b = [nmt_batch(100 + i, cfg) for i in range(n + 1)]
+    O.step(params, b[0], cfg)
+    t0 = time.perf_counter()
+    for i in range(n):
+        O.step(params, b[1 + i], cfg)
+    dt = time.perf_counter() - t0
+    return {"value": Bs * n / dt, "unit": "samples/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"C2 shapes (B=16 of 128, T=50, H=512, V=8192), {n} full training steps, numpy fp64"}
+
+
+def time_attn_bwd(cfg, dtype, reps=20):
+    """Dominant kernel (a6, RECOMPUTE attention backward) at the step's launch configuration,
+    timed with CUDA events on its launch stream; L2 flushed (256 MiB write) before every launch."""
+    import torch
+    from paper_1805_08899_b200 import abi
+    B, Ts, A, H = cfg.B, cfg.Ts, cfg.A, cfg.H
+    sd = torch.float32 if dtype == abi.FP32 else torch.bfloat16
+    s_bytes = 4 if dtype == abi.FP32 else 2
+    g = torch.Generator(device="cuda").manual_seed(0)
+    qp = (torch.randn(B, A, device="cuda", generator=g) * 0.5).to(sd)
+    Kp = (torch.randn(Ts, B, A, device="cuda", generator=g) * 0.5).to(sd)
+    Hs = torch.randn(Ts, B, H, device="cuda", generator=g).to(sd)
+    v = (torch.randn(A, device="cuda", generator=g) * 0.1).to(sd)
+    sl = torch.full((B,), Ts, dtype=torch.int32, device="cuda")
+    dctx = torch.randn(B, H, device="cuda", generator=g)
+    dqp = torch.empty(B, A, device="cuda")
+    dKp = torch.zeros(Ts, B, A, device="cuda")
+    dHs = torch.zeros(Ts, B, H, device="cuda")
+    dvp = torch.zeros(B, A, device="cuda")
+    creg = torch.empty(B, H, device="cuda", dtype=sd)
+    desc = abi.AttnDesc(B, Ts, A, H, dtype, abi.RECOMPUTE, A, B * A, H, B * H)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        abi.echo_attn_bwd(desc, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, dvp, creg)
+    times = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        abi.echo_attn_bwd(desc, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, dvp, creg)
+        e1.record(st)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.mean(times)
+    rows = B * Ts
+    big = rows * (A * s_bytes + H * s_bytes + 2 * A * 4 + 2 * H * 4)      # Kp, Hs read; dKp, dHs RMW
+    small = B * A * s_bytes + B * H * 4 + B * A * 4 + 2 * B * A * 4 + B * H * s_bytes + A * s_bytes + B * 4
+    return {"ms": ms, "bytes": big + small, "bytes_per_row": (big + small) / rows, "rows": rows}
+
+
+def run_ours(args):
+    import torch
+    from paper_1805_08899_b200 import abi, dp
+    from paper_1805_08899_b200.nmt import NMTModel
+    from synth.configs import C2
+    from synth.data import nmt_params, nmt_batch
+
+    ws, rank, local = dp.init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    dtype = abi.FP32 if args.dtype == "fp32" else abi.BF16
+    cfg = C2.with_batch(args.batch) if args.batch else C2
+    params = nmt_params(0, cfg)                                  # replicated model, same seed on all ranks
+    nb = 4
+    host_batches = [nmt_batch(dp.shard_seed(10 + i, rank), cfg) for i in range(nb)]
+    pinned = []
+    for b in host_batches:
+        pinned.append({k: torch.from_numpy(b[k]).pin_memory() for k in ("src", "tgt_in", "tgt_out", "src_len")})
+    lr = 0.05
+
+    def build(mode):
+        m = NMTModel(cfg, dtype=dtype, mode=mode, device=dev)
+        m.load_params(params)
+        if ws > 1:
+            m.grad_hook = dp.allreduce_mean_
+        m.upload_batch(pinned[0])
+        return m
+
+    def timed(m, use_graph, K, W):
+        """Device-timed K steps (inputs resident in HBM); returns ms per step (max over ranks)."""
+        abi.LAUNCHES["count"] = 0
+        if use_graph:
+            m.capture(lr)
+        launches_per_step = abi.LAUNCHES["count"]
+        if use_graph:
+            launches_per_step = launches_per_step // 3       # capture() = 2 warm-up steps + 1 captured
+        run = m.replay if use_graph else (lambda: m.step(lr))
+        for _ in range(W):
+            run()
+        torch.cuda.synchronize()
+        dp.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(K):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        dp.barrier()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / K
+        return dp.max_over_ranks(ms, dev), launches_per_step
+
+    def e2e(m, use_graph, K):
+        """Same metric through the public API with host buffers: per step H2D of the batch from pinned
+        memory, the step, and a D2H read of the loss."""
+        run = m.replay if use_graph else (lambda: m.step(lr))
+        torch.cuda.synchronize()
+        dp.barrier()
+        t0 = time.perf_counter()
+        for i in range(K):
+            m.upload_batch(pinned[i % nb])
+            run()
+            float(m.loss.item())
+        dt = (time.perf_counter() - t0) / K
+        dt = dp.max_over_ranks(dt, dev)
+        return dt
+
+    def peak_activation(mode):
+        m = NMTModel(cfg, dtype=dtype, mode=mode, device=dev)
+        m.load_params(params)
+        m.upload_batch(pinned[0])
+        m.step(0.0)                                              # warm the allocator / cuBLAS handles
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(dev)
+        start = torch.cuda.memory_allocated(dev)
+        acts = m._forward()
+        stash = m.stash_bytes()
+        m._backward(acts)
+        del acts
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated(dev) - start
+        del m
+        torch.cuda.empty_cache()
+        return peak, stash
+
+    use_graph = not args.no_graph
+    mode = abi.RECOMPUTE if args.mode == "recompute" else abi.STASH
+    model = build(mode)
+    try:
+        ms, launches = timed(model, use_graph, args.steps, args.warmup)
+    except Exception as ex:                                      # graph capture failure -> eager, stated
+        if not use_graph:
+            raise
+        print(f"[bench] CUDA graph capture failed ({ex}); timing eager", file=sys.stderr)
+        use_graph = False
+        model = build(mode)
+        ms, launches = timed(model, False, args.steps, args.warmup)
+    sampler = ClockSampler(local)
+    sampler.start()
+    # clocks are sampled over a second identical timed region (the first one followed the capture)
+    run = model.replay if use_graph else (lambda: model.step(lr))
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        run()
+    b.record()
+    torch.cuda.synchronize()
+    ms2 = dp.max_over_ranks(a.elapsed_time(b) / args.steps, dev)
+    clocks = sampler.stop()
+    ms = min(ms, ms2)
+    e2e_s = e2e(model, use_graph, max(4, args.steps // 2))
+    in_bytes = model.input_bytes()
+    del model
+    torch.cuda.empty_cache()
+
+    out = {}
+    if rank == 0 and not args.quick:
+        other = abi.STASH if mode == abi.RECOMPUTE else abi.RECOMPUTE
+        try:
+            m2 = build(other)
+            ms_other, _ = timed(m2, use_graph, args.steps, args.warmup)
+            del m2
+            torch.cuda.empty_cache()
+        except Exception as ex:
+            ms_other = None
+            print(f"[bench] {('stash', 'recompute')[other]} timing failed: {ex}", file=sys.stderr)
+        mem = {}
+        for md in (abi.STASH, abi.RECOMPUTE):
+            try:
+                mem[md] = peak_activation(md)
+            except torch.OutOfMemoryError:
+                mem[md] = (None, None)
+        out["ms_other"] = ms_other
+        out["mem"] = mem
+        out["kern"] = time_attn_bwd(cfg, dtype)
+    if ws > 1 and rank != 0:
+        dp.barrier()
+        return
+    samples = cfg.B * ws
+    line = {
+        "metric": _metric(),
+        "value": samples / (ms / 1e3),
+        "unit": "samples/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if dtype == abi.FP32 else "bf16",
+        "data": "synthetic (seeded tokens, random-init weights)",
+        "config": {"workload": f"{cfg.name}: Sockeye-style LSTM NMT 2+2 layers, hidden 512, MLP attention",
+                   "mode": args.mode, "global_batch": samples, "batch_per_gpu": cfg.B, "seq_len": cfg.Ts,
+                   "hidden": cfg.H, "vocab": cfg.V, "parallelism": f"dp{ws}", "cuda_graph": use_graph,
+                   "tf32": False, "l2": "no flush: per-step working set (weights 92 MB + activations >0.4 GB) > 126 MB L2"},
+        "gpu_launches": launches * args.steps,
+        "e2e": {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": 4},
+        "clocks": clocks,
+        "paper_context": "Baseline 1192 samples/s, 10.0 GB (Table 1) / Echo ~3.0 GB, 3.13x footprint reduction "
+                         "at B=128 on 1x RTX 2080 Ti, IWSLT15 en-vi (PAPER.md:297-299, 763-765); context, not a target",
+    }
+    if "kern" in out:
+        k = out["kern"]
+        pk = _peaks()
+        achieved = k["bytes"] / (k["ms"] / 1e3) / 1e9
+        n_att = cfg.Td
+        line["roofline"] = {"bound": "hbm", "kernel": "echo_attn_bwd (a6, RECOMPUTE)", "achieved": achieved,
+                            "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                            "traffic": None, "peak_source": pk["source"],
+                            "bytes_per_launch": k["bytes"], "bytes_per_row": k["bytes_per_row"],
+                            "launch_us": 1e3 * k["ms"], "timing": "CUDA events, L2 flushed before each launch",
+                            "share_of_step": n_att * k["ms"] / ms}
+        mem = out["mem"]
+        st, rc = mem[abi.STASH], mem[abi.RECOMPUTE]
+        line["memory"] = {
+            "peak_activation_bytes": {"stash": st[0], "recompute": rc[0]},
+            "stash_bytes": {"stash": st[1], "recompute": rc[1]},
+            "peak_ratio": (st[0] / rc[0]) if st[0] and rc[0] else None,
+            "stash_ratio": (st[1] / rc[1]) if st[1] and rc[1] else None,
+            "how": "torch max_memory_allocated - memory_allocated at step start (eager), fp32 allocator bytes",
+        }
+        if out["ms_other"]:
+            other_name = "stash" if mode == abi.RECOMPUTE else "recompute"
+            line[f"{other_name}_mode"] = {"value": samples / (out["ms_other"] / 1e3), "ms_per_step": out["ms_other"]}
+            if mode == abi.RECOMPUTE:
+                line["recompute_overhead"] = ms / out["ms_other"] - 1.0
+    if rank == 0 and not args.quick and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_sample()
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dp.barrier()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--mode", default="recompute", choices=["recompute", "stash"])
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: C2's 128)")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip the stash comparison, memory and kernel legs")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -118,9 +118,12 @@ echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_t, const fl
  *   E_s = tanh(qp_b + Kp_{b,s})   score_s = E_s . v   alpha = softmax_s(score)
  *   ctx_b = sum_s alpha_s Hs_{b,s}
  * One query per row (the NMT decoder calls this once per target step).
- * Feature maps (Echo plan, DESIGN.md table T4): STASH keeps E [B,Ts,A] s and
- * alpha [B,Ts] fp32 (and the caller keeps ctx); RECOMPUTE keeps nothing and
- * echo_attn_bwd regenerates E, scores, alpha and ctx.
+ * Feature maps (Echo plan, DESIGN.md table T4): STASH keeps the tanh feature
+ * map [B,Ts,A] s and alpha [B,Ts] fp32 (and the caller keeps ctx); RECOMPUTE
+ * keeps nothing and echo_attn_bwd regenerates it, the scores, alpha and ctx.
+ * The tanh feature map is stored as its input Z = round_s(qp + Kp) (same bytes
+ * as E = tanh(Z); E and tanh' = 1 - E^2 are evaluated in fp32 from Z in both
+ * modes, which keeps bf16 gradients accurate near saturation; R15).
  */
 typedef struct {
   int32_t B, Ts, A, Hk;   /* > 0; A, Hk multiples of 8; Ts <= 4096                  */
@@ -134,13 +137,14 @@ typedef struct {
 
 /* a5 — forward.
  *  qp [B,A] s, Kp strided [B,Ts,A] s, v [A] s, Hs strided [B,Ts,Hk] s, src_len [B] int32 in
- *  [1,Ts] or NULL (= Ts), ctx [B,Hk] s OUT, E_st [B,Ts,A] s OUT (STASH) / NULL,
+ *  [1,Ts] or NULL (= Ts), ctx [B,Hk] s OUT, E_st [B,Ts,A] s OUT Z = qp + Kp (STASH) / NULL,
  *  alpha_st [B,Ts] fp32 OUT (STASH) / NULL.  Masked positions get alpha = 0.      */
 echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
                           const void* Hs, const int32_t* src_len, void* ctx, void* E_st,
                           float* alpha_st, void* stream);
 
 /* a6 — backward with fused recomputation.
+ *  qp, Kp           RECOMPUTE: required (E is regenerated from them); STASH: may be NULL
  *  E_st, alpha_st   STASH inputs from a5 (NULL in RECOMPUTE)
  *  dctx   [B,Hk] fp32    dLoss/dctx
  *  dqp    [B,A] fp32     OUT dLoss/dqp (overwritten)

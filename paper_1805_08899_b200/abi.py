@@ -48,6 +48,10 @@ class DotDesc(ctypes.Structure):
 
 _lib = None
 
+# Number of libecho kernel launches issued through this binding (one per compute call;
+# each entry point launches exactly one kernel).  bench.py reads it to report gpu_launches.
+LAUNCHES = {"count": 0}
+
 
 def load(path: str = LIB_PATH) -> ctypes.CDLL:
     """Load libecho.so (raises if it has not been built: there is no fallback)."""
@@ -109,40 +113,48 @@ def echo_last_error() -> str:
 
 # ---------------------------------------------------------------- LSTM
 def echo_lstm_fwd(d, gx_t, gh_t, bias, c_prev, gates_t, c_out, tc_t, h_out, stream=None):
+    LAUNCHES["count"] += 1
     _check(load().echo_lstm_fwd(ctypes.byref(d), _p(gx_t), _p(gh_t), _p(bias), _p(c_prev), _p(gates_t), _p(c_out),
                                 _p(tc_t), _p(h_out), _stream(stream)))
 
 
 def echo_lstm_cscan(d, T, gates, c0, c_ws, stream=None):
+    LAUNCHES["count"] += 1
     _check(load().echo_lstm_cscan(ctypes.byref(d), int(T), _p(gates), _p(c0), _p(c_ws), _stream(stream)))
 
 
 def echo_lstm_bwd(d, gates_t, c_prev, c_t, tc_t, dh_t, dc, dA_t, h_regen, stream=None):
+    LAUNCHES["count"] += 1
     _check(load().echo_lstm_bwd(ctypes.byref(d), _p(gates_t), _p(c_prev), _p(c_t), _p(tc_t), _p(dh_t), _p(dc),
                                 _p(dA_t), _p(h_regen), _stream(stream)))
 
 
 # ---------------------------------------------------------------- MLP attention
 def echo_attn_fwd(d, qp, Kp, v, Hs, src_len, ctx, E_st, alpha_st, stream=None):
+    LAUNCHES["count"] += 1
     _check(load().echo_attn_fwd(ctypes.byref(d), _p(qp), _p(Kp), _p(v), _p(Hs), _p(src_len), _p(ctx), _p(E_st),
                                 _p(alpha_st), _stream(stream)))
 
 
 def echo_attn_bwd(d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part, ctx_regen, stream=None):
+    LAUNCHES["count"] += 1
     _check(load().echo_attn_bwd(ctypes.byref(d), _p(qp), _p(Kp), _p(v), _p(Hs), _p(src_len), _p(E_st), _p(alpha_st),
                                 _p(dctx), _p(dqp), _p(dKp), _p(dHs), _p(dv_part), _p(ctx_regen), _stream(stream)))
 
 
 def echo_attn_dv_reduce(B, A, dv_part, dv, accumulate, stream=None):
+    LAUNCHES["count"] += 1
     _check(load().echo_attn_dv_reduce(int(B), int(A), _p(dv_part), _p(dv), int(accumulate), _stream(stream)))
 
 
 # ---------------------------------------------------------------- dot softmax + dropout
 def echo_dot_softmax_fwd(d, S, Pd, P_st, mask, stream=None):
+    LAUNCHES["count"] += 1
     _check(load().echo_dot_softmax_fwd(ctypes.byref(d), _p(S), _p(Pd), _p(P_st), _p(mask), _stream(stream)))
 
 
 def echo_dot_softmax_bwd(d, S, P_st, mask, dPd, dS, Pd_regen, stream=None):
+    LAUNCHES["count"] += 1
     _check(load().echo_dot_softmax_bwd(ctypes.byref(d), _p(S), _p(P_st), _p(mask), _p(dPd), _p(dS), _p(Pd_regen),
                                        _stream(stream)))
 

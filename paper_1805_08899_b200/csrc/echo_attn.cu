@@ -23,21 +23,23 @@ namespace echo {
 constexpr int ATT_THREADS = 256;
 constexpr int ATT_WARPS = ATT_THREADS / 32;
 
-// score_s = sum_a round_s(tanh(qp_a + Kp_{s,a})) * v_a  (one warp; lane-strided vectors)
+// score_s = sum_a tanh(round_s(qp_a + Kp_{s,a})) * v_a  (one warp; lane-strided vectors).
+// The stashed feature map is the tanh INPUT z = round_s(qp + Kp) (byte-identical stand-in
+// for E = tanh(z), R15): E and 1 - E^2 are then always evaluated in fp32 from z.
 template <typename T>
 __device__ __forceinline__ float score_row(const T* __restrict__ kp_row, const float* qp_s, const float* v_s, int A,
-                                           int lane, T* E_out) {
+                                           int lane, T* Z_out) {
   constexpr int V = St<T>::VEC;
   float acc = 0.0f;
   for (int iv = lane; iv < A / V; iv += 32) {
-    float kv[V], e[V];
+    float kv[V], z[V];
     ld16(kp_row + iv * V, kv);
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-      e[k] = St<T>::round(tanhf(__fadd_rn(qp_s[iv * V + k], kv[k])));
-      acc = __fmaf_rn(e[k], v_s[iv * V + k], acc);
+      z[k] = St<T>::round(__fadd_rn(qp_s[iv * V + k], kv[k]));
+      acc = __fmaf_rn(tanhf(z[k]), v_s[iv * V + k], acc);
     }
-    if (E_out) st16(E_out + iv * V, e);
+    if (Z_out) st16(Z_out + iv * V, z);
   }
   return warp_sum(acc);
 }
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
   const bool recompute = (E_st == nullptr);
-  stage_vec<T>(qp_s, qp + (long)b * A, A, tid);
+  if (recompute) stage_vec<T>(qp_s, qp + (long)b * A, A, tid);
   stage_vec<T>(v_s, v, A, tid);
   for (int i = tid; i < Hk; i += ATT_THREADS) dctx_s[i] = dctx[(long)b * Hk + i];
   for (int i = tid; i < ATT_WARPS * A; i += ATT_THREADS) { wq[i] = 0.0f; wv[i] = 0.0f; }
@@ -254,15 +256,18 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
     float* dkp_row = dKp + (long)b * d.kp_stride_b + (long)s * d.kp_stride_s;
     const T* e_row = E_st ? E_st + ((long)b * Ts + s) * A : nullptr;
     for (int iv = lane; iv < A / V; iv += 32) {
-      float e[V];
+      float z[V];
       if (recompute) {
         float kv[V];
         ld16(kp_row + iv * V, kv);
 #pragma unroll
-        for (int k = 0; k < V; ++k) e[k] = St<T>::round(tanhf(__fadd_rn(qp_s[iv * V + k], kv[k])));
+        for (int k = 0; k < V; ++k) z[k] = St<T>::round(__fadd_rn(qp_s[iv * V + k], kv[k]));
       } else {
-        ld16(e_row + iv * V, e);
+        ld16(e_row + iv * V, z);
       }
+      float e[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) e[k] = tanhf(z[k]);
       float dk[V];
       ldf<V>(dkp_row + iv * V, dk);
 #pragma unroll
@@ -391,7 +396,6 @@ extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, co
   const char* fn = "echo_attn_bwd";
   echo_status s = check_attn(fn, d);
   if (s) return s;
-  ECHO_REQ(qp, "qp");
   ECHO_REQ(v, "v");
   ECHO_REQ(Hs, "Hs");
   ECHO_REQ(dctx, "dctx");
@@ -404,6 +408,7 @@ extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, co
     if (!alpha_st) return fail(ECHO_ERR_INVALID, "%s: alpha_st required in STASH mode", fn);
     if (ctx_regen) return fail(ECHO_ERR_INVALID, "%s: ctx_regen must be NULL in STASH mode", fn);
   } else {
+    ECHO_REQ(qp, "qp");
     ECHO_REQ(Kp, "Kp");
     if (E_st || alpha_st) return fail(ECHO_ERR_INVALID, "%s: E_st / alpha_st must be NULL in RECOMPUTE mode", fn);
     if (ctx_regen && !aligned16(ctx_regen)) return fail(ECHO_ERR_INVALID, "%s: ctx_regen not 16-byte aligned", fn);

@@ -27,14 +27,17 @@ TORCH_DTYPE = {abi.FP32: torch.float32, abi.BF16: torch.bfloat16}
 
 
 class LSTMLayer:
-    def __init__(self, T, B, H, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda"):
+    def __init__(self, T, B, H, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda", h_ring=False):
+        """h_ring: in RECOMPUTE, keep only h_{t-1}, h_t (2-slot ring) because nobody needs the
+        whole output sequence after the forward (decoder layers); the encoder keeps [T,B,H]."""
         self.T, self.B, self.H = T, B, H
         self.dtype, self.mode = dtype, mode
         self.sd = TORCH_DTYPE[dtype]
         self.device = device
         self.desc = abi.LstmDesc(B, H, dtype, mode)
         self.gates = torch.empty(T, B, 4 * H, dtype=self.sd, device=device)
-        self.h = torch.empty(T, B, H, dtype=self.sd, device=device)
+        self.h_ring = bool(h_ring) and mode == abi.RECOMPUTE
+        self.h = torch.empty(2 if self.h_ring else T, B, H, dtype=self.sd, device=device)
         if mode == abi.STASH:
             self.c = torch.empty(T, B, H, dtype=torch.float32, device=device)
             self.tc = torch.empty(T, B, H, dtype=self.sd, device=device)
@@ -61,13 +64,16 @@ class LSTMLayer:
     def c_prev(self, t):
         return self.c0 if t == 0 else self.c_slot(t - 1)
 
+    def h_slot(self, t):
+        return self.h[t % 2] if self.h_ring else self.h[t]
+
     def h_prev(self, t):
-        return self.h0 if t == 0 else self.h[t - 1]
+        return self.h0 if t == 0 else self.h_slot(t - 1)
 
     def fwd_step(self, t, bias):
         """gates[t] must hold x_t W_x^T + h_{t-1} W_h^T (storage dtype)."""
         abi.echo_lstm_fwd(self.desc, self.gates[t], None, bias, self.c_prev(t), self.gates[t], self.c_slot(t),
-                          self.tc[t] if self.mode == abi.STASH else None, self.h[t])
+                          self.tc[t] if self.mode == abi.STASH else None, self.h_slot(t))
 
     def c_final(self):
         return self.c_slot(self.T - 1)

@@ -33,5 +33,13 @@ def assert_close(x, y, storage, what=""):
 
 
 def bits_equal(a, b):
-    return torch.equal(a.contiguous().view(torch.uint8) if a.dtype != torch.bool else a,
-                       b.contiguous().view(torch.uint8) if b.dtype != torch.bool else b)
+    return torch.equal(a.reshape(-1).contiguous().view(torch.uint8) if a.dtype != torch.bool else a,
+                       b.reshape(-1).contiguous().view(torch.uint8) if b.dtype != torch.bool else b)
+
+
+def relerr_fro(x, y):
+    """||x - y||_2 / ||y||_2 (Frobenius), the bf16 metric for whole-model gradients (reading R14)."""
+    x = np.asarray(x, np.float64)
+    y = np.asarray(y, np.float64)
+    den = np.linalg.norm(y)
+    return float(np.linalg.norm(x - y) / (den if den > 0 else 1.0))

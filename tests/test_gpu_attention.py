@@ -65,7 +65,7 @@ def test_attention_parity_and_bit_identity(storage, B, Ts, A, Hk, layout, cuda_d
             assert_close(host(r[k]), ref[k], storage, k)
     s, r = res[abi.STASH], res[abi.RECOMPUTE]
     assert_close(host(s["alpha"]), ref["alpha"], storage, "alpha")
-    assert_close(host(s["E"]), ref["E"], storage, "E")
+    assert_close(np.tanh(host(s["E"])), ref["E"], storage, "tanh(Z)")   # stash holds Z = qp + Kp (R15)
     assert bits_equal(r["ctx_regen"], r["ctx"])
     assert bits_equal(s["ctx"], r["ctx"])
     for k in ("dqp", "dKp", "dHs", "dv"):
