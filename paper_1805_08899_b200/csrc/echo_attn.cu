@@ -5,20 +5,27 @@
 // largest stash of the NMT model; Echo keeps them mirrored and
 // regenerates them in the backward pass.
 //
-// Design: one CTA per batch row b (the rows are
-// independent; per-row work is a [Ts x A] + [Ts x Hk] stream).  Warp w owns
-// source positions s = w, w + NW, ...; a lane owns 16-byte vectors of the A /
-// Hk axis, so each warp-wide access is a coalesced 512-byte (fp32) row
-// segment.  Scores use a fixed-order per-lane FMA chain + fixed xor-shuffle
-// tree; the softmax and the context reduction are the SAME device functions
-// with the SAME thread mapping in the forward and backward kernels, which is
-// what makes the regenerated alpha / ctx bit-identical to the stashed ones.
-// dv is produced as per-row partials (no atomics) and reduced in fixed order.
+// Design: one thread-block CLUSTER of C CTAs per batch
+// row b (C in {1,2,4,8}, from Ts); CTA rank r owns the source positions
+// [r*chunk, (r+1)*chunk).  The softmax statistics (max, sum), the dot
+// sum_s alpha_s dalpha_s and the cross-position reductions (ctx, dqp, dv) are
+// combined across the cluster through distributed shared memory in ascending
+// rank order, so one row's Ts x (A + Hk) stream is spread over C SMs (B*C CTAs
+// per launch instead of B) without atomics.  Inside a CTA, warp w owns local
+// positions i = w, w + NW, ...; a lane owns 16-byte vectors of the A / Hk axis,
+// so each warp access is a coalesced 512-byte (fp32) row segment.  The score,
+// softmax and context code is the SAME device code with the SAME mapping in
+// the forward and backward kernels, which makes the regenerated alpha / ctx
+// bit-identical to the stashed ones.
 #include <cmath>
+
+#include <cooperative_groups.h>
 
 #include "echo_common.cuh"
 
 namespace echo {
+
+namespace cg = cooperative_groups;
 
 constexpr int ATT_THREADS = 256;
 constexpr int ATT_WARPS = ATT_THREADS / 32;
@@ -44,79 +51,18 @@ __device__ __forceinline__ float score_row(const T* __restrict__ kp_row, const f
   return warp_sum(acc);
 }
 
-// In-place: sc[0..n) scores -> alpha; sc[n..Ts) = 0.  Executed by ONE warp.
-__device__ __forceinline__ void softmax_warp(float* sc, int n, int Ts, int lane) {
-  float m = -INFINITY;
-  for (int s = lane; s < n; s += 32) m = fmaxf(m, sc[s]);
-  m = warp_max(m);
-  float sum = 0.0f;
-  for (int s = lane; s < n; s += 32) {
-    const float e = expf(__fsub_rn(sc[s], m));
-    sc[s] = e;
-    sum = __fadd_rn(sum, e);
-  }
-  sum = warp_sum(sum);
-  for (int s = lane; s < n; s += 32) sc[s] = __fdiv_rn(sc[s], sum);
-  for (int s = n + lane; s < Ts; s += 32) sc[s] = 0.0f;
-}
 
 __host__ __device__ __forceinline__ int ctx_groups(int Hk, int V) {
   const int ncols = Hk / V;
   return ncols >= ATT_THREADS ? 1 : ATT_THREADS / ncols;
 }
 
-// ctx = sum_{s<n} alpha_s Hs_s : G thread groups split s, fixed-order combine.
-template <typename T>
-__device__ __forceinline__ void context(const T* __restrict__ hs_b, long stride_s, const float* alpha, int n, int Hk,
-                                        float* part, T* ctx_out, int tid) {
-  constexpr int V = St<T>::VEC;
-  const int ncols = Hk / V;
-  const int G = ctx_groups(Hk, V);
-  if (G > 1) {
-    const int g = tid / ncols, cv = tid - (tid / ncols) * ncols;
-    if (g < G) {
-      float acc[V];
-#pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = 0.0f;
-      for (int s = g; s < n; s += G) {
-        float h[V];
-        ld16(hs_b + (long)s * stride_s + cv * V, h);
-        const float a = alpha[s];
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] = __fmaf_rn(a, h[k], acc[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < V; ++k) part[g * Hk + cv * V + k] = acc[k];
-    }
-  } else {
-    for (int cv = tid; cv < ncols; cv += ATT_THREADS) {
-      float acc[V];
-#pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = 0.0f;
-      for (int s = 0; s < n; ++s) {
-        float h[V];
-        ld16(hs_b + (long)s * stride_s + cv * V, h);
-        const float a = alpha[s];
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] = __fmaf_rn(a, h[k], acc[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < V; ++k) part[cv * V + k] = acc[k];
-    }
-  }
-  __syncthreads();
-  if (ctx_out) {
-    for (int cv = tid; cv < ncols; cv += ATT_THREADS) {
-      float r[V];
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        float x = part[cv * V + k];
-        for (int g = 1; g < G; ++g) x = __fadd_rn(x, part[g * Hk + cv * V + k]);
-        r[k] = St<T>::round(x);
-      }
-      st16(ctx_out + cv * V, r);
-    }
-  }
+// cluster size for a row of Ts positions: next power of two of ceil(Ts / 8), capped at 8
+static inline int att_cluster(int Ts) {
+  const int want = (Ts + 7) / 8;
+  int C = 1;
+  while (C < want && C < 8) C <<= 1;
+  return C;
 }
 
 template <typename T>
@@ -136,74 +82,237 @@ __device__ __forceinline__ int row_len(const int32_t* src_len, int b, int Ts) {
   return n < 1 ? 1 : (n > Ts ? Ts : n);
 }
 
+// Rank-ordered cluster reductions of one float per CTA; the C (<= 8) remote DSMEM loads are
+// issued back to back before the fixed-order combine.
+__device__ __forceinline__ float cl_sum(cg::cluster_group& cl, float* p, int C) {
+  float t[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) t[c] = c < C ? *cl.map_shared_rank(p, c) : 0.0f;
+  float x = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < C) x = __fadd_rn(x, t[c]);
+  return x;
+}
+
+// Softmax over the row, distributed over the cluster, with ONE cluster barrier: every CTA
+// publishes its local (max m_c, sum l_c = sum exp(score - m_c)); all CTAs then form the same
+// m = max_c m_c and L = sum_c l_c exp(m_c - m) in rank order.  sc[0..ns) holds this CTA's
+// scores on entry and alpha = exp(score - m) / L on exit.  Uses red[0], red[1].
+__device__ __forceinline__ void softmax_cluster(cg::cluster_group& cl, float* sc, int ns, float* red, int C,
+                                                int tid) {
+  const int lane = tid & 31, w = tid >> 5;
+  if (w == 0) {
+    float m = -INFINITY;
+    for (int i = lane; i < ns; i += 32) m = fmaxf(m, sc[i]);
+    m = warp_max(m);
+    float l = 0.0f;
+    for (int i = lane; i < ns; i += 32) l = __fadd_rn(l, expf(__fsub_rn(sc[i], m)));
+    l = warp_sum(l);
+    if (lane == 0) { red[0] = m; red[1] = l; }
+  }
+  cl.sync();
+  float mc[8], lc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    mc[c] = c < C ? *cl.map_shared_rank(red, c) : -INFINITY;
+    lc[c] = c < C ? *cl.map_shared_rank(red + 1, c) : 0.0f;
+  }
+  float m = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) m = fmaxf(m, mc[c]);
+  float L = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < C && lc[c] > 0.0f) L = __fadd_rn(L, __fmul_rn(lc[c], expf(__fsub_rn(mc[c], m))));
+  if (w == 0)
+    for (int i = lane; i < ns; i += 32) sc[i] = __fdiv_rn(expf(__fsub_rn(sc[i], m)), L);
+  __syncthreads();
+}
+
+// Rank r writes its slice of the Hk columns: out = round_s(sum_c xfer_c) in rank order.
+template <typename T>
+__device__ __forceinline__ void ctx_finish(cg::cluster_group& cl, float* xfer, int Hk, T* ctx_out, int C, int r,
+                                           int tid) {
+  constexpr int V = St<T>::VEC;
+  const int ncols = Hk / V;
+  const int per = (ncols + C - 1) / C;
+  const int c0 = r * per, c1 = min(ncols, c0 + per);
+  for (int cv = c0 + tid; cv < c1; cv += ATT_THREADS) {
+    float t[8][V];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < C) {
+        const float* q = cl.map_shared_rank(xfer, c) + cv * V;
+#pragma unroll
+        for (int k = 0; k < V; ++k) t[c][k] = q[k];
+      }
+    float o[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float x = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < C) x = __fadd_rn(x, t[c][k]);
+      o[k] = St<T>::round(x);
+    }
+    st16(ctx_out + cv * V, o);
+  }
+}
+
+// This CTA's part of ctx = sum_{s<n} alpha_s Hs_s: G thread groups split the local positions,
+// fixed-order combine into xfer[Hk].  The caller then cl.sync()s and runs ctx_finish.
+template <typename T>
+__device__ __forceinline__ void context_partial(const T* __restrict__ hs_b, long stride_s, const float* alpha, int s0,
+                                                int ns, int Hk, float* part, float* xfer, int tid) {
+  constexpr int V = St<T>::VEC;
+  const int ncols = Hk / V;
+  const int G = ctx_groups(Hk, V);
+  if (G > 1) {
+    const int g = tid / ncols, cv = tid - g * ncols;
+    if (g < G) {
+      float acc[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = 0.0f;
+      for (int i = g; i < ns; i += G) {
+        float h[V];
+        ld16(hs_b + (long)(s0 + i) * stride_s + cv * V, h);
+        const float a = alpha[i];
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = __fmaf_rn(a, h[k], acc[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) part[g * Hk + cv * V + k] = acc[k];
+    }
+  } else {
+    for (int cv = tid; cv < ncols; cv += ATT_THREADS) {
+      float acc[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = 0.0f;
+      for (int i = 0; i < ns; ++i) {
+        float h[V];
+        ld16(hs_b + (long)(s0 + i) * stride_s + cv * V, h);
+        const float a = alpha[i];
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = __fmaf_rn(a, h[k], acc[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) part[cv * V + k] = acc[k];
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < Hk; k += ATT_THREADS) {
+    float x = part[k];
+    for (int g = 1; g < G; ++g) x = __fadd_rn(x, part[g * Hk + k]);
+    xfer[k] = x;
+  }
+  __syncthreads();
+}
+
+// rank r finishes its slice of A: dqp = sum_c xq_c, dv_part += sum_c xv_c (rank order)
+__device__ __forceinline__ void dqp_dv_finish(cg::cluster_group& cl, float* xq, float* xv, int A, float* dqp_b,
+                                              float* dvp_b, int C, int r, int tid) {
+  const int per = (A + C - 1) / C;
+  for (int a = r * per + tid; a < min(A, (r + 1) * per); a += ATT_THREADS) {
+    float tq[8], tv[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < C) { tq[c] = cl.map_shared_rank(xq, c)[a]; tv[c] = cl.map_shared_rank(xv, c)[a]; }
+    float q = 0.0f, vv = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < C) { q = __fadd_rn(q, tq[c]); vv = __fadd_rn(vv, tv[c]); }
+    dqp_b[a] = q;
+    dvp_b[a] = __fadd_rn(dvp_b[a], vv);
+  }
+}
+
 // ---------------------------------------------------------------- a5 forward
 template <typename T>
-__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_kernel(echo_attn_desc d, const T* __restrict__ qp,
+__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_kernel(echo_attn_desc d, int chunk, const T* __restrict__ qp,
                                                                const T* __restrict__ Kp, const T* __restrict__ v,
                                                                const T* __restrict__ Hs,
                                                                const int32_t* __restrict__ src_len,
-                                                               T* __restrict__ ctx, T* __restrict__ E_st,
+                                                               T* __restrict__ ctx, T* __restrict__ Z_st,
                                                                float* __restrict__ alpha_st) {
+  constexpr int V = St<T>::VEC;
+  cg::cluster_group cl = cg::this_cluster();
   extern __shared__ float sm[];
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
+  const int C = (int)cl.num_blocks(), r = (int)cl.block_rank();
+  const int G = ctx_groups(Hk, V);
   float* qp_s = sm;
   float* v_s = qp_s + A;
-  float* sc = v_s + A;
-  float* part = sc + ((Ts + 3) & ~3);
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  float* red = v_s + A;                 // [4]
+  float* sc = red + 4;                  // [chunk]
+  float* part = sc + ((chunk + 3) & ~3);
+  float* xfer = part + G * Hk;
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
+  const int s0 = r * chunk;
+  const int ns = max(0, min(s0 + chunk, n) - s0);
+  const int send = min(s0 + chunk, Ts);
   stage_vec<T>(qp_s, qp + (long)b * A, A, tid);
   stage_vec<T>(v_s, v, A, tid);
   __syncthreads();
   const T* kp_b = Kp + (long)b * d.kp_stride_b;
-  for (int s = w; s < n; s += ATT_WARPS) {
-    T* e_out = E_st ? E_st + ((long)b * Ts + s) * A : nullptr;
-    const float scv = score_row<T>(kp_b + (long)s * d.kp_stride_s, qp_s, v_s, A, lane, e_out);
-    if (lane == 0) sc[s] = scv;
+  for (int i = w; i < ns; i += ATT_WARPS) {
+    T* z_out = Z_st ? Z_st + ((long)b * Ts + s0 + i) * A : nullptr;
+    const float scv = score_row<T>(kp_b + (long)(s0 + i) * d.kp_stride_s, qp_s, v_s, A, lane, z_out);
+    if (lane == 0) sc[i] = scv;
   }
-  if (E_st) {  // masked positions hold zeros (as the oracle's E)
-    constexpr int V = St<T>::VEC;
+  if (Z_st) {  // masked positions of this chunk hold zeros
     float z[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) z[k] = 0.0f;
-    for (int s = n + w; s < Ts; s += ATT_WARPS)
-      for (int iv = lane; iv < A / V; iv += 32) st16(E_st + ((long)b * Ts + s) * A + iv * V, z);
+    for (int s = max(s0, n) + w; s < send; s += ATT_WARPS)
+      for (int iv = lane; iv < A / V; iv += 32) st16(Z_st + ((long)b * Ts + s) * A + iv * V, z);
   }
   __syncthreads();
-  if (w == 0) softmax_warp(sc, n, Ts, lane);
-  __syncthreads();
+  softmax_cluster(cl, sc, ns, red, C, tid);
   if (alpha_st)
-    for (int s = tid; s < Ts; s += ATT_THREADS) alpha_st[(long)b * Ts + s] = sc[s];
-  context<T>(Hs + (long)b * d.hs_stride_b, d.hs_stride_s, sc, n, Hk, part, ctx + (long)b * Hk, tid);
+    for (int s = s0 + tid; s < send; s += ATT_THREADS) alpha_st[(long)b * Ts + s] = (s - s0 < ns) ? sc[s - s0] : 0.0f;
+  context_partial<T>(Hs + (long)b * d.hs_stride_b, d.hs_stride_s, sc, s0, ns, Hk, part, xfer, tid);
+  cl.sync();
+  ctx_finish<T>(cl, xfer, Hk, ctx + (long)b * Hk, C, r, tid);
+  cl.sync();
 }
 
 // ---------------------------------------------------------------- a6 backward (fused recompute)
 template <typename T>
-__global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d, const T* __restrict__ qp,
+__global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d, int chunk, const T* __restrict__ qp,
                                                                const T* __restrict__ Kp, const T* __restrict__ v,
                                                                const T* __restrict__ Hs,
                                                                const int32_t* __restrict__ src_len,
-                                                               const T* __restrict__ E_st,
+                                                               const T* __restrict__ Z_st,
                                                                const float* __restrict__ alpha_st,
                                                                const float* __restrict__ dctx, float* __restrict__ dqp,
                                                                float* __restrict__ dKp, float* __restrict__ dHs,
                                                                float* __restrict__ dv_part, T* __restrict__ ctx_regen) {
   constexpr int V = St<T>::VEC;
+  cg::cluster_group cl = cg::this_cluster();
   extern __shared__ float sm[];
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
-  const int Tp = (Ts + 3) & ~3;
+  const int C = (int)cl.num_blocks(), r = (int)cl.block_rank();
+  const int G = ctx_groups(Hk, V);
+  const int cp = (chunk + 3) & ~3;
   float* qp_s = sm;
   float* v_s = qp_s + A;
   float* dctx_s = v_s + A;
-  float* sc = dctx_s + Hk;           // scores -> alpha
-  float* dal = sc + Tp;              // dLoss/dalpha
-  float* red = dal + Tp;             // [0] = sum_s alpha_s dalpha_s
-  float* wq = red + 4;               // [NW][A] per-warp dqp partials
-  float* wv = wq + ATT_WARPS * A;    // [NW][A] per-warp dv partials
-  float* part = wv + ATT_WARPS * A;  // [G][Hk] context partials
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  float* red = dctx_s + Hk;             // [0] max [1] sum [2] dot
+  float* sc = red + 4;                  // [chunk] scores -> alpha
+  float* dal = sc + cp;                 // [chunk] dLoss/dalpha
+  float* wq = dal + cp;                 // [NW][A] per-warp dqp partials
+  float* wv = wq + ATT_WARPS * A;       // [NW][A] per-warp dv partials
+  float* xq = wv + ATT_WARPS * A;       // [A] CTA dqp partial
+  float* xv = xq + A;                   // [A] CTA dv partial
+  float* part = xv + A;                 // [G][Hk]
+  float* xfer = part + G * Hk;          // [Hk]
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
-  const bool recompute = (E_st == nullptr);
+  const int s0 = r * chunk;
+  const int ns = max(0, min(s0 + chunk, n) - s0);
+  const bool recompute = (Z_st == nullptr);
   if (recompute) stage_vec<T>(qp_s, qp + (long)b * A, A, tid);
   stage_vec<T>(v_s, v, A, tid);
   for (int i = tid; i < Hk; i += ATT_THREADS) dctx_s[i] = dctx[(long)b * Hk + i];
@@ -212,10 +321,11 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
   const T* kp_b = Kp + (long)b * d.kp_stride_b;
   const T* hs_b = Hs + (long)b * d.hs_stride_b;
   // phase 1: regenerate scores (RECOMPUTE) and dalpha_s = dctx . Hs_s
-  for (int s = w; s < n; s += ATT_WARPS) {
+  for (int i = w; i < ns; i += ATT_WARPS) {
+    const int s = s0 + i;
     if (recompute) {
       const float scv = score_row<T>(kp_b + (long)s * d.kp_stride_s, qp_s, v_s, A, lane, nullptr);
-      if (lane == 0) sc[s] = scv;
+      if (lane == 0) sc[i] = scv;
     }
     float acc = 0.0f;
     const T* hrow = hs_b + (long)s * d.hs_stride_s;
@@ -226,35 +336,37 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
       for (int k = 0; k < V; ++k) acc = __fmaf_rn(dctx_s[iv * V + k], h[k], acc);
     }
     acc = warp_sum(acc);
-    if (lane == 0) dal[s] = acc;
+    if (lane == 0) dal[i] = acc;
   }
   if (!recompute)
-    for (int s = tid; s < Ts; s += ATT_THREADS) sc[s] = alpha_st[(long)b * Ts + s];
+    for (int i = tid; i < ns; i += ATT_THREADS) sc[i] = alpha_st[(long)b * Ts + s0 + i];
   __syncthreads();
-  // phase 2: softmax (same device function as a5)
-  if (recompute && w == 0) softmax_warp(sc, n, Ts, lane);
-  __syncthreads();
-  // phase 3: regenerate ctx (same device function and mapping as a5)
-  if (recompute && ctx_regen) {
-    context<T>(hs_b, d.hs_stride_s, sc, n, Hk, part, ctx_regen + (long)b * Hk, tid);
+  // phase 2/3: softmax and ctx, the same device code as a5 (RECOMPUTE only)
+  const bool do_ctx = recompute && ctx_regen;
+  if (recompute) {
+    softmax_cluster(cl, sc, ns, red, C, tid);
+    if (do_ctx) context_partial<T>(hs_b, d.hs_stride_s, sc, s0, ns, Hk, part, xfer, tid);
   }
+  // dot = sum_s alpha_s dalpha_s, cluster-wide in rank order (same barrier as the ctx exchange)
   if (w == 0) {
     float acc = 0.0f;
-    for (int s = lane; s < n; s += 32) acc = __fmaf_rn(sc[s], dal[s], acc);
+    for (int i = lane; i < ns; i += 32) acc = __fmaf_rn(sc[i], dal[i], acc);
     acc = warp_sum(acc);
-    if (lane == 0) red[0] = acc;
+    if (lane == 0) red[2] = acc;
   }
-  __syncthreads();
-  const float dot = red[0];
+  cl.sync();
+  if (do_ctx) ctx_finish<T>(cl, xfer, Hk, ctx_regen + (long)b * Hk, C, r, tid);
+  const float dot = cl_sum(cl, red + 2, C);
   // phase 4: ds, dE, dKp +=, dHs +=, dqp / dv partials
   float* wq_w = wq + w * A;
   float* wv_w = wv + w * A;
-  for (int s = w; s < n; s += ATT_WARPS) {
-    const float al = sc[s];
-    const float ds = __fmul_rn(al, __fsub_rn(dal[s], dot));
+  for (int i = w; i < ns; i += ATT_WARPS) {
+    const int s = s0 + i;
+    const float al = sc[i];
+    const float ds = __fmul_rn(al, __fsub_rn(dal[i], dot));
     const T* kp_row = kp_b + (long)s * d.kp_stride_s;
     float* dkp_row = dKp + (long)b * d.kp_stride_b + (long)s * d.kp_stride_s;
-    const T* e_row = E_st ? E_st + ((long)b * Ts + s) * A : nullptr;
+    const T* z_row = Z_st ? Z_st + ((long)b * Ts + s) * A : nullptr;
     for (int iv = lane; iv < A / V; iv += 32) {
       float z[V];
       if (recompute) {
@@ -263,19 +375,17 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
 #pragma unroll
         for (int k = 0; k < V; ++k) z[k] = St<T>::round(__fadd_rn(qp_s[iv * V + k], kv[k]));
       } else {
-        ld16(e_row + iv * V, z);
+        ld16(z_row + iv * V, z);
       }
-      float e[V];
-#pragma unroll
-      for (int k = 0; k < V; ++k) e[k] = tanhf(z[k]);
       float dk[V];
       ldf<V>(dkp_row + iv * V, dk);
 #pragma unroll
       for (int k = 0; k < V; ++k) {
-        const float dE = __fmul_rn(__fmul_rn(ds, v_s[iv * V + k]), __fsub_rn(1.0f, __fmul_rn(e[k], e[k])));
+        const float e = tanhf(z[k]);
+        const float dE = __fmul_rn(__fmul_rn(ds, v_s[iv * V + k]), __fsub_rn(1.0f, __fmul_rn(e, e)));
         dk[k] = __fadd_rn(dk[k], dE);
         wq_w[iv * V + k] = __fadd_rn(wq_w[iv * V + k], dE);
-        wv_w[iv * V + k] = __fmaf_rn(ds, e[k], wv_w[iv * V + k]);
+        wv_w[iv * V + k] = __fmaf_rn(ds, e, wv_w[iv * V + k]);
       }
       stf<V>(dkp_row + iv * V, dk);
     }
@@ -295,9 +405,378 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
       q = __fadd_rn(q, wq[ww * A + a]);
       vv = __fadd_rn(vv, wv[ww * A + a]);
     }
-    dqp[(long)b * A + a] = q;
-    dv_part[(long)b * A + a] = __fadd_rn(dv_part[(long)b * A + a], vv);
+    xq[a] = q;
+    xv[a] = vv;
   }
+  cl.sync();
+  dqp_dv_finish(cl, xq, xv, A, dqp + (long)b * A, dv_part + (long)b * A, C, r, tid);
+  cl.sync();
+}
+
+// ================================================================ TMA-staged feature-split cluster path
+// The row b is processed by a cluster of C CTAs that split the FEATURE axes: CTA r owns a
+// slice of <= 128 columns of A (and of Hk).  At kernel entry one warp issues bulk async
+// copies (cp.async.bulk, the TMA engine's 1-D mode) of every row slice this CTA needs — Kp (or
+// the stashed Z) and Hs, and in the backward also the dKp / dHs accumulators — into shared
+// memory, completing on mbarriers; so all of the CTA's HBM traffic is in flight at once.
+// Per position, a warp produces the partial score (and partial dalpha) over the slice; ONE
+// cluster exchange (DSMEM) sums the partials in rank order; every CTA runs the tiny softmax
+// redundantly; ctx, dKp, dHs, dqp and dv are then column-local, one thread per column looping
+// over s.  Forward and backward share the partial-score code, the rank-ordered gather, the
+// softmax warp and the ctx column loop, so the regenerated alpha / ctx are bit-identical to the
+// stashed ones.
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct Slice {
+  int C, r, a0, a1, h0, h1;   // this CTA's column ranges [a0, a1) of A and [h0, h1) of Hk
+};
+static __host__ __device__ __forceinline__ int tma_cluster(int A, int Hk) {
+  const int m = A > Hk ? A : Hk;
+  const int want = (m + 127) / 128;
+  int C = 1;
+  while (C < want && C < 8) C <<= 1;
+  return C;
+}
+static __host__ __device__ __forceinline__ int tma_width(int X, int C) { return ((X + C - 1) / C + 7) / 8 * 8; }
+__device__ __forceinline__ Slice make_slice(int A, int Hk, int C, int r) {
+  Slice g;
+  g.C = C;
+  g.r = r;
+  const int pa = tma_width(A, C), ph = tma_width(Hk, C);
+  g.a0 = min(A, r * pa);
+  g.a1 = min(A, g.a0 + pa);
+  g.h0 = min(Hk, r * ph);
+  g.h1 = min(Hk, g.h0 + ph);
+  return g;
+}
+
+// 4 consecutive storage elements from shared memory as floats
+__device__ __forceinline__ void lds4(const float* p, float (&o)[4]) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void lds4(const __nv_bfloat16* p, float (&o)[4]) {
+  const uint2 v = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+  o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+}
+__device__ __forceinline__ void stg4(float* p, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void stg4(__nv_bfloat16* p, const float (&v)[4]) {
+  uint2 u;
+  *reinterpret_cast<__nv_bfloat162*>(&u.x) = __floats2bfloat162_rn(v[0], v[1]);
+  *reinterpret_cast<__nv_bfloat162*>(&u.y) = __floats2bfloat162_rn(v[2], v[3]);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+// z = round_s(qp + kz) (RECOMPUTE / forward) or the stashed z
+template <typename T>
+__device__ __forceinline__ float z_of(float qp, float kz, bool add_qp) {
+  return add_qp ? St<T>::round(__fadd_rn(qp, kz)) : kz;
+}
+
+// partial score over this CTA's A slice for one position (one warp; lanes over 4-column groups)
+template <typename T>
+__device__ __forceinline__ float score_partial(const T* kz_row, const float* qps, const float* vs, int W, int lane,
+                                               bool add_qp, T* z_out, float* e_out) {
+  float acc = 0.0f;
+  for (int c4 = lane; c4 < W / 4; c4 += 32) {
+    float kz[4], z[4], e[4];
+    lds4(kz_row + c4 * 4, kz);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      z[k] = z_of<T>(qps[c4 * 4 + k], kz[k], add_qp);
+      e[k] = tanhf(z[k]);
+      acc = __fmaf_rn(e[k], vs[c4 * 4 + k], acc);
+    }
+    if (z_out) stg4(z_out + c4 * 4, z);
+    if (e_out) *reinterpret_cast<float4*>(e_out + c4 * 4) = make_float4(e[0], e[1], e[2], e[3]);
+  }
+  return warp_sum(acc);
+}
+
+// rank-ordered gather of the C partial vectors part_c[0..n) into out[0..n)
+__device__ __forceinline__ void gather_sum(cg::cluster_group& cl, float* part, float* out, int n, int C, int tid) {
+  for (int s = tid; s < n; s += ATT_THREADS) {
+    float t[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) t[c] = c < C ? cl.map_shared_rank(part, c)[s] : 0.0f;
+    float x = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < C) x = __fadd_rn(x, t[c]);
+    out[s] = x;
+  }
+}
+
+// softmax of sc[0..n) into al[0..n) by ONE warp (max-subtracted, fixed order)
+__device__ __forceinline__ void softmax_row_warp(const float* sc, float* al, int n, int lane) {
+  float m = -INFINITY;
+  for (int s = lane; s < n; s += 32) m = fmaxf(m, sc[s]);
+  m = warp_max(m);
+  float l = 0.0f;
+  for (int s = lane; s < n; s += 32) l = __fadd_rn(l, expf(__fsub_rn(sc[s], m)));
+  l = warp_sum(l);
+  for (int s = lane; s < n; s += 32) al[s] = __fdiv_rn(expf(__fsub_rn(sc[s], m)), l);
+}
+
+// ctx columns of this CTA: one thread per column; positions are split round-robin over four
+// accumulators (s mod 4) for ILP and combined in fixed order ((a0 + a1) + (a2 + a3)).
+template <typename T>
+__device__ __forceinline__ void ctx_columns(const T* hs_s, int WH, const float* al, int n, T* ctx_out, int tid) {
+  for (int c = tid; c < WH; c += ATT_THREADS) {
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    int s = 0;
+    for (; s + 4 <= n; s += 4) {
+      a0 = __fmaf_rn(al[s], to_f(hs_s[(s + 0) * WH + c]), a0);
+      a1 = __fmaf_rn(al[s + 1], to_f(hs_s[(s + 1) * WH + c]), a1);
+      a2 = __fmaf_rn(al[s + 2], to_f(hs_s[(s + 2) * WH + c]), a2);
+      a3 = __fmaf_rn(al[s + 3], to_f(hs_s[(s + 3) * WH + c]), a3);
+    }
+    if (s < n) a0 = __fmaf_rn(al[s], to_f(hs_s[s * WH + c]), a0);
+    if (s + 1 < n) a1 = __fmaf_rn(al[s + 1], to_f(hs_s[(s + 1) * WH + c]), a1);
+    if (s + 2 < n) a2 = __fmaf_rn(al[s + 2], to_f(hs_s[(s + 2) * WH + c]), a2);
+    ctx_out[c] = from_f<T>(St<T>::round(__fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3))));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void stage_slice(float* dst, const T* __restrict__ src, int n, int tid) {
+  for (int i = tid; i < n; i += ATT_THREADS) dst[i] = to_f(src[i]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, const T* __restrict__ qp,
+                                                            const T* __restrict__ Kp, const T* __restrict__ v,
+                                                            const T* __restrict__ Hs,
+                                                            const int32_t* __restrict__ src_len, T* __restrict__ ctx,
+                                                            T* __restrict__ Z_st, float* __restrict__ alpha_st) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bar[1];
+  const int A = d.A, Ts = d.Ts, Hk = d.Hk;
+  const Slice g = make_slice(A, Hk, (int)cl.num_blocks(), (int)cl.block_rank());
+  const int W = g.a1 - g.a0, WH = g.h1 - g.h0;
+  const int Tp = (Ts + 3) & ~3;
+  T* kz = reinterpret_cast<T*>(smraw);                       // [Ts][W]
+  T* hs = kz + (size_t)Ts * W;                                // [Ts][WH]
+  float* f = reinterpret_cast<float*>(hs + (size_t)Ts * WH);
+  float* sc_part = f;                                         // [Tp]
+  float* sc = sc_part + Tp;                                   // [Tp]
+  float* al = sc + Tp;                                        // [Tp]
+  float* qps = al + Tp;                                       // [W]
+  float* vs = qps + W;                                        // [W]
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int n = row_len(src_len, b, Ts);
+  const T* kp_b = Kp + (long)b * d.kp_stride_b + g.a0;
+  const T* hs_b = Hs + (long)b * d.hs_stride_b + g.h0;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (w == 0) {
+    if (lane == 0) mbar_expect_tx(&bar[0], (uint32_t)(n * (W + WH) * sizeof(T)));
+    __syncwarp();
+    for (int s = lane; s < n; s += 32) {
+      bulk_g2s(kz + (size_t)s * W, kp_b + (long)s * d.kp_stride_s, W * sizeof(T), &bar[0]);
+      bulk_g2s(hs + (size_t)s * WH, hs_b + (long)s * d.hs_stride_s, WH * sizeof(T), &bar[0]);
+    }
+  }
+  stage_slice<T>(qps, qp + (long)b * A + g.a0, W, tid);
+  stage_slice<T>(vs, v + g.a0, W, tid);
+  __syncthreads();
+  mbar_wait(&bar[0], 0);
+  for (int s = w; s < n; s += ATT_WARPS) {
+    T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
+    const float p = score_partial<T>(kz + (size_t)s * W, qps, vs, W, lane, true, z_out, nullptr);
+    if (lane == 0) sc_part[s] = p;
+  }
+  if (Z_st) {                                                 // masked positions: zeros in this slice
+    float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int s = n + w; s < Ts; s += ATT_WARPS)
+      for (int c4 = lane; c4 < W / 4; c4 += 32) stg4(Z_st + ((long)b * Ts + s) * A + g.a0 + c4 * 4, z);
+  }
+  cl.sync();
+  gather_sum(cl, sc_part, sc, n, g.C, tid);
+  cluster_arrive();                                           // remote reads of sc_part done
+  __syncthreads();
+  if (w == 0) softmax_row_warp(sc, al, n, lane);
+  __syncthreads();
+  if (alpha_st && g.r == 0)
+    for (int s = tid; s < Ts; s += ATT_THREADS) alpha_st[(long)b * Ts + s] = s < n ? al[s] : 0.0f;
+  ctx_columns<T>(hs, WH, al, n, ctx + (long)b * Hk + g.h0, tid);
+  cluster_wait();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, const T* __restrict__ qp,
+                                                            const T* __restrict__ Kp, const T* __restrict__ v,
+                                                            const T* __restrict__ Hs,
+                                                            const int32_t* __restrict__ src_len,
+                                                            const T* __restrict__ Z_st,
+                                                            const float* __restrict__ alpha_st,
+                                                            const float* __restrict__ dctx, float* __restrict__ dqp,
+                                                            float* __restrict__ dKp, float* __restrict__ dHs,
+                                                            float* __restrict__ dv_part, T* __restrict__ ctx_regen) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bar[1];
+  const int A = d.A, Ts = d.Ts, Hk = d.Hk;
+  const Slice g = make_slice(A, Hk, (int)cl.num_blocks(), (int)cl.block_rank());
+  const int W = g.a1 - g.a0, WH = g.h1 - g.h0;
+  const int Tp = (Ts + 3) & ~3;
+  // E [Ts][W] fp32 tanh feature map; for fp32 storage it overwrites the kz rows in place
+  constexpr bool kE_ALIAS = sizeof(T) == sizeof(float);
+  float* E = reinterpret_cast<float*>(smraw);
+  T* kz = kE_ALIAS ? reinterpret_cast<T*>(smraw) : reinterpret_cast<T*>(E + (size_t)Ts * W);  // [Ts][W] Kp or Z
+  T* hs = kz + (size_t)Ts * W;                                // [Ts][WH] Hs slice rows
+  float* f = reinterpret_cast<float*>(hs + (size_t)Ts * WH);
+  float* sc_part = f;                                         // [Tp]
+  float* dal_part = sc_part + Tp;                             // [Tp]
+  float* sc = dal_part + Tp;                                  // [Tp]
+  float* dal = sc + Tp;                                       // [Tp]
+  float* al = dal + Tp;                                       // [Tp]
+  float* dsv = al + Tp;                                       // [Tp]
+  float* qps = dsv + Tp;                                      // [W]
+  float* vs = qps + W;                                        // [W]
+  float* dcs = vs + W;                                        // [WH]
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int n = row_len(src_len, b, Ts);
+  const bool recompute = (Z_st == nullptr);
+  const T* kz_b = recompute ? Kp + (long)b * d.kp_stride_b + g.a0 : Z_st + (long)b * Ts * A + g.a0;
+  const long kz_ss = recompute ? d.kp_stride_s : (long)A;
+  const T* hs_b = Hs + (long)b * d.hs_stride_b + g.h0;
+  float* dkp_b = dKp + (long)b * d.kp_stride_b + g.a0;
+  float* dhs_b = dHs + (long)b * d.hs_stride_b + g.h0;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (w == 0) {                                               // TMA: every Kp/Z and Hs row slice, at once
+    if (lane == 0) mbar_expect_tx(&bar[0], (uint32_t)(n * (W + WH) * sizeof(T)));
+    __syncwarp();
+    for (int s = lane; s < n; s += 32) {
+      bulk_g2s(kz + (size_t)s * W, kz_b + (long)s * kz_ss, W * sizeof(T), &bar[0]);
+      bulk_g2s(hs + (size_t)s * WH, hs_b + (long)s * d.hs_stride_s, WH * sizeof(T), &bar[0]);
+    }
+  }
+  if (recompute) stage_slice<T>(qps, qp + (long)b * A + g.a0, W, tid);
+  stage_slice<T>(vs, v + g.a0, W, tid);
+  for (int i = tid; i < WH; i += ATT_THREADS) dcs[i] = dctx[(long)b * Hk + g.h0 + i];
+  __syncthreads();
+  mbar_wait(&bar[0], 0);
+  // phase 1: E = tanh(z) into smem (fp32), partial scores (RECOMPUTE) and partial dalpha
+  for (int s = w; s < n; s += ATT_WARPS) {
+    const float p = score_partial<T>(kz + (size_t)s * W, qps, vs, W, lane, recompute, nullptr, E + (size_t)s * W);
+    float acc = 0.0f;
+    const T* hrow = hs + (size_t)s * WH;
+    for (int c4 = lane; c4 < WH / 4; c4 += 32) {
+      float h4[4];
+      lds4(hrow + c4 * 4, h4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc = __fmaf_rn(dcs[c4 * 4 + k], h4[k], acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      sc_part[s] = p;
+      dal_part[s] = acc;
+    }
+  }
+  cl.sync();
+  if (recompute) gather_sum(cl, sc_part, sc, n, g.C, tid);
+  gather_sum(cl, dal_part, dal, n, g.C, tid);
+  cluster_arrive();
+  __syncthreads();
+  if (w == 0) {
+    if (recompute) softmax_row_warp(sc, al, n, lane);
+    else
+      for (int s = lane; s < n; s += 32) al[s] = alpha_st[(long)b * Ts + s];
+    __syncwarp();
+    float acc = 0.0f;                                          // dot = sum_s alpha_s dalpha_s (fixed order)
+    for (int s = lane; s < n; s += 32) acc = __fmaf_rn(al[s], dal[s], acc);
+    acc = warp_sum(acc);
+    for (int s = lane; s < n; s += 32) dsv[s] = __fmul_rn(al[s], __fsub_rn(dal[s], acc));
+  }
+  __syncthreads();
+  if (recompute && ctx_regen) ctx_columns<T>(hs, WH, al, n, ctx_regen + (long)b * Hk + g.h0, tid);
+  // phase 4 (column-local, 8 positions of loads in flight per thread):
+  //   A columns : dKp += dE ; dqp = sum_s dE ; dv_part += sum_s ds E   with dE = ds v (1 - E^2)
+  //   Hk columns: dHs += alpha_s dctx
+  for (int i = tid; i < W + WH; i += ATT_THREADS) {
+    if (i < W) {
+      const int c = i;
+      const float vc = vs[c];
+      float dq = 0.0f, dvv = 0.0f;
+      for (int s0 = 0; s0 < n; s0 += 8) {
+        float dk[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < n) dk[u] = dkp_b[(long)(s0 + u) * d.kp_stride_s + c];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int s = s0 + u;
+          if (s < n) {
+            const float e = E[(size_t)s * W + c];
+            const float ds = dsv[s];
+            const float dE = __fmul_rn(__fmul_rn(ds, vc), __fsub_rn(1.0f, __fmul_rn(e, e)));
+            dkp_b[(long)s * d.kp_stride_s + c] = __fadd_rn(dk[u], dE);
+            dq = __fadd_rn(dq, dE);
+            dvv = __fmaf_rn(ds, e, dvv);
+          }
+        }
+      }
+      const long o = (long)b * A + g.a0 + c;
+      dqp[o] = dq;
+      dv_part[o] = __fadd_rn(dv_part[o], dvv);
+    } else {
+      const int c = i - W;
+      const float dcv = dcs[c];
+      for (int s0 = 0; s0 < n; s0 += 8) {
+        float dh[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < n) dh[u] = dhs_b[(long)(s0 + u) * d.hs_stride_s + c];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < n) dhs_b[(long)(s0 + u) * d.hs_stride_s + c] = __fmaf_rn(al[s0 + u], dcv, dh[u]);
+      }
+    }
+  }
+  cluster_wait();
 }
 
 __global__ void dv_reduce_kernel(int B, int A, const float* __restrict__ part, float* __restrict__ dv, int acc) {
@@ -309,16 +788,53 @@ __global__ void dv_reduce_kernel(int B, int A, const float* __restrict__ part, f
 }
 
 // ---------------------------------------------------------------- host side
+static int att_chunk(int Ts, int C) { return (Ts + C - 1) / C; }
+
 static size_t fwd_smem(const echo_attn_desc* d) {
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
   const int G = ctx_groups(d->Hk, V);
-  return sizeof(float) * (2 * (size_t)d->A + ((d->Ts + 3) & ~3) + (size_t)G * d->Hk);
+  const int chunk = att_chunk(d->Ts, att_cluster(d->Ts));
+  return sizeof(float) * (2 * (size_t)d->A + 4 + ((chunk + 3) & ~3) + (size_t)G * d->Hk + d->Hk);
 }
 static size_t bwd_smem(const echo_attn_desc* d) {
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
   const int G = ctx_groups(d->Hk, V);
-  return sizeof(float) * (2 * (size_t)d->A + d->Hk + 2 * (size_t)((d->Ts + 3) & ~3) + 4 +
-                          2 * (size_t)ATT_WARPS * d->A + (size_t)G * d->Hk);
+  const int chunk = att_chunk(d->Ts, att_cluster(d->Ts));
+  return sizeof(float) * (2 * (size_t)d->A + d->Hk + 4 + 2 * (size_t)((chunk + 3) & ~3) +
+                          2 * (size_t)ATT_WARPS * d->A + 2 * (size_t)d->A + (size_t)G * d->Hk + d->Hk);
+}
+
+// TMA path: cluster size and shared-memory footprint; returns false if the generic path must run
+static bool tma_params(const echo_attn_desc* d, int* C, size_t* smem_fwd, size_t* smem_bwd) {
+  const size_t sT = d->dtype == ECHO_FP32 ? 4 : 2;
+  if (d->A > 1024 || d->Hk > 1024) return false;
+  const int c = tma_cluster(d->A, d->Hk);
+  const size_t W = tma_width(d->A, c), WH = tma_width(d->Hk, c);
+  const size_t Tp = (d->Ts + 3) & ~3;
+  const size_t fwd = d->Ts * (W + WH) * sT + (3 * Tp + 2 * W) * 4;
+  const size_t bwd = d->Ts * (W * (sT == 4 ? 4 : 4 + sT) + WH * sT) + (6 * Tp + 2 * W + WH) * 4;
+  if (bwd > 200 * 1024) return false;
+  *C = c;
+  *smem_fwd = fwd;
+  *smem_bwd = bwd;
+  return true;
+}
+
+template <typename Kern, typename... Args>
+static cudaError_t launch_cluster(Kern kern, int C, int B, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, B, 1);
+  cfg.blockDim = dim3(ATT_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 static echo_status check_attn(const char* fn, const echo_attn_desc* d) {
@@ -327,6 +843,7 @@ static echo_status check_attn(const char* fn, const echo_attn_desc* d) {
     return fail(ECHO_ERR_INVALID, "%s: B=%d Ts=%d A=%d Hk=%d must be > 0", fn, d->B, d->Ts, d->A, d->Hk);
   if (d->A % 8 || d->Hk % 8) return fail(ECHO_ERR_INVALID, "%s: A=%d and Hk=%d must be multiples of 8", fn, d->A, d->Hk);
   if (d->Ts > 4096) return fail(ECHO_ERR_CAPACITY, "%s: Ts=%d exceeds 4096", fn, d->Ts);
+  if (d->B > 65535) return fail(ECHO_ERR_CAPACITY, "%s: B=%d exceeds 65535 rows per launch", fn, d->B);
   if (d->dtype != ECHO_FP32 && d->dtype != ECHO_BF16) return fail(ECHO_ERR_INVALID, "%s: bad dtype %d", fn, d->dtype);
   if (d->mode != ECHO_STASH && d->mode != ECHO_RECOMPUTE) return fail(ECHO_ERR_INVALID, "%s: bad mode %d", fn, d->mode);
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
@@ -373,19 +890,37 @@ extern "C" echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, co
   } else if (E_st || alpha_st) {
     return fail(ECHO_ERR_INVALID, "%s: E_st / alpha_st must be NULL in RECOMPUTE mode", fn);
   }
-  const size_t smem = fwd_smem(d);
   cudaStream_t st = (cudaStream_t)stream;
+  const int C = att_cluster(d->Ts), chunk = att_chunk(d->Ts, C);
+  cudaError_t e;
+  int tC;
+  size_t sf, sb;
+  if (tma_params(d, &tC, &sf, &sb)) {
+    if (d->dtype == ECHO_FP32) {
+      if ((s = set_smem((const void*)attn_fwd_tma<float>, sf, fn))) return s;
+      e = launch_cluster(attn_fwd_tma<float>, tC, d->B, sf, st, *d, (const float*)qp, (const float*)Kp, (const float*)v,
+                         (const float*)Hs, src_len, (float*)ctx, (float*)E_st, alpha_st);
+    } else {
+      typedef __nv_bfloat16 bf;
+      if ((s = set_smem((const void*)attn_fwd_tma<bf>, sf, fn))) return s;
+      e = launch_cluster(attn_fwd_tma<bf>, tC, d->B, sf, st, *d, (const bf*)qp, (const bf*)Kp, (const bf*)v,
+                         (const bf*)Hs, src_len, (bf*)ctx, (bf*)E_st, alpha_st);
+    }
+    if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+    return check_launch(fn);
+  }
+  const size_t smem = fwd_smem(d);
   if (d->dtype == ECHO_FP32) {
     if ((s = set_smem((const void*)attn_fwd_kernel<float>, smem, fn))) return s;
-    attn_fwd_kernel<float><<<d->B, ATT_THREADS, smem, st>>>(*d, (const float*)qp, (const float*)Kp, (const float*)v,
-                                                            (const float*)Hs, src_len, (float*)ctx, (float*)E_st,
-                                                            alpha_st);
+    e = launch_cluster(attn_fwd_kernel<float>, C, d->B, smem, st, *d, chunk, (const float*)qp, (const float*)Kp,
+                       (const float*)v, (const float*)Hs, src_len, (float*)ctx, (float*)E_st, alpha_st);
   } else {
     typedef __nv_bfloat16 bf;
     if ((s = set_smem((const void*)attn_fwd_kernel<bf>, smem, fn))) return s;
-    attn_fwd_kernel<bf><<<d->B, ATT_THREADS, smem, st>>>(*d, (const bf*)qp, (const bf*)Kp, (const bf*)v, (const bf*)Hs,
-                                                         src_len, (bf*)ctx, (bf*)E_st, alpha_st);
+    e = launch_cluster(attn_fwd_kernel<bf>, C, d->B, smem, st, *d, chunk, (const bf*)qp, (const bf*)Kp, (const bf*)v,
+                       (const bf*)Hs, src_len, (bf*)ctx, (bf*)E_st, alpha_st);
   }
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);
 }
 
@@ -413,20 +948,41 @@ extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, co
     if (E_st || alpha_st) return fail(ECHO_ERR_INVALID, "%s: E_st / alpha_st must be NULL in RECOMPUTE mode", fn);
     if (ctx_regen && !aligned16(ctx_regen)) return fail(ECHO_ERR_INVALID, "%s: ctx_regen not 16-byte aligned", fn);
   }
-  const size_t smem = bwd_smem(d);
   cudaStream_t st = (cudaStream_t)stream;
+  const int C = att_cluster(d->Ts), chunk = att_chunk(d->Ts, C);
+  cudaError_t e;
+  int tC;
+  size_t sf, sb;
+  if (tma_params(d, &tC, &sf, &sb)) {
+    if (d->dtype == ECHO_FP32) {
+      if ((s = set_smem((const void*)attn_bwd_tma<float>, sb, fn))) return s;
+      e = launch_cluster(attn_bwd_tma<float>, tC, d->B, sb, st, *d, (const float*)qp, (const float*)Kp, (const float*)v,
+                         (const float*)Hs, src_len, (const float*)E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part,
+                         (float*)ctx_regen);
+    } else {
+      typedef __nv_bfloat16 bf;
+      if ((s = set_smem((const void*)attn_bwd_tma<bf>, sb, fn))) return s;
+      e = launch_cluster(attn_bwd_tma<bf>, tC, d->B, sb, st, *d, (const bf*)qp, (const bf*)Kp, (const bf*)v,
+                         (const bf*)Hs, src_len, (const bf*)E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part,
+                         (bf*)ctx_regen);
+    }
+    if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+    return check_launch(fn);
+  }
+  const size_t smem = bwd_smem(d);
   if (d->dtype == ECHO_FP32) {
     if ((s = set_smem((const void*)attn_bwd_kernel<float>, smem, fn))) return s;
-    attn_bwd_kernel<float><<<d->B, ATT_THREADS, smem, st>>>(*d, (const float*)qp, (const float*)Kp, (const float*)v,
-                                                            (const float*)Hs, src_len, (const float*)E_st, alpha_st,
-                                                            dctx, dqp, dKp, dHs, dv_part, (float*)ctx_regen);
+    e = launch_cluster(attn_bwd_kernel<float>, C, d->B, smem, st, *d, chunk, (const float*)qp, (const float*)Kp,
+                       (const float*)v, (const float*)Hs, src_len, (const float*)E_st, alpha_st, dctx, dqp, dKp, dHs,
+                       dv_part, (float*)ctx_regen);
   } else {
     typedef __nv_bfloat16 bf;
     if ((s = set_smem((const void*)attn_bwd_kernel<bf>, smem, fn))) return s;
-    attn_bwd_kernel<bf><<<d->B, ATT_THREADS, smem, st>>>(*d, (const bf*)qp, (const bf*)Kp, (const bf*)v, (const bf*)Hs,
-                                                         src_len, (const bf*)E_st, alpha_st, dctx, dqp, dKp, dHs,
-                                                         dv_part, (bf*)ctx_regen);
+    e = launch_cluster(attn_bwd_kernel<bf>, C, d->B, smem, st, *d, chunk, (const bf*)qp, (const bf*)Kp, (const bf*)v,
+                       (const bf*)Hs, src_len, (const bf*)E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part,
+                       (bf*)ctx_regen);
   }
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);
 }
 

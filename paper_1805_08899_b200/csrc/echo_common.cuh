@@ -93,6 +93,13 @@ __device__ __forceinline__ void stf(float* p, const float (&v)[N]) {
   for (int k = 0; k < N; k += 4) *reinterpret_cast<float4*>(p + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
 }
 
+// scalar storage <-> float
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
 // ------------------------------------------------------------------ math (IEEE, no fast-math)
 __device__ __forceinline__ float sigmoidf_(float x) {
   return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));

@@ -320,13 +320,17 @@ class NMTModel:
                     addmm_(dHdec[l - 1][t], dA, self.w(f"dec{l}.Wx"))
                 elif t > 0:
                     addmm_(dAout[t - 1], dA, WxA)                # input feeding: carry into da_{t-1}
-        # deferred weight-gradient GEMMs (their inputs are stashed or were regenerated above)
-        qall = dec[-1].h_for_grad().reshape(N, H)
-        dPREs = self._to_s(dPRE.view(N, H))
-        gi(G["att.Wcc"], dPREs.t(), ctx_all.view(N, H))
+        # deferred weight-gradient GEMMs (their inputs are stashed or were regenerated above).  The
+        # gradient operands dpre / dqp are fp32: for bf16 storage the GEMM is run in fp32 on the
+        # up-cast activations rather than rounding the gradient to bf16 (no-op for fp32).
+        f32 = lambda x: x if x.dtype == torch.float32 else x.float()
+        qall = f32(dec[-1].h_for_grad().reshape(N, H))
+        dPREs = dPRE.view(N, H)
+        gi(G["att.Wcc"], dPREs.t(), f32(ctx_all.view(N, H)))
         gi(G["att.Wch"], dPREs.t(), qall)
-        gi(G["att.Wq"], self._to_s(dQP.view(N, A)).t(), qall)
+        gi(G["att.Wq"], dQP.view(N, A).t(), qall)
         abi.echo_attn_dv_reduce(B, A, dv_part, G["att.v"], 0)
+        del qall
         del dPREs, dPRE, dQP
         for l in range(Ld):
             L = dec[l]
@@ -352,9 +356,10 @@ class NMTModel:
         # attention key projection Kp = Hs W_k^T + b_q --------------------------------------
         dKpf = dKp.view(Ts * B, A)
         torch.sum(dKpf, dim=0, out=G["att.bq"])
-        dKps = self._to_s(dKpf)
-        gi(G["att.Wk"], dKps.t(), Hs.reshape(Ts * B, H))
-        addmm_(dHs.view(Ts * B, H), dKps, self.w("att.Wk"))
+        Hs32 = Hs.reshape(Ts * B, H)
+        gi(G["att.Wk"], dKpf.t(), Hs32 if Hs32.dtype == torch.float32 else Hs32.float())
+        dHs.view(Ts * B, H).addmm_(dKpf, self.P["att.Wk"])
+        dKps = None
         del dKp, dKpf, dKps
         # encoder, top-down; dW_x of layer l+1 needs this layer's h (stashed or regenerated) ---
         enc = a["enc"]
