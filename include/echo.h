@@ -91,12 +91,15 @@ echo_status echo_lstm_fwd(const echo_lstm_desc* d, const void* gx_t, const void*
 /* a2 — cell-state regeneration scan (RECOMPUTE backward prologue, run once per
  * layer before the reverse time loop).  Re-executes the mirrored c-chain from
  * the stashed gates and c_0 (Fig. 4 step 4; recomputation path
- * Fig. 8(c)), with the exact device function of a1.
+ * Fig. 8(c)), with the exact device functions of a1.
  *  gates [T,B,4H] s   stashed gates in processing order
  *  c0    [B,H] fp32
- *  c_ws  [T,B,H] fp32 OUT c_1..c_T (transient workspace owned by the caller) */
+ *  c_ws  [T,B,H] fp32 OUT c_1..c_T (transient workspace owned by the caller)
+ *  h_ws  [T,B,H] s    OUT h_1..h_T, bit-identical to a1's outputs, or NULL (used when a
+ *                     layer's outputs are themselves mirrored, e.g. the encoder states H_s
+ *                     that the attention backward reads at every decoder step)            */
 echo_status echo_lstm_cscan(const echo_lstm_desc* d, int32_t T, const void* gates,
-                            const float* c0, float* c_ws, void* stream);
+                            const float* c0, float* c_ws, void* h_ws, void* stream);
 
 /* a3 — backward step with fused recomputation (Echo-dagger fusion).
  *  gates_t [B,4H] s    stashed i|f|g|o

@@ -66,7 +66,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.echo_abi_version.restype = ctypes.c_int
     sigs = {
         "echo_lstm_fwd": [ctypes.POINTER(LstmDesc)] + [vp] * 9,
-        "echo_lstm_cscan": [ctypes.POINTER(LstmDesc), i32, vp, vp, vp, vp],
+        "echo_lstm_cscan": [ctypes.POINTER(LstmDesc), i32, vp, vp, vp, vp, vp],
         "echo_lstm_bwd": [ctypes.POINTER(LstmDesc)] + [vp] * 9,
         "echo_attn_fwd": [ctypes.POINTER(AttnDesc)] + [vp] * 9,
         "echo_attn_bwd": [ctypes.POINTER(AttnDesc)] + [vp] * 14,
@@ -118,9 +118,9 @@ def echo_lstm_fwd(d, gx_t, gh_t, bias, c_prev, gates_t, c_out, tc_t, h_out, stre
                                 _p(tc_t), _p(h_out), _stream(stream)))
 
 
-def echo_lstm_cscan(d, T, gates, c0, c_ws, stream=None):
+def echo_lstm_cscan(d, T, gates, c0, c_ws, h_ws=None, stream=None):
     LAUNCHES["count"] += 1
-    _check(load().echo_lstm_cscan(ctypes.byref(d), int(T), _p(gates), _p(c0), _p(c_ws), _stream(stream)))
+    _check(load().echo_lstm_cscan(ctypes.byref(d), int(T), _p(gates), _p(c0), _p(c_ws), _p(h_ws), _stream(stream)))
 
 
 def echo_lstm_bwd(d, gates_t, c_prev, c_t, tc_t, dh_t, dc, dA_t, h_regen, stream=None):

@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(128) lstm_fwd_kernel(int B, int H, const T* gx
 // ---------------------------------------------------------------- a2 c-regeneration scan
 template <typename T, int U>
 __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, const T* __restrict__ gates,
-                                                         const float* __restrict__ c0, float* __restrict__ cws) {
+                                                         const float* __restrict__ c0, float* __restrict__ cws,
+                                                         T* __restrict__ hws) {
   constexpr int V = St<T>::VEC;
   const int nvec = H / V;
   const long total = (long)B * nvec;
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, c
     const int j = (int)(idx - (long)b * nvec) * V;
     const T* gp = gates + (long)b * 4 * H + j;
     float* cp = cws + (long)b * H + j;
+    T* hp = hws ? hws + (long)b * H + j : nullptr;
     float c[V];
     ldf<V>(c0 + (long)b * H + j, c);
     for (int t0 = 0; t0 < T_; t0 += U) {
@@ -123,6 +125,13 @@ __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, c
 #pragma unroll
           for (int k = 0; k < V; ++k) c[k] = cell_update(gf[u][k], c[k], gi[u][k], gg[u][k]);
           stf<V>(cp + (long)(t0 + u) * cstep, c);
+          if (hp) {                                         // mirrored outputs: h_t = o * tanh(c_t)
+            float go[V], h[V];
+            ld16_stream(gp + (long)(t0 + u) * gstep + 3 * H, go);
+#pragma unroll
+            for (int k = 0; k < V; ++k) h[k] = hidden<T>(go[k], tanh_c<T>(c[k]));
+            st16(hp + (long)(t0 + u) * cstep, h);
+          }
         }
       }
     }
@@ -240,7 +249,7 @@ extern "C" echo_status echo_lstm_fwd(const echo_lstm_desc* d, const void* gx_t, 
 }
 
 extern "C" echo_status echo_lstm_cscan(const echo_lstm_desc* d, int32_t T, const void* gates, const float* c0,
-                                       float* c_ws, void* stream) {
+                                       float* c_ws, void* h_ws, void* stream) {
   const char* fn = "echo_lstm_cscan";
   echo_status s = check_desc(d);
   if (s) return s;
@@ -248,13 +257,15 @@ extern "C" echo_status echo_lstm_cscan(const echo_lstm_desc* d, int32_t T, const
   ECHO_REQ(gates, "gates");
   ECHO_REQ(c0, "c0");
   ECHO_REQ(c_ws, "c_ws");
+  ECHO_OPT(h_ws, "h_ws");
   cudaStream_t st = (cudaStream_t)stream;
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
   const int grid = grid_for((long)d->B * d->H / V, 128);
   if (d->dtype == ECHO_FP32)
-    lstm_cscan_kernel<float, 8><<<grid, 128, 0, st>>>(T, d->B, d->H, (const float*)gates, c0, c_ws);
+    lstm_cscan_kernel<float, 8><<<grid, 128, 0, st>>>(T, d->B, d->H, (const float*)gates, c0, c_ws, (float*)h_ws);
   else
-    lstm_cscan_kernel<__nv_bfloat16, 4><<<grid, 128, 0, st>>>(T, d->B, d->H, (const __nv_bfloat16*)gates, c0, c_ws);
+    lstm_cscan_kernel<__nv_bfloat16, 4><<<grid, 128, 0, st>>>(T, d->B, d->H, (const __nv_bfloat16*)gates, c0, c_ws,
+                                                              (__nv_bfloat16*)h_ws);
   return check_launch(fn);
 }
 

@@ -156,6 +156,8 @@ class NMTModel:
                 enc[l - 1].h = None                              # lower layer's output was only the FC input
             enc.append(L)
             X = L.h
+            if l == 0 and md == abi.RECOMPUTE:
+                a["X0"] = None                                   # embeddings: recomputed from the tokens
         a["enc"] = enc
         Hs = X                                                   # [Ts,B,H] s-major source hidden state
         a["Hs"] = Hs
@@ -172,6 +174,9 @@ class NMTModel:
             L.h0, L.c0 = self.zero_h, self.zero_c
         Wx0 = self.w("dec0.Wx")
         torch.mm(EmbT.view(Td * B, E), Wx0[:, :E].t(), out=dec[0].gates.view(Td * B, 4 * H))
+        if md == abi.RECOMPUTE:
+            a["EmbT"] = None
+            del EmbT
         Aall = torch.empty(Td, B, H, dtype=sd, device=dev)       # attention hidden a_t (stash, both modes)
         a["Aall"] = Aall
         if md == abi.STASH:
@@ -209,6 +214,13 @@ class NMTModel:
             addmm_(pre, q, Wch.t())
             torch.tanh(pre, out=Aall[t])
         a["dec"] = dec
+        if md == abi.RECOMPUTE:                                  # H_s is mirrored (Echo plan): regenerated
+            a["Hs"] = None                                       # by the top encoder layer's scan
+            enc[-1].h = None
+            Hs = None
+        else:                                                    # STASH reads the stashed tanh inputs, not Kp
+            a["Kp"] = None
+            Kp = None
         # output layer + CE; logits are overwritten in place by dlogits (the CE's fp32 feature map)
         N = B * Td
         logits = mm(Aall.view(N, H), self.w("out.Wo").t(), torch.float32)
@@ -226,8 +238,12 @@ class NMTModel:
 
     def _stash_registry(self, a):
         """Every tensor kept across the forward->backward boundary for the backward pass."""
-        reg = {"emb_src_out": a["X0"], "emb_tgt_out": a["EmbT"], "Hs": a["Hs"], "Kp": a["Kp"], "a_t": a["Aall"],
-               "ce_probs": a["dlogits"]}
+        inp = self.inputs
+        reg = {"src_tokens": inp["src"], "tgt_tokens": inp["tgt_in"], "src_len": inp["src_len"], "h0": self.zero_h,
+               "c0": self.zero_c, "a_t": a["Aall"], "ce_probs": a["dlogits"]}
+        for k in ("X0", "EmbT", "Hs", "Kp"):
+            if a.get(k) is not None:
+                reg[k] = a[k]
         for l, L in enumerate(a["enc"]):
             for k, t in L.stash_views().items():
                 reg[f"enc{l}.{k}"] = t
@@ -279,6 +295,11 @@ class NMTModel:
         # decoder, reverse time ----------------------------------------------------------
         dec = a["dec"]
         Ld = len(dec)
+        enc = a["enc"]
+        if md == abi.RECOMPUTE:                                  # mirrored H_s: top encoder layer's a2 scan
+            Hs = enc[-1].prepare_backward(regen_h=True)          # also regenerates its h_1..h_Ts
+        else:
+            Hs = a["Hs"]
         for L in dec:
             L.prepare_backward()                                 # RECOMPUTE: a2 c-scan per layer
         dHdec = [torch.zeros(Td, B, H, dtype=torch.float32, device=dev) for _ in range(Ld)]
@@ -293,7 +314,7 @@ class NMTModel:
         Wx0 = self.w("dec0.Wx")
         WxA = Wx0[:, E:]
         Wq, Wcc, Wch, v = self.w("att.Wq"), self.w("att.Wcc"), self.w("att.Wch"), self.w("att.v")
-        adesc, Kp, Hs, sl = a["adesc"], a["Kp"], a["Hs"], self.inputs["src_len"]
+        adesc, Kp, sl = a["adesc"], a["Kp"], self.inputs["src_len"]
         # per-step backward-data GEMMs of the attention block use the fp32 master weights, so
         # the fp32 gradient signals dpre / dqp are not rounded to the storage dtype (no-op in fp32)
         Wcc32, Wch32, Wq32 = self.P["att.Wcc"], self.P["att.Wch"], self.P["att.Wq"]
@@ -342,7 +363,10 @@ class NMTModel:
             if l > 0:
                 gi(G[f"dec{l}.Wx"], dAl.t(), dec[l - 1].h_for_grad().reshape(N, H))
             else:
-                gi(G["dec0.Wx"][:, :E], dAl.t(), a["EmbT"].view(N, E))
+                EmbT = a["EmbT"] if md == abi.STASH else \
+                    self.w("emb_tgt").index_select(0, self.inputs["tgt_in"].t().reshape(-1))   # recomputed
+                gi(G["dec0.Wx"][:, :E], dAl.t(), EmbT.view(N, E))
+                del EmbT
                 if Td > 1:
                     gi(G["dec0.Wx"][:, E:], L.gates[1:].reshape((Td - 1) * B, 4 * H).t(),
                        Aall[: Td - 1].reshape((Td - 1) * B, H))
@@ -360,9 +384,9 @@ class NMTModel:
         gi(G["att.Wk"], dKpf.t(), Hs32 if Hs32.dtype == torch.float32 else Hs32.float())
         dHs.view(Ts * B, H).addmm_(dKpf, self.P["att.Wk"])
         dKps = None
+        del Hs, Hs32
         del dKp, dKpf, dKps
         # encoder, top-down; dW_x of layer l+1 needs this layer's h (stashed or regenerated) ---
-        enc = a["enc"]
         Le = len(enc)
         n = Ts * B
         dH = dHs
@@ -386,7 +410,10 @@ class NMTModel:
                 enc[l + 1] = None
             dX = mm(dAl, self.w(f"enc{l}.Wx"), torch.float32).view(Ts, B, -1)
             if l == 0:
-                gi(G["enc0.Wx"], dAl.t(), a["X0"].view(n, E))
+                X0 = a["X0"] if md == abi.STASH else \
+                    self.w("emb_src").index_select(0, self.inputs["src"].t().reshape(-1))      # recomputed
+                gi(G["enc0.Wx"], dAl.t(), X0.view(n, E))
+                del X0
                 _det_index_add(G["emb_src"], self.inputs["src"].t().reshape(-1), dX.view(n, E))
                 enc[0] = None
             L.release_backward()

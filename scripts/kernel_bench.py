@@ -95,7 +95,7 @@ for md, mname in ((abi.RECOMPUTE, "recompute"), (abi.STASH, "stash")):
         report(f"lstm_bwd a3 ({mname})", ms, nb)
 if want("cscan"):
     d = abi.LstmDesc(B, H, dt, abi.RECOMPUTE)
-    ms = timeit(lambda: abi.echo_lstm_cscan(d, T, gates, c0, cws))
+    ms = timeit(lambda: abi.echo_lstm_cscan(d, T, gates, c0, cws, None))
     report("lstm_cscan a2", ms, T * BH * (3 * s + 4) + BH * 4)
 
 # ---- attention (s-major layout as in the NMT step)

@@ -93,6 +93,22 @@ def test_layer_parity_and_bit_identity(storage, T, B, I, H, cuda_dev):
         assert bits_equal(s[2][k], r[2][k]), f"STASH vs RECOMPUTE differ in {k}"
 
 
+@pytest.mark.parametrize("storage", STORAGES)
+def test_cscan_regenerates_h_bitwise(storage, cuda_dev):
+    abi = _abi()
+    from paper_1805_08899_b200.lstm import LSTMLayer
+    T, B, I, H = 9, 5, 16, 40
+    d = lstm_layer_inputs(4, T, B, I, H, storage)
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    S = LSTMLayer(T, B, H, dt, abi.STASH)
+    S.forward_seq(dev(d["X"], storage), dev(d["Wx"], storage), dev(d["Wh"], storage), dev(d["b"], dtype=torch.float32),
+                  dev(d["h0"], storage), dev(d["c0"], dtype=torch.float32))
+    cws = torch.empty(T, B, H, device="cuda")
+    hws = torch.empty_like(S.h)
+    abi.echo_lstm_cscan(abi.LstmDesc(B, H, dt, abi.RECOMPUTE), T, S.gates, S.c0, cws, hws)
+    assert bits_equal(cws[: T - 1], S.c[: T - 1]) and bits_equal(hws, S.h)
+
+
 def test_cscan_matches_forward_c_bitwise(cuda_dev):
     """a2 regenerates exactly the c_t the forward produced (same device function)."""
     abi = _abi()
@@ -102,8 +118,10 @@ def test_cscan_matches_forward_c_bitwise(cuda_dev):
     S = LSTMLayer(T, B, H, abi.FP32, abi.STASH)
     S.forward_seq(dev(d["X"]), dev(d["Wx"]), dev(d["Wh"]), dev(d["b"]), dev(d["h0"]), dev(d["c0"]))
     cws = torch.empty(T, B, H, device="cuda")
-    abi.echo_lstm_cscan(abi.LstmDesc(B, H, abi.FP32, abi.RECOMPUTE), T, S.gates, S.c0, cws)
+    hws = torch.empty(T, B, H, device="cuda")
+    abi.echo_lstm_cscan(abi.LstmDesc(B, H, abi.FP32, abi.RECOMPUTE), T, S.gates, S.c0, cws, hws)
     assert bits_equal(cws, S.c)
+    assert bits_equal(hws, S.h)          # mirrored layer outputs regenerate bit-identically
 
 
 def test_validation_errors(cuda_dev):

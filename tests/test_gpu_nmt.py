@@ -29,9 +29,12 @@ def _run(cfg, params, batch, dtype, mode):
     return m, loss
 
 
-@pytest.mark.parametrize("cfg", [C1, SMALL_NMT, RAGGED], ids=lambda c: c.name)
-@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("cfg,storage", [(C1, "fp32"), (SMALL_NMT, "fp32"), (RAGGED, "fp32"),
+                                         (SMALL_NMT, "bf16"), (RAGGED, "bf16")],
+                         ids=lambda x: getattr(x, "name", x))
 def test_nmt_step_parity_and_bit_identity(cfg, storage, cuda_dev):
+    """BASELINE.json configs[0] (C1) is fp32; bf16 storage is exercised on the multi-layer configs
+    (C2's bf16 variant is checked at full size below)."""
     from paper_1805_08899_b200 import abi
     params = nmt_params(11, cfg, storage)
     batch = nmt_batch(12, cfg, lengths="random")
@@ -62,18 +65,22 @@ def test_nmt_run_to_run_bitwise(cuda_dev):
     assert bits_equal(g1, g2)
 
 
-def test_nmt_c2_full_size_parity(cuda_dev):
-    """C2 (B=128, T=50, H=512, V=8192) one step vs the fp64 oracle (all gradients), RECOMPUTE."""
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+def test_nmt_c2_full_size_parity(storage, cuda_dev):
+    """C2 (B=128, T=50, H=512, V=8192) one step vs the fp64 oracle (all gradients), RECOMPUTE,
+    in the launch configuration bench.py times."""
     from paper_1805_08899_b200 import abi
     cfg = C2
-    params = nmt_params(3, cfg)
+    params = nmt_params(3, cfg, storage)
     batch = nmt_batch(4, cfg, lengths="random")
     ref = O.step(params, batch, cfg)
-    m, loss = _run(cfg, params, batch, abi.FP32, abi.RECOMPUTE)
-    assert abs(loss - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    m, loss = _run(cfg, params, batch, abi.FP32 if storage == "fp32" else abi.BF16, abi.RECOMPUTE)
+    tol = 1e-4 if storage == "fp32" else 2e-2
+    metric = relerr if storage == "fp32" else relerr_fro
+    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
     g = m.grads_numpy()
     for k, v in ref["grads"].items():
-        assert relerr(g[k], v) <= 1e-4, (k, relerr(g[k], v))
+        assert metric(g[k], v) <= tol, (k, metric(g[k], v))
 
 
 def test_stash_bytes_ratio_c2(cuda_dev):
@@ -89,3 +96,25 @@ def test_stash_bytes_ratio_c2(cuda_dev):
         out[mode] = m.stash_bytes()
         del acts
     assert out[abi.STASH] / out[abi.RECOMPUTE] >= 1.8, out
+
+
+@pytest.mark.parametrize("cfg", [C1, SMALL_NMT, RAGGED, C2], ids=lambda c: c.name)
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+def test_stash_bytes_equal_estimator(cfg, storage, cuda_dev):
+    """Exact integer bytes: the tensors the GPU step keeps across the forward -> backward boundary
+    sum to the estimator's stash bytes — Baseline plan for STASH, Echo's plan for RECOMPUTE."""
+    import json
+    from paper_1805_08899_b200 import abi
+    from paper_1805_08899_b200.nmt import NMTModel
+    from synth import graphs as Gr
+    doc = json.dumps(Gr.nmt(cfg, "f32" if storage == "fp32" else "bf16"))
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    for mode, strat in ((abi.STASH, "baseline"), (abi.RECOMPUTE, "echo")):
+        rep = json.loads(abi.echo_footprint_estimate(doc, json.dumps({"strategy": strat})))
+        m = NMTModel(cfg, dt, mode)
+        m.upload_batch(nmt_batch(0, cfg))
+        acts = m._forward()
+        assert m.stash_bytes() == rep["stash_bytes"], (strat, m.stash_bytes(), rep["stash_bytes"],
+                                                       {k: v.numel() * v.element_size() for k, v in m.stash.items()})
+        m._backward(acts)
+        del acts
