@@ -139,6 +139,18 @@ def cpu_baseline_sample():
             "sample": f"C2 shapes (B=16 of 128, T=50, H=512, V=8192), {n} full training steps, numpy fp64"}
 
 
+def ncu_traffic(dtype):
+    """DRAM read + write bytes per launch of the a6 kernel from the committed `ncu --set full`
+    capture of the same launch configuration (profiles/), or None."""
+    import glob
+    tag = "fp32" if dtype == 0 else "bf16"
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", f"*ncu_attn_bwd_c2_{tag}.txt")), reverse=True):
+        for line in open(f):
+            if line.startswith("traffic = dram read + write"):
+                return {"bytes": float(line.split()[-1]), "source": os.path.relpath(f, ROOT)}
+    return None
+
+
 def time_attn_bwd(cfg, dtype, reps=20):
     """Dominant kernel (a6, RECOMPUTE attention backward) at the step's launch configuration,
     timed with CUDA events on its launch stream; L2 flushed (256 MiB read) before every launch."""
@@ -320,6 +332,7 @@ def run_ours(args):
         out["ms_other"] = ms_other
         out["mem"] = mem
         out["kern"] = time_attn_bwd(cfg, dtype)
+        out["traffic"] = ncu_traffic(dtype) if cfg.B == 128 else None
     if ws > 1 and rank != 0:
         dp.barrier()
         return
@@ -354,7 +367,8 @@ def run_ours(args):
         n_att = cfg.Td
         line["roofline"] = {"bound": "hbm", "kernel": "echo_attn_bwd (a6, RECOMPUTE)", "achieved": achieved,
                             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                            "traffic": None, "peak_source": pk["source"],
+                            "traffic": (out["traffic"] or {}).get("bytes"),
+                            "traffic_source": (out["traffic"] or {}).get("source"), "peak_source": pk["source"],
                             "bytes_per_launch": k["bytes"], "bytes_per_row": k["bytes_per_row"],
                             "launch_us": 1e3 * k["ms"], "timing": "CUDA events, L2 flushed (256 MiB read) before each launch",
                             "share_of_step": n_att * k["ms"] / ms}
