@@ -48,6 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in _sources():
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include")]
+        cmd += os.environ.get("ECHO_NVCC_EXTRA", "").split()
         if src.endswith(".cu"):
             cmd += ["-lineinfo", "-Xptxas", "-v" if verbose else "-O3"]
         cmd += ["-c", src, "-o", obj]

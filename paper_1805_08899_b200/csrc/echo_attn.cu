@@ -20,12 +20,34 @@
 #include <cmath>
 
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include "echo_common.cuh"
 
 namespace echo {
 
 namespace cg = cooperative_groups;
+
+#ifdef ECHO_PHASE_TIMING
+// debug-only per-CTA phase timestamps (clock64 of thread 0; slot 15 = globaltimer at start)
+__device__ unsigned long long g_echo_phase[16][8192];
+#define ECHO_PHASE(k)                                                                         \
+  do {                                                                                        \
+    if (threadIdx.x == 0) {                                                                   \
+      const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                   \
+      if (cta_ < 8192) {                                                                      \
+        g_echo_phase[k][cta_] = clock64();                                                    \
+        if ((k) == 0) {                                                                       \
+          unsigned long long gt_;                                                             \
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                             \
+          g_echo_phase[15][cta_] = gt_;                                                       \
+        }                                                                                     \
+      }                                                                                       \
+    }                                                                                         \
+  } while (0)
+#else
+#define ECHO_PHASE(k) do { } while (0)
+#endif
 
 constexpr int ATT_THREADS = 256;
 constexpr int ATT_WARPS = ATT_THREADS / 32;
@@ -450,12 +472,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 
 struct Slice {
   int C, r, a0, a1, h0, h1;   // this CTA's column ranges [a0, a1) of A and [h0, h1) of Hk
@@ -555,19 +571,19 @@ __device__ __forceinline__ void softmax_row_warp(const float* sc, float* al, int
 // ctx columns of this CTA: one thread per column; positions are split round-robin over four
 // accumulators (s mod 4) for ILP and combined in fixed order ((a0 + a1) + (a2 + a3)).
 template <typename T>
-__device__ __forceinline__ void ctx_columns(const T* hs_s, int WH, const float* al, int n, T* ctx_out, int tid) {
+__device__ __forceinline__ void ctx_columns(const T* hs_s, int ld, int WH, const float* al, int n, T* ctx_out, int tid) {
   for (int c = tid; c < WH; c += ATT_THREADS) {
     float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
     int s = 0;
     for (; s + 4 <= n; s += 4) {
-      a0 = __fmaf_rn(al[s], to_f(hs_s[(s + 0) * WH + c]), a0);
-      a1 = __fmaf_rn(al[s + 1], to_f(hs_s[(s + 1) * WH + c]), a1);
-      a2 = __fmaf_rn(al[s + 2], to_f(hs_s[(s + 2) * WH + c]), a2);
-      a3 = __fmaf_rn(al[s + 3], to_f(hs_s[(s + 3) * WH + c]), a3);
+      a0 = __fmaf_rn(al[s], to_f(hs_s[(s + 0) * ld + c]), a0);
+      a1 = __fmaf_rn(al[s + 1], to_f(hs_s[(s + 1) * ld + c]), a1);
+      a2 = __fmaf_rn(al[s + 2], to_f(hs_s[(s + 2) * ld + c]), a2);
+      a3 = __fmaf_rn(al[s + 3], to_f(hs_s[(s + 3) * ld + c]), a3);
     }
-    if (s < n) a0 = __fmaf_rn(al[s], to_f(hs_s[s * WH + c]), a0);
-    if (s + 1 < n) a1 = __fmaf_rn(al[s + 1], to_f(hs_s[(s + 1) * WH + c]), a1);
-    if (s + 2 < n) a2 = __fmaf_rn(al[s + 2], to_f(hs_s[(s + 2) * WH + c]), a2);
+    if (s < n) a0 = __fmaf_rn(al[s], to_f(hs_s[s * ld + c]), a0);
+    if (s + 1 < n) a1 = __fmaf_rn(al[s + 1], to_f(hs_s[(s + 1) * ld + c]), a1);
+    if (s + 2 < n) a2 = __fmaf_rn(al[s + 2], to_f(hs_s[(s + 2) * ld + c]), a2);
     ctx_out[c] = from_f<T>(St<T>::round(__fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3))));
   }
 }
@@ -577,43 +593,60 @@ __device__ __forceinline__ void stage_slice(float* dst, const T* __restrict__ sr
   for (int i = tid; i < n; i += ATT_THREADS) dst[i] = to_f(src[i]);
 }
 
+// ---- tensor-map TMA (cp.async.bulk.tensor) helpers
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_wait() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ size_t al128(size_t b) { return (b + 127) & ~(size_t)127; }
+
+// Shared-memory tiles: one TMA box per tensor = Ts rows x (box width) columns of this CTA's slice.
 template <typename T>
-__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, const T* __restrict__ qp,
-                                                            const T* __restrict__ Kp, const T* __restrict__ v,
-                                                            const T* __restrict__ Hs,
+__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, const __grid_constant__ CUtensorMap mK,
+                                                            const __grid_constant__ CUtensorMap mH,
+                                                            const T* __restrict__ qp, const T* __restrict__ v,
                                                             const int32_t* __restrict__ src_len, T* __restrict__ ctx,
                                                             T* __restrict__ Z_st, float* __restrict__ alpha_st) {
   cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(128) unsigned char smraw[];
+  extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar[1];
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
   const Slice g = make_slice(A, Hk, (int)cl.num_blocks(), (int)cl.block_rank());
-  const int W = g.a1 - g.a0, WH = g.h1 - g.h0;
+  const int W = g.a1 - g.a0, WH = g.h1 - g.h0;               // valid widths
+  const int Wb = tma_width(A, g.C), WHb = tma_width(Hk, g.C);  // box widths (smem row strides)
   const int Tp = (Ts + 3) & ~3;
-  T* kz = reinterpret_cast<T*>(smraw);                       // [Ts][W]
-  T* hs = kz + (size_t)Ts * W;                                // [Ts][WH]
-  float* f = reinterpret_cast<float*>(hs + (size_t)Ts * WH);
-  float* sc_part = f;                                         // [Tp]
-  float* sc = sc_part + Tp;                                   // [Tp]
-  float* al = sc + Tp;                                        // [Tp]
-  float* qps = al + Tp;                                       // [W]
-  float* vs = qps + W;                                        // [W]
+  T* kz = reinterpret_cast<T*>(smraw);                                         // [Ts][Wb]
+  T* hs = reinterpret_cast<T*>(smraw + al128((size_t)Ts * Wb * sizeof(T)));    // [Ts][WHb]
+  float* f = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(hs) + al128((size_t)Ts * WHb * sizeof(T)));
+  float* sc_part = f;
+  float* sc = sc_part + Tp;
+  float* al = sc + Tp;
+  float* qps = al + Tp;
+  float* vs = qps + Wb;
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
-  const T* kp_b = Kp + (long)b * d.kp_stride_b + g.a0;
-  const T* hs_b = Hs + (long)b * d.hs_stride_b + g.h0;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (w == 0) {
-    if (lane == 0) mbar_expect_tx(&bar[0], (uint32_t)(n * (W + WH) * sizeof(T)));
-    __syncwarp();
-    for (int s = lane; s < n; s += 32) {
-      bulk_g2s(kz + (size_t)s * W, kp_b + (long)s * d.kp_stride_s, W * sizeof(T), &bar[0]);
-      bulk_g2s(hs + (size_t)s * WH, hs_b + (long)s * d.hs_stride_s, WH * sizeof(T), &bar[0]);
-    }
+  if (tid == 0) {                                             // two TMA instructions stage the whole row slice
+    mbar_expect_tx(&bar[0], (uint32_t)((size_t)Ts * (Wb + WHb) * sizeof(T)));
+    tma_load_3d(kz, &mK, g.a0, b, 0, &bar[0]);
+    tma_load_3d(hs, &mH, g.h0, b, 0, &bar[0]);
   }
   stage_slice<T>(qps, qp + (long)b * A + g.a0, W, tid);
   stage_slice<T>(vs, v + g.a0, W, tid);
@@ -621,7 +654,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, co
   mbar_wait(&bar[0], 0);
   for (int s = w; s < n; s += ATT_WARPS) {
     T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
-    const float p = score_partial<T>(kz + (size_t)s * W, qps, vs, W, lane, true, z_out, nullptr);
+    const float p = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, true, z_out, nullptr);
     if (lane == 0) sc_part[s] = p;
   }
   if (Z_st) {                                                 // masked positions: zeros in this slice
@@ -637,62 +670,66 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, co
   __syncthreads();
   if (alpha_st && g.r == 0)
     for (int s = tid; s < Ts; s += ATT_THREADS) alpha_st[(long)b * Ts + s] = s < n ? al[s] : 0.0f;
-  ctx_columns<T>(hs, WH, al, n, ctx + (long)b * Hk + g.h0, tid);
+  ctx_columns<T>(hs, WHb, WH, al, n, ctx + (long)b * Hk + g.h0, tid);
   cluster_wait();
 }
 
 template <typename T>
-__global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, const T* __restrict__ qp,
-                                                            const T* __restrict__ Kp, const T* __restrict__ v,
-                                                            const T* __restrict__ Hs,
-                                                            const int32_t* __restrict__ src_len,
-                                                            const T* __restrict__ Z_st,
+__global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, const __grid_constant__ CUtensorMap mK,
+                                                            const __grid_constant__ CUtensorMap mH,
+                                                            const __grid_constant__ CUtensorMap mdK,
+                                                            const __grid_constant__ CUtensorMap mdH,
+                                                            const T* __restrict__ qp, const T* __restrict__ v,
+                                                            const int32_t* __restrict__ src_len, bool recompute,
                                                             const float* __restrict__ alpha_st,
                                                             const float* __restrict__ dctx, float* __restrict__ dqp,
-                                                            float* __restrict__ dKp, float* __restrict__ dHs,
                                                             float* __restrict__ dv_part, T* __restrict__ ctx_regen) {
   cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ __align__(8) uint64_t bar[1];
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bar[2];
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
   const Slice g = make_slice(A, Hk, (int)cl.num_blocks(), (int)cl.block_rank());
   const int W = g.a1 - g.a0, WH = g.h1 - g.h0;
+  const int Wb = tma_width(A, g.C), WHb = tma_width(Hk, g.C);
   const int Tp = (Ts + 3) & ~3;
-  // E [Ts][W] fp32 tanh feature map; for fp32 storage it overwrites the kz rows in place
+  // dk [Ts][Wb] f32 | dh [Ts][WHb] f32 | kz [Ts][Wb] T (E overwrites it in place for fp32) | hs [Ts][WHb] T
+  // | E [Ts][Wb] f32 (bf16 only) | floats
   constexpr bool kE_ALIAS = sizeof(T) == sizeof(float);
-  float* E = reinterpret_cast<float*>(smraw);
-  T* kz = kE_ALIAS ? reinterpret_cast<T*>(smraw) : reinterpret_cast<T*>(E + (size_t)Ts * W);  // [Ts][W] Kp or Z
-  T* hs = kz + (size_t)Ts * W;                                // [Ts][WH] Hs slice rows
-  float* f = reinterpret_cast<float*>(hs + (size_t)Ts * WH);
-  float* sc_part = f;                                         // [Tp]
-  float* dal_part = sc_part + Tp;                             // [Tp]
-  float* sc = dal_part + Tp;                                  // [Tp]
-  float* dal = sc + Tp;                                       // [Tp]
-  float* al = dal + Tp;                                       // [Tp]
-  float* dsv = al + Tp;                                       // [Tp]
-  float* qps = dsv + Tp;                                      // [W]
-  float* vs = qps + W;                                        // [W]
-  float* dcs = vs + W;                                        // [WH]
+  unsigned char* p = smraw;
+  float* dk = reinterpret_cast<float*>(p);
+  p += al128((size_t)Ts * Wb * 4);
+  float* dh = reinterpret_cast<float*>(p);
+  p += al128((size_t)Ts * WHb * 4);
+  T* kz = reinterpret_cast<T*>(p);
+  p += al128((size_t)Ts * Wb * sizeof(T));
+  T* hs = reinterpret_cast<T*>(p);
+  p += al128((size_t)Ts * WHb * sizeof(T));
+  float* E = kE_ALIAS ? reinterpret_cast<float*>(kz) : reinterpret_cast<float*>(p);
+  if (!kE_ALIAS) p += al128((size_t)Ts * Wb * 4);
+  float* sc_part = reinterpret_cast<float*>(p);
+  float* dal_part = sc_part + Tp;
+  float* sc = dal_part + Tp;
+  float* dal = sc + Tp;
+  float* al = dal + Tp;
+  float* dsv = al + Tp;
+  float* qps = dsv + Tp;
+  float* vs = qps + Wb;
+  float* dcs = vs + Wb;
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
-  const bool recompute = (Z_st == nullptr);
-  const T* kz_b = recompute ? Kp + (long)b * d.kp_stride_b + g.a0 : Z_st + (long)b * Ts * A + g.a0;
-  const long kz_ss = recompute ? d.kp_stride_s : (long)A;
-  const T* hs_b = Hs + (long)b * d.hs_stride_b + g.h0;
-  float* dkp_b = dKp + (long)b * d.kp_stride_b + g.a0;
-  float* dhs_b = dHs + (long)b * d.hs_stride_b + g.h0;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (w == 0) {                                               // TMA: every Kp/Z and Hs row slice, at once
-    if (lane == 0) mbar_expect_tx(&bar[0], (uint32_t)(n * (W + WH) * sizeof(T)));
-    __syncwarp();
-    for (int s = lane; s < n; s += 32) {
-      bulk_g2s(kz + (size_t)s * W, kz_b + (long)s * kz_ss, W * sizeof(T), &bar[0]);
-      bulk_g2s(hs + (size_t)s * WH, hs_b + (long)s * d.hs_stride_s, WH * sizeof(T), &bar[0]);
-    }
+  if (tid == 0) {                                             // four TMA instructions stage everything
+    mbar_expect_tx(&bar[0], (uint32_t)((size_t)Ts * (Wb + WHb) * sizeof(T)));
+    tma_load_3d(kz, &mK, g.a0, b, 0, &bar[0]);
+    tma_load_3d(hs, &mH, g.h0, b, 0, &bar[0]);
+    mbar_expect_tx(&bar[1], (uint32_t)((size_t)Ts * (Wb + WHb) * 4));
+    tma_load_3d(dk, &mdK, g.a0, b, 0, &bar[1]);
+    tma_load_3d(dh, &mdH, g.h0, b, 0, &bar[1]);
   }
   if (recompute) stage_slice<T>(qps, qp + (long)b * A + g.a0, W, tid);
   stage_slice<T>(vs, v + g.a0, W, tid);
@@ -701,9 +738,9 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, co
   mbar_wait(&bar[0], 0);
   // phase 1: E = tanh(z) into smem (fp32), partial scores (RECOMPUTE) and partial dalpha
   for (int s = w; s < n; s += ATT_WARPS) {
-    const float p = score_partial<T>(kz + (size_t)s * W, qps, vs, W, lane, recompute, nullptr, E + (size_t)s * W);
+    const float ps = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, recompute, nullptr, E + (size_t)s * Wb);
     float acc = 0.0f;
-    const T* hrow = hs + (size_t)s * WH;
+    const T* hrow = hs + (size_t)s * WHb;
     for (int c4 = lane; c4 < WH / 4; c4 += 32) {
       float h4[4];
       lds4(hrow + c4 * 4, h4);
@@ -712,7 +749,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, co
     }
     acc = warp_sum(acc);
     if (lane == 0) {
-      sc_part[s] = p;
+      sc_part[s] = ps;
       dal_part[s] = acc;
     }
   }
@@ -732,8 +769,9 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, co
     for (int s = lane; s < n; s += 32) dsv[s] = __fmul_rn(al[s], __fsub_rn(dal[s], acc));
   }
   __syncthreads();
-  if (recompute && ctx_regen) ctx_columns<T>(hs, WH, al, n, ctx_regen + (long)b * Hk + g.h0, tid);
-  // phase 4 (column-local, 8 positions of loads in flight per thread):
+  if (recompute && ctx_regen) ctx_columns<T>(hs, WHb, WH, al, n, ctx_regen + (long)b * Hk + g.h0, tid);
+  mbar_wait(&bar[1], 0);
+  // phase 4 (column-local, all operands in shared memory):
   //   A columns : dKp += dE ; dqp = sum_s dE ; dv_part += sum_s ds E   with dE = ds v (1 - E^2)
   //   Hk columns: dHs += alpha_s dctx
   for (int i = tid; i < W + WH; i += ATT_THREADS) {
@@ -741,23 +779,13 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, co
       const int c = i;
       const float vc = vs[c];
       float dq = 0.0f, dvv = 0.0f;
-      for (int s0 = 0; s0 < n; s0 += 8) {
-        float dk[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (s0 + u < n) dk[u] = dkp_b[(long)(s0 + u) * d.kp_stride_s + c];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int s = s0 + u;
-          if (s < n) {
-            const float e = E[(size_t)s * W + c];
-            const float ds = dsv[s];
-            const float dE = __fmul_rn(__fmul_rn(ds, vc), __fsub_rn(1.0f, __fmul_rn(e, e)));
-            dkp_b[(long)s * d.kp_stride_s + c] = __fadd_rn(dk[u], dE);
-            dq = __fadd_rn(dq, dE);
-            dvv = __fmaf_rn(ds, e, dvv);
-          }
-        }
+      for (int s = 0; s < n; ++s) {
+        const float e = E[(size_t)s * Wb + c];
+        const float ds = dsv[s];
+        const float dE = __fmul_rn(__fmul_rn(ds, vc), __fsub_rn(1.0f, __fmul_rn(e, e)));
+        dk[(size_t)s * Wb + c] = __fadd_rn(dk[(size_t)s * Wb + c], dE);
+        dq = __fadd_rn(dq, dE);
+        dvv = __fmaf_rn(ds, e, dvv);
       }
       const long o = (long)b * A + g.a0 + c;
       dqp[o] = dq;
@@ -765,16 +793,15 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, co
     } else {
       const int c = i - W;
       const float dcv = dcs[c];
-      for (int s0 = 0; s0 < n; s0 += 8) {
-        float dh[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (s0 + u < n) dh[u] = dhs_b[(long)(s0 + u) * d.hs_stride_s + c];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (s0 + u < n) dhs_b[(long)(s0 + u) * d.hs_stride_s + c] = __fmaf_rn(al[s0 + u], dcv, dh[u]);
-      }
+      for (int s = 0; s < n; ++s) dh[(size_t)s * WHb + c] = __fmaf_rn(al[s], dcv, dh[(size_t)s * WHb + c]);
     }
+  }
+  fence_proxy_async();                                         // smem writes -> visible to the TMA engine
+  __syncthreads();
+  if (tid == 0) {                                              // two TMA stores write the accumulators back
+    tma_store_3d(&mdK, g.a0, b, 0, dk);
+    tma_store_3d(&mdH, g.h0, b, 0, dh);
+    tma_store_commit_wait();
   }
   cluster_wait();
 }
@@ -805,19 +832,52 @@ static size_t bwd_smem(const echo_attn_desc* d) {
 }
 
 // TMA path: cluster size and shared-memory footprint; returns false if the generic path must run
+static size_t al128h(size_t b) { return (b + 127) & ~(size_t)127; }
 static bool tma_params(const echo_attn_desc* d, int* C, size_t* smem_fwd, size_t* smem_bwd) {
   const size_t sT = d->dtype == ECHO_FP32 ? 4 : 2;
-  if (d->A > 1024 || d->Hk > 1024) return false;
+  if (d->A > 1024 || d->Hk > 1024 || d->Ts > 256) return false;
   const int c = tma_cluster(d->A, d->Hk);
   const size_t W = tma_width(d->A, c), WH = tma_width(d->Hk, c);
   const size_t Tp = (d->Ts + 3) & ~3;
-  const size_t fwd = d->Ts * (W + WH) * sT + (3 * Tp + 2 * W) * 4;
-  const size_t bwd = d->Ts * (W * (sT == 4 ? 4 : 4 + sT) + WH * sT) + (6 * Tp + 2 * W + WH) * 4;
-  if (bwd > 200 * 1024) return false;
+  const size_t Ts = d->Ts;
+  const size_t fwd = al128h(Ts * W * sT) + al128h(Ts * WH * sT) + (3 * Tp + 2 * W) * 4;
+  const size_t bwd = al128h(Ts * W * 4) + al128h(Ts * WH * 4) + al128h(Ts * W * sT) + al128h(Ts * WH * sT) +
+                     (sT == 4 ? 0 : al128h(Ts * W * 4)) + (6 * Tp + 2 * W + WH) * 4;
+  if (bwd > 220 * 1024) return false;
   *C = c;
   *smem_fwd = fwd;
   *smem_bwd = bwd;
   return true;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 3-D map over a [Ts][B][X]-strided tensor: dims {X, B, Ts}, box {boxX, 1, Ts}
+static bool map3d(CUtensorMap* m, const void* base, bool bf16, uint64_t X, uint64_t B, uint64_t Ts, int64_t stride_b,
+                  int64_t stride_s, uint32_t boxX) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const uint64_t es = bf16 ? 2 : 4;
+  cuuint64_t dims[3] = {X, B, Ts};
+  cuuint64_t strides[2] = {(cuuint64_t)stride_b * es, (cuuint64_t)stride_s * es};
+  cuuint32_t box[3] = {boxX, 1, (cuuint32_t)Ts};
+  cuuint32_t el[3] = {1, 1, 1};
+  return fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
+            strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <typename Kern, typename... Args>
@@ -895,16 +955,20 @@ extern "C" echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, co
   cudaError_t e;
   int tC;
   size_t sf, sb;
-  if (tma_params(d, &tC, &sf, &sb)) {
+  CUtensorMap mK, mH;
+  const bool bfd = d->dtype == ECHO_BF16;
+  if (tma_params(d, &tC, &sf, &sb) &&
+      map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC)) &&
+      map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC))) {
     if (d->dtype == ECHO_FP32) {
       if ((s = set_smem((const void*)attn_fwd_tma<float>, sf, fn))) return s;
-      e = launch_cluster(attn_fwd_tma<float>, tC, d->B, sf, st, *d, (const float*)qp, (const float*)Kp, (const float*)v,
-                         (const float*)Hs, src_len, (float*)ctx, (float*)E_st, alpha_st);
+      e = launch_cluster(attn_fwd_tma<float>, tC, d->B, sf, st, *d, mK, mH, (const float*)qp, (const float*)v, src_len,
+                         (float*)ctx, (float*)E_st, alpha_st);
     } else {
       typedef __nv_bfloat16 bf;
       if ((s = set_smem((const void*)attn_fwd_tma<bf>, sf, fn))) return s;
-      e = launch_cluster(attn_fwd_tma<bf>, tC, d->B, sf, st, *d, (const bf*)qp, (const bf*)Kp, (const bf*)v,
-                         (const bf*)Hs, src_len, (bf*)ctx, (bf*)E_st, alpha_st);
+      e = launch_cluster(attn_fwd_tma<bf>, tC, d->B, sf, st, *d, mK, mH, (const bf*)qp, (const bf*)v, src_len, (bf*)ctx,
+                         (bf*)E_st, alpha_st);
     }
     if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
     return check_launch(fn);
@@ -953,18 +1017,24 @@ extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, co
   cudaError_t e;
   int tC;
   size_t sf, sb;
-  if (tma_params(d, &tC, &sf, &sb)) {
+  CUtensorMap mK, mH, mdK, mdH;
+  const bool bfd = d->dtype == ECHO_BF16;
+  const bool rec = d->mode == ECHO_RECOMPUTE;
+  if (tma_params(d, &tC, &sf, &sb) &&
+      (rec ? map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC))
+           : map3d(&mK, E_st, bfd, d->A, d->B, d->Ts, (int64_t)d->Ts * d->A, d->A, tma_width(d->A, tC))) &&
+      map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC)) &&
+      map3d(&mdK, dKp, false, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC)) &&
+      map3d(&mdH, dHs, false, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC))) {
     if (d->dtype == ECHO_FP32) {
       if ((s = set_smem((const void*)attn_bwd_tma<float>, sb, fn))) return s;
-      e = launch_cluster(attn_bwd_tma<float>, tC, d->B, sb, st, *d, (const float*)qp, (const float*)Kp, (const float*)v,
-                         (const float*)Hs, src_len, (const float*)E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part,
-                         (float*)ctx_regen);
+      e = launch_cluster(attn_bwd_tma<float>, tC, d->B, sb, st, *d, mK, mH, mdK, mdH, (const float*)qp, (const float*)v,
+                         src_len, rec, alpha_st, dctx, dqp, dv_part, (float*)ctx_regen);
     } else {
       typedef __nv_bfloat16 bf;
       if ((s = set_smem((const void*)attn_bwd_tma<bf>, sb, fn))) return s;
-      e = launch_cluster(attn_bwd_tma<bf>, tC, d->B, sb, st, *d, (const bf*)qp, (const bf*)Kp, (const bf*)v,
-                         (const bf*)Hs, src_len, (const bf*)E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part,
-                         (bf*)ctx_regen);
+      e = launch_cluster(attn_bwd_tma<bf>, tC, d->B, sb, st, *d, mK, mH, mdK, mdH, (const bf*)qp, (const bf*)v, src_len,
+                         rec, alpha_st, dctx, dqp, dv_part, (bf*)ctx_regen);
     }
     if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
     return check_launch(fn);
@@ -985,6 +1055,12 @@ extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, co
   if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);
 }
+
+#ifdef ECHO_PHASE_TIMING
+extern "C" int echo_debug_phase_times(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, echo::g_echo_phase, sizeof(unsigned long long) * (size_t)n);
+}
+#endif
 
 extern "C" echo_status echo_attn_dv_reduce(int32_t B, int32_t A, const float* dv_part, float* dv, int32_t accumulate,
                                            void* stream) {
