@@ -437,10 +437,11 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
 
 // ================================================================ TMA-staged feature-split cluster path
 // The row b is processed by a cluster of C CTAs that split the FEATURE axes: CTA r owns a
-// slice of <= 128 columns of A (and of Hk).  At kernel entry one warp issues bulk async
-// copies (cp.async.bulk, the TMA engine's 1-D mode) of every row slice this CTA needs — Kp (or
-// the stashed Z) and Hs, and in the backward also the dKp / dHs accumulators — into shared
-// memory, completing on mbarriers; so all of the CTA's HBM traffic is in flight at once.
+// slice of <= 128 columns of A (and of Hk).  At kernel entry ONE thread issues tensor-map TMA
+// loads (cp.async.bulk.tensor.3d; one box = all Ts positions x the CTA's column slice) of Kp (or
+// the stashed Z) and Hs, and in the backward also of the dKp / dHs accumulators, completing on
+// mbarriers — all of the CTA's HBM traffic is in flight at once — and the backward writes the
+// updated accumulators back with two TMA stores.
 // Per position, a warp produces the partial score (and partial dalpha) over the slice; ONE
 // cluster exchange (DSMEM) sums the partials in rank order; every CTA runs the tiny softmax
 // redundantly; ctx, dKp, dHs, dqp and dv are then column-local, one thread per column looping
