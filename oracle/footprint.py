@@ -17,8 +17,11 @@ Readings (R11-R13, R22-R25):
     stash set if G(s) is removed from the mirror path ("the storage released from
     its inputs is greater than or equal to that allocated for its outputs"); remove iff
     Rel >= Alloc.  Compute-heavy members become dead mirrors when their gradient needs no output
-    (Alg. 1 lines 13-17); binarizable members are not mirrored and their feature map
-    is kept as a 1-bit mask (line 18).
+    (Alg. 1 lines 13-17); binarizable members (relu, dropout) stay on the mirror path
+    without trimming (line 18 "insert encode and decode subroutines ...; continue"), and the
+    feature map their gradient reads is kept as a 1-bit mask: dropout's keep-mask
+    is random, so it is never recomputed — a mirrored dropout re-applies the stored mask; a relu that
+    is not mirrored keeps its output's sign bits (reading R26).
   * DeadNodeElimination removes mirrors whose outputs nobody in the backward pass reads.
   * Memory is exact integer bytes; `stack` is a view (its inputs are written into its buffer).
 This module recomputes the stash set from scratch for every decision (no incremental state) and
@@ -42,7 +45,8 @@ GRAD_DEPS = {
     "sum_reduce": (set(), set(), 1), "mul": ({0, 1}, set(), 1), "sigmoid": (set(), {0}, 1),
     "tanh": (set(), {0}, 1), "relu": (set(), {0}, 1), "dropout": (set(), {1}, 2),
     "dot_last": ({0, 1}, set(), 1), "masked_softmax": ({1}, {0}, 1), "weighted_sum": ({0, 1}, set(), 1),
-    "softmax_ce_loss": (set(), {1}, 2),
+    "softmax_ce_loss": (set(), {1}, 2), "softmax": (set(), {0}, 1), "to_heads": (set(), set(), 1),
+    "from_heads": (set(), set(), 1),
 }
 
 
@@ -74,7 +78,15 @@ class Graph:
         elif op in ("matmul",):
             out = [[S[0][0], S[1][1]]]
         elif op == "batched_dot":
-            out = [[S[0][0], S[0][1], S[1][2]]]
+            out = [[S[0][0], S[0][1], S[1][1] if a.get("trans_b") else S[1][2]]]
+        elif op == "softmax":
+            out = [list(S[0])]
+        elif op == "to_heads":
+            Bt, Hh = a["batch"], a["heads"]
+            out = [[Bt * Hh, S[0][0] // Bt, S[0][1] // Hh]]
+        elif op == "from_heads":
+            Hh = a["heads"]
+            out = [[S[0][0] // Hh * S[0][1], Hh * S[0][2]]]
         elif op == "embedding":
             out = [S[0] + [S[1][1]]]
         elif op == "slice":
@@ -88,7 +100,7 @@ class Graph:
         elif op in ("add", "mul", "sigmoid", "tanh", "relu"):
             out = [list(S[0])]
         elif op == "dropout":
-            out = [list(S[0]), list(S[0])]
+            out = [list(S[0]), list(S[0])]                  # y, keep-mask (u8)
         elif op == "broadcast_add":
             out = [list(S[1])]
         elif op == "stack":
@@ -117,6 +129,8 @@ class Graph:
             d = dt
             if op == "softmax_ce_loss":
                 d = "f32"
+            if op == "dropout" and k == 1:
+                d = "u8"
             self.dtype[(n["id"], k)] = d
 
     # -------------------------------------------------------------- helpers
@@ -133,6 +147,10 @@ class Graph:
         if bit:
             return math.ceil(self.numel(e) / 8)
         return math.ceil(self.numel(e) * WIDTH[self.dtype[e]])
+
+    def is_random(self, e):
+        """dropout's keep-mask: random state, never recomputable."""
+        return e[0] in self.nodes and self.nodes[e[0]]["op"] == "dropout" and e[1] == 1
 
     def n_out(self, i):
         return GRAD_DEPS[self.nodes[i]["op"]][2]
@@ -157,7 +175,7 @@ class Graph:
             return 2 * self.shape[ins[0]][0] * self.shape[ins[0]][1] * self.shape[ins[1]][1]
         if op == "batched_dot":
             s = self.shape[ins[0]]
-            return 2 * s[0] * s[1] * s[2] * self.shape[ins[1]][2]
+            return 2 * s[0] * s[1] * s[2] * self.numel(o) // (s[0] * s[1])
         if op in ("dot_last", "weighted_sum"):
             return 2 * self.numel(ins[1] if op == "weighted_sum" else ins[0])
         if op == "dropout":
@@ -207,13 +225,14 @@ def stash_set(G, M, st):
     for i in G.order:
         n = G.nodes[i]
         heavy_orig = st.is_heavy(G, i) and not st.dead      # heavy grad reads the ORIGINAL inputs
-        binz = st.binarize and n["op"] in st.binarizable and i not in M
         for e in G.grad_refs(i):
             if G.trainable(e):
                 continue
-            if e[0] in M and not heavy_orig:
+            p = e[0]
+            rnd = G.is_random(e)
+            if p in M and not heavy_orig and not rnd:
                 continue                                    # gradient reads the recomputed copy
-            bit = binz and e[0] == i
+            bit = st.binarize and (rnd or (p == i and p not in M and n["op"] in st.binarizable))
             S[e] = S.get(e, True) and bit
         if i in M:
             for e in n["inputs"]:
@@ -221,6 +240,9 @@ def stash_set(G, M, st):
                 if e[0] in M or G.trainable(e):
                     continue
                 S[e] = False                                # needed at full precision to recompute i
+            for e in G.outs(i):
+                if G.is_random(e):                          # a mirrored dropout re-applies its stored mask
+                    S[e] = S.get(e, True) and st.binarize
     return S
 
 
@@ -278,10 +300,11 @@ def run_echo(G, st):
     subs = partition(G, st)
     M = set()
     for S in subs:                                          # create every recomputation path
-        M |= {s for s in S if not st.is_heavy(G, s) and G.nodes[s]["op"] not in st.binarizable}
+        M |= {s for s in S if not st.is_heavy(G, s)}
+    binz = lambda i: G.nodes[i]["op"] in st.binarizable
     for S in subs:                                          # forward trimming, subgraph by subgraph
         for s in S:                                         # ... in topological order
-            if s not in M:
+            if s not in M or binz(s):                       # Alg. 1 line 18: binarizable -> continue
                 continue
             group = {s}
             cur = stash_set(G, M, st)
@@ -294,7 +317,7 @@ def run_echo(G, st):
                         if e not in cur:
                             continue
                         for c in G.consumers.get(e, []):
-                            if c in M and c not in group:
+                            if c in M and c not in group and not binz(c):
                                 group.add(c)
                                 changed = True
             after = stash_set(G, M - group, st)
@@ -318,7 +341,7 @@ def run_echo(G, st):
 def run_mirror(G, st):
     """Chen et al. 'Mirror': every cheap node is mirrored, heavy gradients keep
     their original inputs, no footprint check; useless mirrors are then eliminated."""
-    M = {i for i in G.order if not st.is_heavy(G, i) and G.nodes[i]["op"] not in st.binarizable}
+    M = {i for i in G.order if not st.is_heavy(G, i)}
     return dead_node_elimination(G, M, st), [], []
 
 
@@ -336,7 +359,7 @@ def dead_node_elimination(G, M, st):
     while changed:
         changed = False
         for m in sorted(M, reverse=True):
-            if not any(needed_in_backward(G, M, st, e) for e in G.outs(m)):
+            if not any(needed_in_backward(G, M, st, e) for e in G.outs(m) if not G.is_random(e)):
                 M.discard(m)
                 changed = True
     return M
@@ -361,8 +384,9 @@ def exhaustive_min_stash(doc, cfg=None, limit=16):
     """Brute force over all 2^|cheap| mirror sets (tiny graphs): the optimum stash bytes."""
     G = Graph(doc)
     st = Strategy(cfg)
-    cand = [i for i in G.order if not st.is_heavy(G, i) and G.nodes[i]["op"] not in st.binarizable]
-    assert len(cand) <= limit
+    cand = [i for i in G.order if not st.is_heavy(G, i)]
+    if len(cand) > limit:
+        return None
     best = None
     for r in range(len(cand) + 1):
         for sub in itertools.combinations(cand, r):
@@ -380,7 +404,7 @@ def schedule(G, M, st):
 
     def need_mirrors(edges):
         out = []
-        stack = [e[0] for e in edges if e[0] in M]
+        stack = [e[0] for e in edges if e[0] in M and not G.is_random(e)]
         seen = set()
         while stack:
             m = stack.pop()
@@ -421,11 +445,13 @@ def live_timeline(G, M, S, st):
         u = []
         for i in G.order:
             heavy_orig = st.is_heavy(G, i) and not st.dead
-            if e in G.grad_refs(i) and (e[0] not in M or heavy_orig):
+            if e in G.grad_refs(i) and (e[0] not in M or heavy_orig or G.is_random(e)):
                 u.append(pos[("grad", i)])
         for c in G.consumers.get(e, []):
             if c in M:
                 u.append(pos[("mirror", c)])
+        if G.is_random(e) and e[0] in M:
+            u.append(pos[("mirror", e[0])])                 # the mirror re-applies the stored mask
         return u
 
     # forward outputs (a stack input lives inside the stack's buffer)
@@ -445,6 +471,8 @@ def live_timeline(G, M, S, st):
     # recomputed outputs
     for m in M:
         for e in G.outs(m):
+            if G.is_random(e):
+                continue
             uses = [pos[("grad", i)] for i in G.order if e in G.grad_refs(i) and not (st.is_heavy(G, i) and not st.dead)]
             uses += [pos[("mirror", c)] for c in G.consumers.get(e, []) if c in M]
             if uses:

@@ -156,7 +156,7 @@ std::string jstr(const std::string& s) {
 // ============================================================================ graph model
 enum Op {
   FC, MATMUL, BDOT, EMBED, SLICE, ADD, BADD, STACK, CONCAT, SUM, MUL, SIGMOID, TANH, RELU, DROPOUT, DOTLAST,
-  MSOFTMAX, WSUM, CE, N_OPS
+  MSOFTMAX, WSUM, CE, SOFTMAX, TO_HEADS, FROM_HEADS, N_OPS
 };
 struct OpInfo {
   const char* name;
@@ -172,6 +172,7 @@ const OpInfo OPS[N_OPS] = {
     {"tanh", 1, 1, 1, 0, 0b1},             {"relu", 1, 1, 1, 0, 0b1},      {"dropout", 1, 1, 2, 0, 0b10},
     {"dot_last", 2, 2, 1, 0b11, 0},        {"masked_softmax", 2, 2, 1, 0b10, 0b1},
     {"weighted_sum", 2, 2, 1, 0b11, 0},    {"softmax_ce_loss", 2, 2, 2, 0, 0b10},
+    {"softmax", 1, 1, 1, 0, 0b1},          {"to_heads", 1, 1, 1, 0, 0},    {"from_heads", 1, 1, 1, 0, 0},
 };
 
 double dtype_width(const std::string& d) {
@@ -252,10 +253,26 @@ void infer(Graph& g, Node& n) {
       need(I[0]->shape.size() == 2 && I[1]->shape.size() == 2 && I[0]->shape[1] == I[1]->shape[0], "[m,k]x[k,n]");
       out.push_back({I[0]->shape[0], I[1]->shape[1]});
       break;
-    case BDOT:
-      need(I[0]->shape.size() == 3 && I[1]->shape.size() == 3 && I[0]->shape[2] == I[1]->shape[1], "[b,m,k]x[b,k,n]");
-      out.push_back({I[0]->shape[0], I[0]->shape[1], I[1]->shape[2]});
+    case BDOT: {
+      const bool tb = attr_int(n, "trans_b", 0) != 0;
+      need(I[0]->shape.size() == 3 && I[1]->shape.size() == 3 && I[0]->shape[2] == I[1]->shape[tb ? 2 : 1],
+           "[b,m,k]x[b,k,n] (or [b,n,k] with trans_b)");
+      out.push_back({I[0]->shape[0], I[0]->shape[1], I[1]->shape[tb ? 1 : 2]});
       break;
+    }
+    case SOFTMAX: out.push_back(I[0]->shape); break;
+    case TO_HEADS: {
+      const int64_t Bt = attr_int(n, "batch", 1), Hh = attr_int(n, "heads", 1);
+      need(I[0]->shape.size() == 2 && Bt > 0 && Hh > 0 && I[0]->shape[0] % Bt == 0 && I[0]->shape[1] % Hh == 0, "[B*L, d]");
+      out.push_back({Bt * Hh, I[0]->shape[0] / Bt, I[0]->shape[1] / Hh});
+      break;
+    }
+    case FROM_HEADS: {
+      const int64_t Hh = attr_int(n, "heads", 1);
+      need(I[0]->shape.size() == 3 && Hh > 0 && I[0]->shape[0] % Hh == 0, "[B*H, L, dh]");
+      out.push_back({I[0]->shape[0] / Hh * I[0]->shape[1], Hh * I[0]->shape[2]});
+      break;
+    }
     case EMBED: {
       need(I[1]->shape.size() == 2, "table [V,E]");
       auto s = I[0]->shape;
@@ -319,7 +336,7 @@ void infer(Graph& g, Node& n) {
   if (dt.empty()) dt = n.op == EMBED ? I[1]->dtype : I[0]->dtype;
   dtype_width(dt);
   for (size_t k = 0; k < out.size(); ++k) {
-    Edge e{n.id, (int)k, out[k], n.op == CE ? std::string("f32") : dt};
+    Edge e{n.id, (int)k, out[k], n.op == CE ? std::string("f32") : (n.op == DROPOUT && k == 1 ? std::string("u8") : dt)};
     for (auto s : e.shape) need(s >= 1, "non-positive dim");
     g.edge_of[{n.id, (int)k}] = (int)g.edges.size();
     n.out.push_back((int)g.edges.size());
@@ -468,7 +485,7 @@ int64_t flops(const Graph& g, const Node& n) {
   switch (n.op) {
     case FC: return 2 * o.numel() * E(0).shape.back();
     case MATMUL: return 2 * E(0).shape[0] * E(0).shape[1] * E(1).shape[1];
-    case BDOT: return 2 * E(0).shape[0] * E(0).shape[1] * E(0).shape[2] * E(1).shape[2];
+    case BDOT: return 2 * E(0).shape[0] * E(0).shape[1] * E(0).shape[2] * (o.numel() / (E(0).shape[0] * E(0).shape[1]));
     case DOTLAST: return 2 * E(0).numel();
     case WSUM: return 2 * E(1).numel();
     case DROPOUT: return 2 * o.numel();
@@ -500,21 +517,31 @@ struct Analysis {
     const Node& p = g.nodes[g.edges[e].node];
     return p.placeholder && p.trainable;
   }
+  // dropout's keep-mask: random state, never recomputed (reading R26)
+  bool is_random(int e) const {
+    const Node& p = g.nodes[g.edges[e].node];
+    return !p.placeholder && p.op == DROPOUT && g.edges[e].out == 1;
+  }
   // 0: not stashed, 1: stashed at full precision, 2: stashed as a 1-bit mask
   int status(int e) const {
     if (trainable(e)) return 0;
     const int p = g.edges[e].node;
     const bool pm = mirrored[p];
+    const bool rnd = is_random(e);
     int st = 0;
     for (int r : g.grad_readers[e]) {
-      if (pm && !heavy_orig[r]) continue;                    // gradient reads the recomputed copy
-      const bool bit = cfg.binarize && binz[r] && !mirrored[r] && p == r;
+      if (pm && !heavy_orig[r] && !rnd) continue;            // gradient reads the recomputed copy
+      const bool bit = cfg.binarize && (rnd || (p == r && !mirrored[r] && binz[r]));
       if (!bit) return 1;
       st = 2;
     }
     if (!pm)
       for (int c : g.consumers[e])
         if (mirrored[c]) return 1;                           // needed to recompute c
+    if (rnd && pm) {                                         // a mirrored dropout re-applies its mask
+      if (!cfg.binarize) return 1;
+      st = 2;
+    }
     return st;
   }
   int64_t status_bytes(int e, int st) const { return st == 0 ? 0 : g.edges[e].bytes(st == 2); }
@@ -566,7 +593,7 @@ void dead_node_elimination(const Graph& g, Analysis& a) {
       int m = *it;
       if (!a.mirrored[m]) continue;
       bool need = false;
-      for (int e : g.nodes[m].out) need = need || a.needed_in_backward(e);
+      for (int e : g.nodes[m].out) need = need || (!a.is_random(e) && a.needed_in_backward(e));
       if (!need) { a.mirrored[m] = 0; changed = true; }
     }
   }
@@ -582,12 +609,12 @@ Result run_echo(const Graph& g, Analysis& a) {
   r.subs = partition(g, a);
   for (auto& S : r.subs)
     for (int s : S)
-      if (!a.heavy[s] && !a.binz[s]) a.mirrored[s] = 1;
+      if (!a.heavy[s]) a.mirrored[s] = 1;                         // binarizable nodes included (line 18)
   std::vector<int> mark(g.edges.size(), 0), gmark(g.nodes.size(), 0);
   int stamp = 0;
   for (auto& S : r.subs) {
     for (int s : S) {
-      if (!a.mirrored[s]) continue;
+      if (!a.mirrored[s] || a.binz[s]) continue;                  // Alg. 1 line 18: binarizable -> continue
       ++stamp;
       std::vector<int> group{s};
       gmark[s] = stamp;
@@ -595,7 +622,7 @@ Result run_echo(const Graph& g, Analysis& a) {
         for (int e : g.nodes[group[k]].in) {
           if (a.status(e) == 0) continue;
           for (int c : g.consumers[e])
-            if (a.mirrored[c] && gmark[c] != stamp) { gmark[c] = stamp; group.push_back(c); }
+            if (a.mirrored[c] && !a.binz[c] && gmark[c] != stamp) { gmark[c] = stamp; group.push_back(c); }
         }
       }
       std::vector<int> aff;                                       // edges whose status can change
@@ -630,7 +657,7 @@ Result run_echo(const Graph& g, Analysis& a) {
 
 void run_mirror(const Graph& g, Analysis& a) {
   for (int i : g.order)
-    if (!a.heavy[i] && !a.binz[i]) a.mirrored[i] = 1;
+    if (!a.heavy[i]) a.mirrored[i] = 1;
   dead_node_elimination(g, a);
 }
 
@@ -655,9 +682,9 @@ Plan plan(const Graph& g, const Analysis& a, const std::vector<int>& st) {
       std::vector<char> seen(0);
       std::set<int> seen_s;
       for (size_t q = 0; q < n.in.size(); ++q)
-        if (q < 32 && (OPS[n.op].needs_in >> q) & 1u) stack.push_back(g.edges[n.in[q]].node);
+        if (q < 32 && (OPS[n.op].needs_in >> q) & 1u && !a.is_random(n.in[q])) stack.push_back(g.edges[n.in[q]].node);
       for (size_t q = 0; q < n.out.size(); ++q)
-        if ((OPS[n.op].needs_out >> q) & 1u) stack.push_back(i);
+        if ((OPS[n.op].needs_out >> q) & 1u && !a.is_random(n.out[q])) stack.push_back(i);
       while (!stack.empty()) {
         int m = stack.back();
         stack.pop_back();
@@ -681,10 +708,12 @@ Plan plan(const Graph& g, const Analysis& a, const std::vector<int>& st) {
       int last = fwd_pos[i];
       for (int c : g.consumers[e]) last = std::max(last, fwd_pos[c]);
       if (st[e]) {
+        const bool rnd = a.is_random(e);
         for (int r : g.grad_readers[e])
-          if (!a.mirrored[g.edges[e].node] || a.heavy_orig[r]) last = std::max(last, grad_pos[r]);
+          if (!a.mirrored[g.edges[e].node] || a.heavy_orig[r] || rnd) last = std::max(last, grad_pos[r]);
         for (int c : g.consumers[e])
           if (a.mirrored[c]) last = std::max(last, mir_pos[c]);
+        if (rnd && a.mirrored[i]) last = std::max(last, mir_pos[i]);
       }
       lo[e] = fwd_pos[i];
       hi[e] = last;
@@ -700,6 +729,7 @@ Plan plan(const Graph& g, const Analysis& a, const std::vector<int>& st) {
   for (int m : g.order) {
     if (!a.mirrored[m]) continue;
     for (int e : g.nodes[m].out) {
+      if (a.is_random(e)) continue;
       int last = -1;
       for (int r : g.grad_readers[e]) if (!a.heavy_orig[r]) last = std::max(last, grad_pos[r]);
       for (int c : g.consumers[e]) if (a.mirrored[c]) last = std::max(last, mir_pos[c]);

@@ -67,5 +67,7 @@ C2 = NMTConfig("C2-nmt", B=128, Ts=50, Td=50, E=512, H=512, A=512, V=8192, enc_l
 SMALL_NMT = NMTConfig("small-nmt", B=4, Ts=8, Td=8, E=32, H=32, A=32, V=64, enc_layers=2, dec_layers=2)
 C3 = DS2Config("C3-ds2", B=32, T=400, F=1600, H=800, layers=5)
 C4 = TXConfig("C4-tx", B=64, L=256, d_model=512, heads=8, blocks=6)
+SMALL_TX = TXConfig("small-tx", B=2, L=24, d_model=32, heads=4, blocks=2, dropout_p=0.1)
+SMALL_DS2 = DS2Config("small-ds2", B=3, T=7, F=24, H=16, layers=2)
 
 NMT_CONFIGS = {c.name: c for c in (C1, SMALL_NMT, C2)}

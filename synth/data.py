@@ -185,3 +185,27 @@ def ds2_batch(seed, cfg: DS2Config, storage="fp32"):
     g = rng(seed)
     return {"x": as_storage(normal(g, (cfg.T, cfg.B, cfg.F)), storage),
             "labels": g.integers(0, cfg.classes, size=(cfg.T, cfg.B)).astype(np.int64)}
+
+
+# ----------------------------------------------------------------------------- Transformer attention blocks
+def tx_param_shapes(cfg):
+    d = cfg.d_model
+    shapes = []
+    for k in range(cfg.blocks):
+        shapes += [(f"b{k}.Wq", (d, d)), (f"b{k}.Wk", (d, d)), (f"b{k}.Wv", (d, d)), (f"b{k}.Wo", (d, d))]
+    shapes += [("out.r", (d,))]
+    return shapes
+
+
+def tx_params(seed, cfg, storage="fp32"):
+    g = rng(seed)
+    k = 1.0 / np.sqrt(cfg.d_model)
+    return {name: as_storage(uniform(g, shape, k) if name != "out.r" else normal(g, shape), storage)
+            for name, shape in tx_param_shapes(cfg)}
+
+
+def tx_batch(seed, cfg, storage="fp32"):
+    """x [B, L, d] ~ N(0,1); per-block dropout seeds."""
+    g = rng(seed)
+    return {"x": as_storage(normal(g, (cfg.B, cfg.L, cfg.d_model)), storage),
+            "seeds": [int(s) for s in g.integers(1, 2 ** 40, size=cfg.blocks)]}

@@ -239,6 +239,30 @@ def nmt(cfg, s="f32"):
     return g.doc()
 
 
+def transformer(cfg, s="f32"):
+    """Transformer attention-block stack with the op structure of the GPU path
+    (paper_1805_08899_b200/transformer.py): per block q,k,v = FC(x); heads; S = batched_dot(qh, kh^T);
+    P = softmax(S) (scale folded); (P_d, mask) = dropout(P); O = from_heads(batched_dot(P_d, vh));
+    y = FC(O, Wo) + x.  Loss = sum(FC(y_final, r))."""
+    B, L, d, H = cfg.B, cfg.L, cfg.d_model, cfg.heads
+    N = B * L
+    g = GraphBuilder()
+    x = g.placeholder("x", [N, d], s)
+    for k in range(cfg.blocks):
+        W = {n: g.placeholder(f"b{k}.{n}", [d, d], s, trainable=True) for n in ("Wq", "Wk", "Wv", "Wo")}
+        q, kk, v = (g.op("fully_connected", [x, W[n]], tag="tx") for n in ("Wq", "Wk", "Wv"))
+        qh, kh, vh = (g.op("to_heads", [e], tag="tx", batch=B, heads=H) for e in (q, kk, v))
+        S = g.op("batched_dot", [qh, kh], tag="attention", trans_b=1)
+        P = g.op("softmax", [S], tag="attention")
+        Pd, _mask = g.op("dropout", [P], tag="attention", nout=2, p=cfg.dropout_p)
+        Oh = g.op("batched_dot", [Pd, vh], tag="attention")
+        O = g.op("from_heads", [Oh], tag="tx", heads=H)
+        x = g.op("add", [g.op("fully_connected", [O, W["Wo"]], tag="tx"), x], tag="tx")
+    r = g.placeholder("out.r", [1, d], s, trainable=True)
+    g.output(g.op("sum_reduce", [g.op("fully_connected", [x, r], tag="output")]))
+    return g.doc()
+
+
 # ----------------------------------------------------------------------------- random graphs
 CHEAP_UNARY = ["tanh", "sigmoid", "relu"]
 CHEAP_BINARY = ["add", "mul"]

@@ -128,11 +128,14 @@ def test_echo_vs_exhaustive_optimum():
     mirror subsets, and reaches it on the paper's examples."""
     for doc in (Gr.add_tanh(64), Gr.chain4(16), Gr.broadcast_attn(4, 8), Gr.tanh_fc(4, 8)):
         assert F.analyze(doc)["stash_bytes"] == F.exhaustive_min_stash(doc)
-    for seed in range(30):
+    checked = 0
+    for seed in range(40):
         doc = Gr.random_graph(seed, max_nodes=12)
-        opt = F.exhaustive_min_stash(doc, limit=14) if sum(1 for n in doc["nodes"]) <= 18 else None
+        opt = F.exhaustive_min_stash(doc, limit=14)
         if opt is not None:
+            checked += 1
             assert F.analyze(doc)["stash_bytes"] >= opt
+    assert checked >= 10
 
 
 def test_planner_matches_bruteforce_on_c2(est):

@@ -1,0 +1,66 @@
+"""Transformer attention blocks (a7 + cuBLAS) vs the fp64 oracle; STASH == RECOMPUTE bit-identity;
+GPU stash bytes == estimator (Baseline / Echo plans)."""
+import json
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import transformer as O
+from synth.configs import SMALL_TX, C4
+from synth.data import tx_params, tx_batch
+from tests.gpu_util import relerr, relerr_fro, bits_equal
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _strict_fp32():
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+
+def _run(cfg, params, batch, dtype, mode):
+    from paper_1805_08899_b200.transformer import TXModel
+    m = TXModel(cfg, dtype, mode)
+    m.load_params(params)
+    m.upload_batch(batch)
+    return m, m.train_step(lr=0.0)
+
+
+@pytest.mark.parametrize("cfg,storage", [(SMALL_TX, "fp32"), (SMALL_TX, "bf16"),
+                                         (replace(C4, blocks=2), "fp32")], ids=["small-fp32", "small-bf16", "C4x2-fp32"])
+def test_tx_parity_and_bit_identity(cfg, storage, cuda_dev):
+    from paper_1805_08899_b200 import abi
+    params = tx_params(1, cfg, storage)
+    batch = tx_batch(2, cfg, storage)
+    ref = O.step(params, batch, cfg)
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    tol = 1e-4 if storage == "fp32" else 2e-2
+    metric = relerr if storage == "fp32" else relerr_fro
+    res = {}
+    for mode in (abi.STASH, abi.RECOMPUTE):
+        m, loss = _run(cfg, params, batch, dt, mode)
+        assert abs(loss - ref["loss"]) <= tol * max(abs(ref["loss"]), 1e-3), (loss, ref["loss"])
+        g = m.grads_numpy()
+        for k, v in ref["grads"].items():
+            assert metric(g[k], v) <= tol, (k, metric(g[k], v))
+        res[mode] = m.gflat.clone()
+    assert bits_equal(res[abi.STASH], res[abi.RECOMPUTE])
+
+
+@pytest.mark.parametrize("cfg", [SMALL_TX, C4], ids=lambda c: c.name)
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+def test_tx_stash_bytes_equal_estimator(cfg, storage, cuda_dev):
+    from paper_1805_08899_b200 import abi
+    from paper_1805_08899_b200.transformer import TXModel
+    from synth import graphs as Gr
+    doc = json.dumps(Gr.transformer(cfg, "f32" if storage == "fp32" else "bf16"))
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    for mode, strat in ((abi.STASH, "baseline"), (abi.RECOMPUTE, "echo")):
+        rep = json.loads(abi.echo_footprint_estimate(doc, json.dumps({"strategy": strat})))
+        m = TXModel(cfg, dt, mode)
+        m.upload_batch(tx_batch(0, cfg, storage))
+        acts = m._forward()
+        assert m.stash_bytes() == rep["stash_bytes"], (strat, m.stash_bytes(), rep["stash_bytes"])
+        del acts
