@@ -1,0 +1,198 @@
+"""DeepSpeech2-shaped bidirectional LSTM stack on the Echo ABI (BASELINE.json configs[2]).
+
+PAPER.md §6.3.1 (lines 946-953); reading R21: input x [T,B,F] stands in for the conv front-end,
+5 bidirectional LSTM layers whose two directions are concatenated (applied as split FCs, no concat
+buffer), a per-frame linear layer to 29 classes and mean softmax cross-entropy.  Each direction of
+each layer is an LSTMLayer (the reverse one processes t = T-1..0), so the hot path is a1/a2/a3.
+
+STASH keeps every LSTM feature map (gates, c, tanh c, h); RECOMPUTE (Echo's plan) keeps the gates
+and regenerates the c-chain, tanh(c) and h — including the layer outputs the layer above and the
+output FC read, whose weight gradients are therefore deferred until the regenerating backward
+(the dead-node FC of PAPER.md:672).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import abi
+from .gemm import mm, addmm_
+from .lstm import LSTMLayer, TORCH_DTYPE
+from synth.data import ds2_param_shapes
+
+
+class DS2Model:
+    def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda"):
+        abi.load()
+        self.cfg, self.dtype, self.mode = cfg, dtype, mode
+        self.sd = TORCH_DTYPE[dtype]
+        self.device = torch.device(device)
+        self.shapes = ds2_param_shapes(cfg)
+        n = sum(int(np.prod(s)) for _, s in self.shapes)
+        self.master = torch.zeros(n, dtype=torch.float32, device=self.device)
+        self.gflat = torch.zeros(n, dtype=torch.float32, device=self.device)
+        self.sflat = self.master if dtype == abi.FP32 else torch.zeros(n, dtype=self.sd, device=self.device)
+        self.P, self.G, self.S = {}, {}, {}
+        off = 0
+        for name, shape in self.shapes:
+            k = int(np.prod(shape))
+            self.P[name] = self.master[off:off + k].view(shape)
+            self.G[name] = self.gflat[off:off + k].view(shape)
+            self.S[name] = self.sflat[off:off + k].view(shape)
+            off += k
+        T, B, H = cfg.T, cfg.B, cfg.H
+        self.x = torch.zeros(T, B, cfg.F, dtype=self.sd, device=self.device)
+        self.labels = torch.zeros(T * B, dtype=torch.int64, device=self.device)
+        self.zero_h = torch.zeros(B, H, dtype=self.sd, device=self.device)
+        self.zero_c = torch.zeros(B, H, dtype=torch.float32, device=self.device)
+        self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
+        self.stash = {}
+        self.grad_hook = None
+        self.graph = None
+
+    def load_params(self, params):
+        for name, _ in self.shapes:
+            self.P[name].copy_(torch.from_numpy(np.asarray(params[name], np.float32)))
+        if self.sflat is not self.master:
+            self.sflat.copy_(self.master)
+
+    def upload_batch(self, batch):
+        x = batch["x"] if isinstance(batch["x"], torch.Tensor) else torch.from_numpy(np.ascontiguousarray(batch["x"]))
+        lab = batch["labels"] if isinstance(batch["labels"], torch.Tensor) else torch.from_numpy(batch["labels"])
+        self.x.copy_(x.to(self.sd), non_blocking=True)
+        self.labels.copy_(lab.reshape(-1), non_blocking=True)
+
+    def input_bytes(self):
+        return self.x.numel() * self.x.element_size() + self.labels.numel() * 8
+
+    def grads_numpy(self):
+        return {k: v.detach().double().cpu().numpy() for k, v in self.G.items()}
+
+    def stash_bytes(self):
+        seen, total = set(), 0
+        for t in self.stash.values():
+            key = (t.data_ptr(), t.numel())
+            if key not in seen:
+                seen.add(key)
+                total += t.numel() * t.element_size()
+        return total
+
+    def train_step(self, lr=0.1):
+        self.step(lr)
+        return float(self.loss.item())
+
+    def step(self, lr=0.1):
+        acts = self._forward()
+        self._backward(acts)
+        del acts
+        if self.grad_hook is not None:
+            self.grad_hook(self.gflat)
+        if lr != 0.0:
+            self.master.add_(self.gflat, alpha=-lr)
+            if self.sflat is not self.master:
+                self.sflat.copy_(self.master)
+
+    def capture(self, lr=0.1, warmup=2):
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.step(lr)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.step(lr)
+        torch.cuda.synchronize(self.device)
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()
+
+    def _inputs(self, l, low):
+        """(X_i, W_i) input projections of layer l for one direction's Wx."""
+        H = self.cfg.H
+        return lambda W: [(self.x, W)] if l == 0 else [(low[0], W[:, :H]), (low[1], W[:, H:])]
+
+    def _forward(self):
+        c, sd, dev, md = self.cfg, self.sd, self.device, self.mode
+        T, B, H, V = c.T, c.B, c.H, c.classes
+        layers = []
+        low = None
+        for l in range(c.layers):
+            pair = []
+            for d, rev in (("fw", False), ("bw", True)):
+                L = LSTMLayer(T, B, H, self.dtype, md, dev, reverse=rev)
+                Wx = self.S[f"l{l}.{d}.Wx"]
+                ins = [(self.x, Wx)] if l == 0 else [(low[0].h, Wx[:, :H]), (low[1].h, Wx[:, H:])]
+                L.forward_multi(ins, self.S[f"l{l}.{d}.Wh"], self.P[f"l{l}.{d}.b"], self.zero_h, self.zero_c)
+                pair.append(L)
+            if md == abi.RECOMPUTE and low is not None:
+                low[0].h = low[1].h = None                    # lower outputs only fed the input FCs
+            layers.append(pair)
+            low = pair
+        N = T * B
+        Wo = self.S["out.W"]
+        logits = mm(low[0].h.reshape(N, H), Wo[:, :H].t(), torch.float32)
+        logits.add_(mm(low[1].h.reshape(N, H), Wo[:, H:].t(), torch.float32))
+        logits.add_(self.P["out.b"])
+        if md == abi.RECOMPUTE:
+            low[0].h = low[1].h = None
+        y = self.labels
+        lse = torch.logsumexp(logits, dim=1)
+        torch.sub(lse.sum(), logits.gather(1, y[:, None]).sum(), out=self.loss)
+        self.loss.div_(N)
+        logits.sub_(lse[:, None]).exp_()
+        logits.scatter_add_(1, y[:, None], torch.full((N, 1), -1.0, device=dev))
+        logits.div_(N)
+        reg = {"x": self.x, "h0": self.zero_h, "c0": self.zero_c, "ce_probs": logits}
+        for l, pair in enumerate(layers):
+            for d, L in zip(("fw", "bw"), pair):
+                for k, t in L.stash_views().items():
+                    reg[f"l{l}.{d}.{k}"] = t
+        self.stash = reg
+        return {"layers": layers, "dlogits": logits}
+
+    def _backward(self, a):
+        c, sd = self.cfg, self.sd
+        T, B, H = c.T, c.B, c.H
+        N = T * B
+        G = self.G
+        self.gflat.zero_()
+        dlog = a["dlogits"]
+        dlog_s = dlog if sd == torch.float32 else dlog.to(sd)
+        G["out.b"].copy_(dlog.sum(0))
+        Wo = self.S["out.W"]
+        dH = [mm(dlog_s, Wo[:, :H], torch.float32).view(T, B, H), mm(dlog_s, Wo[:, H:], torch.float32).view(T, B, H)]
+        layers = a["layers"]
+        above = None                                          # (layer pair, its weights) awaiting input dW
+        for l in reversed(range(c.layers)):
+            pair = layers[l]
+            dX = None
+            for j, (d, L) in enumerate(zip(("fw", "bw"), pair)):
+                Wx = self.S[f"l{l}.{d}.Wx"]
+                ins = [(None, Wx)] if l == 0 else [(None, Wx[:, :H]), (None, Wx[:, H:])]
+                r = L.backward_multi(ins, self.S[f"l{l}.{d}.Wh"], dH[j], need_dX=l > 0, need_dW=False, release=False)
+                G[f"l{l}.{d}.Wh"].copy_(r["dWh"])
+                G[f"l{l}.{d}.b"].copy_(r["db"])
+                if l > 0:
+                    dX = r["dX"] if dX is None else [dX[0].add_(r["dX"][0]), dX[1].add_(r["dX"][1])]
+            outs = [pair[0].h_time(), pair[1].h_time()]         # stashed, or regenerated by a3
+            if above is None:                                  # output FC (deferred dW, Eq. 2)
+                G["out.W"][:, :H].copy_(mm(dlog_s.t(), outs[0].reshape(N, H), torch.float32))
+                G["out.W"][:, H:].copy_(mm(dlog_s.t(), outs[1].reshape(N, H), torch.float32))
+            else:
+                lu = l + 1
+                for d, U in zip(("fw", "bw"), above):
+                    dW = U.input_weight_grads(outs)
+                    G[f"l{lu}.{d}.Wx"][:, :H].copy_(dW[0])
+                    G[f"l{lu}.{d}.Wx"][:, H:].copy_(dW[1])
+                    U.release_backward()
+                    U.gates = None
+            del outs
+            above = pair
+            dH = dX
+        for d, U in zip(("fw", "bw"), above):
+            G[f"l0.{d}.Wx"].copy_(U.input_weight_grads([self.x])[0])
+            U.release_backward()
+        a["layers"] = None

@@ -239,6 +239,53 @@ def nmt(cfg, s="f32"):
     return g.doc()
 
 
+def ds2(cfg, s="f32"):
+    """DeepSpeech2-shaped bidirectional LSTM stack with the op structure of the GPU path
+    (paper_1805_08899_b200/ds2.py): per step and direction gx = FC(x_t) or FC(hf_t, Wa) + FC(hb_t, Wb),
+    plus FC(h_{t-1}, Wh) (h0 at the first step); per-frame logits = FC(hf_t, Wo_a, b) + FC(hb_t, Wo_b),
+    stacked, softmax cross-entropy."""
+    T, B, F, H, C = cfg.T, cfg.B, cfg.F, cfg.H, cfg.classes
+    g = GraphBuilder()
+    x = g.placeholder("x", [T, B, F], s)
+    labels = g.placeholder("labels", [T * B], "i64")
+    h0 = g.placeholder("h0", [B, H], s)
+    c0 = g.placeholder("c0", [B, H], "f32")
+    xs = [g.op("slice", [x], tag="input", axis=0, begin=t, end=t + 1, squeeze=1) for t in range(T)]
+    low = None
+    for l in range(cfg.layers):
+        outs = {}
+        for d in ("fw", "bw"):
+            if l == 0:
+                Wx = g.placeholder(f"l{l}.{d}.Wx", [4 * H, F], s, trainable=True)
+            else:
+                Wa = g.placeholder(f"l{l}.{d}.Wxa", [4 * H, H], s, trainable=True)
+                Wb = g.placeholder(f"l{l}.{d}.Wxb", [4 * H, H], s, trainable=True)
+            Wh = g.placeholder(f"l{l}.{d}.Wh", [4 * H, H], s, trainable=True)
+            b = g.placeholder(f"l{l}.{d}.b", [4 * H], "f32", trainable=True)
+            order = range(T) if d == "fw" else range(T - 1, -1, -1)
+            h, c = h0, c0
+            hs = [None] * T
+            for t in order:
+                if l == 0:
+                    gx, extra = g.op("fully_connected", [xs[t], Wx, b], tag="rnn"), None
+                else:
+                    gx = g.op("fully_connected", [low["fw"][t], Wa, b], tag="rnn")
+                    extra = g.op("fully_connected", [low["bw"][t], Wb], tag="rnn")
+                h, c = lstm_cell(g, gx, h, c, Wh, H, B, s, tag="rnn", gh=True, extra=extra)
+                hs[t] = h
+            outs[d] = hs
+        low = outs
+    Woa = g.placeholder("out.Wa", [C, H], s, trainable=True)
+    Wob = g.placeholder("out.Wb", [C, H], s, trainable=True)
+    bo = g.placeholder("out.b", [C], "f32", trainable=True)
+    logits = [g.op("add", [g.op("fully_connected", [low["fw"][t], Woa, bo], tag="output", dtype="f32"),
+                           g.op("fully_connected", [low["bw"][t], Wob], tag="output", dtype="f32")], tag="output")
+              for t in range(T)]
+    loss, _ = g.op("softmax_ce_loss", [g.op("stack", logits, tag="output"), labels], tag="output", nout=2)
+    g.output(loss)
+    return g.doc()
+
+
 def transformer(cfg, s="f32"):
     """Transformer attention-block stack with the op structure of the GPU path
     (paper_1805_08899_b200/transformer.py): per block q,k,v = FC(x); heads; S = batched_dot(qh, kh^T);
