@@ -193,6 +193,76 @@ def time_attn_bwd(cfg, dtype, reps=20):
     return {"ms": ms, "bytes": big + small, "bytes_per_row": (big + small) / rows, "rows": rows}
 
 
+def extra_leg(name, dtype_s, steps=5, warmup=3):
+    """Secondary configs (BASELINE.json configs[2..4]): device-timed steps of both modes (CUDA graph),
+    exact stash bytes and allocator peak per mode.  C5 = C2 shapes at a per-GPU batch where STASH
+    runs out of HBM and RECOMPUTE fits (the OOM is caught and reported)."""
+    import torch
+    from paper_1805_08899_b200 import abi
+    from synth import configs as K
+    from synth import data as D
+    dt = abi.FP32 if dtype_s == "fp32" else abi.BF16
+    res = {"dtype": "f32" if dtype_s == "fp32" else "bf16"}
+    if name == "C3":
+        from paper_1805_08899_b200.ds2 import DS2Model as M
+        cfg = K.C3
+        params, batch = D.ds2_params(0, cfg, dtype_s), D.ds2_batch(1, cfg, dtype_s)
+        res["workload"] = "C3 DeepSpeech2-shaped: 5 bidirectional LSTM layers, H=800, T=400, B=32"
+        samples = cfg.B
+    elif name == "C4":
+        from paper_1805_08899_b200.transformer import TXModel as M
+        cfg = K.C4
+        params, batch = D.tx_params(0, cfg, dtype_s), D.tx_batch(1, cfg, dtype_s)
+        res["workload"] = "C4 Transformer-base attention blocks: d=512, 8 heads, L=256, B=64, 6 blocks, dropout 0.1"
+        samples = cfg.B
+    else:
+        from paper_1805_08899_b200.nmt import NMTModel as M
+        Bc5 = 24576 if dtype_s == "bf16" else 16384
+        cfg = K.C2.with_batch(Bc5)
+        params, batch = D.nmt_params(0, cfg, dtype_s), D.nmt_batch(1, cfg)
+        res["workload"] = f"C5 NMT (C2 shapes) at B={Bc5} per GPU: STASH exceeds HBM, RECOMPUTE fits"
+        samples = cfg.B
+    for mode, mname in ((abi.STASH, "stash"), (abi.RECOMPUTE, "recompute")):
+        r = {}
+        try:
+            m = M(cfg, dt, mode)
+            m.load_params(params)
+            m.upload_batch(batch)
+            torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats()
+            base = torch.cuda.memory_allocated()
+            acts = m._forward()
+            r["stash_bytes"] = m.stash_bytes()
+            m._backward(acts)
+            del acts
+            torch.cuda.synchronize()
+            r["peak_activation_bytes"] = torch.cuda.max_memory_allocated() - base
+            m.capture(0.01)
+            for _ in range(warmup):
+                m.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                m.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            r.update({"ms_per_step": ms, "samples_per_s": samples / (ms / 1e3), "steps": steps, "cuda_graph": True})
+        except torch.OutOfMemoryError as ex:
+            r["oom"] = str(ex).split("\n")[0][:160]
+        finally:
+            m = None
+            torch.cuda.empty_cache()
+        res[mname] = r
+    st, rc = res["stash"], res["recompute"]
+    if "ms_per_step" in st and "ms_per_step" in rc:
+        res["recompute_overhead"] = rc["ms_per_step"] / st["ms_per_step"] - 1.0
+    if st.get("stash_bytes") and rc.get("stash_bytes"):
+        res["stash_ratio"] = st["stash_bytes"] / rc["stash_bytes"]
+    return res
+
+
 def run_ours(args):
     import torch
     from paper_1805_08899_b200 import abi, dp
@@ -386,6 +456,14 @@ def run_ours(args):
             line[f"{other_name}_mode"] = {"value": samples / (out["ms_other"] / 1e3), "ms_per_step": out["ms_other"]}
             if mode == abi.RECOMPUTE:
                 line["recompute_overhead"] = ms / out["ms_other"] - 1.0
+    if rank == 0 and not args.quick and args.legs:
+        extra = {}
+        for leg in [x for x in args.legs.split(",") if x]:
+            try:
+                extra[leg] = extra_leg(leg, args.leg_dtype)
+            except Exception as ex:                               # a secondary leg never breaks the line
+                extra[leg] = {"error": f"{type(ex).__name__}: {ex}"[:200]}
+        line["configs_extra"] = extra
     if rank == 0 and not args.quick and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line), flush=True)
@@ -405,6 +483,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the stash comparison, memory and kernel legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--legs", default="C3,C4,C5", help="secondary configs to report (C3,C4,C5; '' for none)")
+    ap.add_argument("--leg-dtype", default="bf16", choices=["fp32", "bf16"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
