@@ -37,10 +37,10 @@ __device__ unsigned long long g_echo_phase[16][8192];
       const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                   \
       if (cta_ < 8192) {                                                                      \
         g_echo_phase[k][cta_] = clock64();                                                    \
-        if ((k) == 0) {                                                                       \
+        if ((k) == 0 || (k) == 10) {                                                          \
           unsigned long long gt_;                                                             \
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                             \
-          g_echo_phase[15][cta_] = gt_;                                                       \
+          g_echo_phase[(k) == 0 ? 15 : 14][cta_] = gt_;                                       \
         }                                                                                     \
       }                                                                                       \
     }                                                                                         \
@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_kernel(echo_attn_desc d,
                                                                const int32_t* __restrict__ src_len,
                                                                T* __restrict__ ctx, T* __restrict__ Z_st,
                                                                float* __restrict__ alpha_st) {
+  pdl_wait();
   constexpr int V = St<T>::VEC;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ float sm[];
@@ -311,6 +312,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
                                                                const float* __restrict__ dctx, float* __restrict__ dqp,
                                                                float* __restrict__ dKp, float* __restrict__ dHs,
                                                                float* __restrict__ dv_part, T* __restrict__ ctx_regen) {
+  pdl_wait();
   constexpr int V = St<T>::VEC;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ float sm[];
@@ -526,17 +528,19 @@ __device__ __forceinline__ float z_of(float qp, float kz, bool add_qp) {
 
 // partial score over this CTA's A slice for one position (one warp; lanes over 4-column groups)
 template <typename T>
-__device__ __forceinline__ float score_partial(const T* kz_row, const float* qps, const float* vs, int W, int lane,
+__device__ __forceinline__ float score_partial(const T* kz_row, const T* qps, const T* vs, int W, int lane,
                                                bool add_qp, T* z_out, float* e_out) {
   float acc = 0.0f;
   for (int c4 = lane; c4 < W / 4; c4 += 32) {
-    float kz[4], z[4], e[4];
+    float kz[4], q[4], vv[4], z[4], e[4];
     lds4(kz_row + c4 * 4, kz);
+    if (add_qp) lds4(qps + c4 * 4, q);
+    lds4(vs + c4 * 4, vv);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      z[k] = z_of<T>(qps[c4 * 4 + k], kz[k], add_qp);
+      z[k] = z_of<T>(add_qp ? q[k] : 0.0f, kz[k], add_qp);
       e[k] = tanhf(z[k]);
-      acc = __fmaf_rn(e[k], vs[c4 * 4 + k], acc);
+      acc = __fmaf_rn(e[k], vv[k], acc);
     }
     if (z_out) stg4(z_out + c4 * 4, z);
     if (e_out) *reinterpret_cast<float4*>(e_out + c4 * 4) = make_float4(e[0], e[1], e[2], e[3]);
@@ -611,49 +615,101 @@ __device__ __forceinline__ void tma_store_commit_wait() {
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
   asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(map), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ size_t al128(size_t b) { return (b + 127) & ~(size_t)127; }
 
-// Shared-memory tiles: one TMA box per tensor = Ts rows x (box width) columns of this CTA's slice.
+// The row slice is staged in up to TMA_CHUNKS chunks of R positions, one mbarrier each, so phase 1
+// starts on the first chunk while the rest is in flight; chunks that start at or beyond the row's
+// length n are never loaded.  R = ceil(Ts / TMA_CHUNKS) rounded up so that every chunk's shared
+// destination stays 128-byte aligned (R * row bytes a multiple of 128 for both tiles); the tiles
+// hold Tr = R * ceil(Ts / R) rows (the last box may extend past Ts: TMA zero-fills those rows).
+constexpr int TMA_CHUNKS = 4;
+static __host__ __device__ __forceinline__ int pow2_gap128(int bytes) {   // 128 / gcd(bytes, 128)
+  int m = 1;
+  while ((bytes * m) % 128) m <<= 1;
+  return m;
+}
+static __host__ __device__ __forceinline__ int tma_rows(int Ts, int Wb, int WHb, int es) {
+  const int m1 = pow2_gap128(Wb * es), m2 = pow2_gap128(WHb * es);
+  const int m = m1 > m2 ? m1 : m2;
+  const int r = (Ts + TMA_CHUNKS - 1) / TMA_CHUNKS;
+  return (r + m - 1) / m * m;
+}
+static __host__ __device__ __forceinline__ int tma_tile_rows(int Ts, int R) { return (Ts + R - 1) / R * R; }
+
+struct SmallCopy {     // contiguous vectors staged with chunk 0 (qp / v / dctx slices)
+  void* dst[3];
+  const void* src[3];
+  uint32_t bytes[3];   // 0 = not staged
+};
+__device__ __forceinline__ void issue_chunks(uint64_t* bar, int n, int R, void* kz, const CUtensorMap* mK, int a0,
+                                             void* hs, const CUtensorMap* mH, int h0, int b, uint32_t rowK,
+                                             uint32_t rowH, const SmallCopy& sm) {
+  const int nch = (n + R - 1) / R;
+  // one arrive.expect_tx per barrier (count 1): chunk 0's also covers the small vectors
+  mbar_expect_tx(&bar[0], sm.bytes[0] + sm.bytes[1] + sm.bytes[2] + (uint32_t)R * (rowK + rowH));
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (sm.bytes[i]) bulk_load(sm.dst[i], sm.src[i], sm.bytes[i], &bar[0]);
+  for (int k = 0; k < nch; ++k) {
+    if (k > 0) mbar_expect_tx(&bar[k], (uint32_t)R * (rowK + rowH));
+    tma_load_3d(static_cast<unsigned char*>(kz) + (size_t)k * R * rowK, mK, a0, b, k * R, &bar[k]);
+    tma_load_3d(static_cast<unsigned char*>(hs) + (size_t)k * R * rowH, mH, h0, b, k * R, &bar[k]);
+  }
+}
+
+// Shared-memory tiles: [Tr][box width] per tensor for this CTA's column slice.
 template <typename T>
 __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, const __grid_constant__ CUtensorMap mK,
                                                             const __grid_constant__ CUtensorMap mH,
                                                             const T* __restrict__ qp, const T* __restrict__ v,
                                                             const int32_t* __restrict__ src_len, T* __restrict__ ctx,
                                                             T* __restrict__ Z_st, float* __restrict__ alpha_st) {
+  pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(1024) unsigned char smraw[];
-  __shared__ __align__(8) uint64_t bar[1];
+  __shared__ __align__(8) uint64_t bar[TMA_CHUNKS];
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
   const Slice g = make_slice(A, Hk, (int)cl.num_blocks(), (int)cl.block_rank());
   const int W = g.a1 - g.a0, WH = g.h1 - g.h0;               // valid widths
   const int Wb = tma_width(A, g.C), WHb = tma_width(Hk, g.C);  // box widths (smem row strides)
   const int Tp = (Ts + 3) & ~3;
-  T* kz = reinterpret_cast<T*>(smraw);                                         // [Ts][Wb]
-  T* hs = reinterpret_cast<T*>(smraw + al128((size_t)Ts * Wb * sizeof(T)));    // [Ts][WHb]
-  float* f = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(hs) + al128((size_t)Ts * WHb * sizeof(T)));
+  const int R = tma_rows(Ts, Wb, WHb, (int)sizeof(T)), Tr = tma_tile_rows(Ts, R);
+  T* kz = reinterpret_cast<T*>(smraw);                                         // [Tr][Wb]
+  T* hs = reinterpret_cast<T*>(smraw + al128((size_t)Tr * Wb * sizeof(T)));    // [Tr][WHb]
+  T* qps = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(hs) + al128((size_t)Tr * WHb * sizeof(T)));
+  T* vs = qps + Wb;                                                            // Wb * sizeof(T) is 16-B aligned
+  float* f = reinterpret_cast<float*>(vs + Wb);
   float* sc_part = f;
   float* sc = sc_part + Tp;
   float* al = sc + Tp;
-  float* qps = al + Tp;
-  float* vs = qps + Wb;
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
+    for (int k = 0; k < TMA_CHUNKS; ++k) mbar_init(&bar[k], 1);
     fence_mbar_init();
+    SmallCopy sm{{qps, vs, nullptr}, {qp + (long)b * A + g.a0, v + g.a0, nullptr},
+                 {(uint32_t)(W * sizeof(T)), (uint32_t)(W * sizeof(T)), 0u}};
+    issue_chunks(bar, n, R, kz, &mK, g.a0, hs, &mH, g.h0, b, Wb * sizeof(T), WHb * sizeof(T), sm);
   }
-  __syncthreads();
-  if (tid == 0) {                                             // two TMA instructions stage the whole row slice
-    mbar_expect_tx(&bar[0], (uint32_t)((size_t)Ts * (Wb + WHb) * sizeof(T)));
-    tma_load_3d(kz, &mK, g.a0, b, 0, &bar[0]);
-    tma_load_3d(hs, &mH, g.h0, b, 0, &bar[0]);
-  }
-  stage_slice<T>(qps, qp + (long)b * A + g.a0, W, tid);
-  stage_slice<T>(vs, v + g.a0, W, tid);
-  __syncthreads();
-  mbar_wait(&bar[0], 0);
+  __syncthreads();                                            // barrier init visible before anyone waits
+  mbar_wait(&bar[0], 0);                                      // chunk 0 + the qp / v slices
   for (int s = w; s < n; s += ATT_WARPS) {
+    mbar_wait(&bar[s / R], 0);
     T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
     const float p = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, true, z_out, nullptr);
     if (lane == 0) sc_part[s] = p;
@@ -663,6 +719,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, co
     for (int s = n + w; s < Ts; s += ATT_WARPS)
       for (int c4 = lane; c4 < W / 4; c4 += 32) stg4(Z_st + ((long)b * Ts + s) * A + g.a0 + c4 * 4, z);
   }
+  for (int k = 0; k * R < n; ++k) mbar_wait(&bar[k], 0);     // every H_s chunk landed
   cl.sync();
   gather_sum(cl, sc_part, sc, n, g.C, tid);
   cluster_arrive();                                           // remote reads of sc_part done
@@ -675,70 +732,75 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, co
   cluster_wait();
 }
 
+// phase-4 work split: G = (W + WH)/4 column groups of four; P = ATT_THREADS / G position phases
+static __host__ __device__ __forceinline__ int tma_phases(int W, int WH) { return ATT_THREADS / ((W + WH) / 4); }
+
+// dKp / dH_s are NOT staged: phase 4 streams them through registers (16-byte vectors, rows s < n
+// only), so the shared footprint is the K/Z and H_s slices alone and four CTAs fit per SM.
 template <typename T>
-__global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, const __grid_constant__ CUtensorMap mK,
-                                                            const __grid_constant__ CUtensorMap mH,
-                                                            const __grid_constant__ CUtensorMap mdK,
-                                                            const __grid_constant__ CUtensorMap mdH,
-                                                            const T* __restrict__ qp, const T* __restrict__ v,
-                                                            const int32_t* __restrict__ src_len, bool recompute,
-                                                            const float* __restrict__ alpha_st,
-                                                            const float* __restrict__ dctx, float* __restrict__ dqp,
-                                                            float* __restrict__ dv_part, T* __restrict__ ctx_regen) {
+__global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d, const __grid_constant__ CUtensorMap mK,
+                                                               const __grid_constant__ CUtensorMap mH,
+                                                               const __grid_constant__ CUtensorMap mdK,
+                                                               const __grid_constant__ CUtensorMap mdH,
+                                                               const T* __restrict__ qp, const T* __restrict__ v,
+                                                               const int32_t* __restrict__ src_len, bool recompute,
+                                                               const float* __restrict__ alpha_st,
+                                                               const float* __restrict__ dctx, float* __restrict__ dqp,
+                                                               float* __restrict__ dKp, float* __restrict__ dHs,
+                                                               float* __restrict__ dv_part, T* __restrict__ ctx_regen) {
+  pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(1024) unsigned char smraw[];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[TMA_CHUNKS];
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
   const Slice g = make_slice(A, Hk, (int)cl.num_blocks(), (int)cl.block_rank());
   const int W = g.a1 - g.a0, WH = g.h1 - g.h0;
   const int Wb = tma_width(A, g.C), WHb = tma_width(Hk, g.C);
   const int Tp = (Ts + 3) & ~3;
-  // dk [Ts][Wb] f32 | dh [Ts][WHb] f32 | kz [Ts][Wb] T (E overwrites it in place for fp32) | hs [Ts][WHb] T
-  // | E [Ts][Wb] f32 (bf16 only) | floats
+  const int P = tma_phases(Wb, WHb);
+  const int R = tma_rows(Ts, Wb, WHb, (int)sizeof(T)), Tr = tma_tile_rows(Ts, R);
+  // kz [Tr][Wb] T (E overwrites it in place for fp32) | hs [Tr][WHb] T | E [Tr][Wb] f32 (bf16 only)
+  // | floats | phase partials [2][P][Wb] (aliased onto E when it fits)
   constexpr bool kE_ALIAS = sizeof(T) == sizeof(float);
   unsigned char* p = smraw;
-  float* dk = reinterpret_cast<float*>(p);
-  p += al128((size_t)Ts * Wb * 4);
-  float* dh = reinterpret_cast<float*>(p);
-  p += al128((size_t)Ts * WHb * 4);
   T* kz = reinterpret_cast<T*>(p);
-  p += al128((size_t)Ts * Wb * sizeof(T));
+  p += al128((size_t)Tr * Wb * sizeof(T));
   T* hs = reinterpret_cast<T*>(p);
-  p += al128((size_t)Ts * WHb * sizeof(T));
+  p += al128((size_t)Tr * WHb * sizeof(T));
   float* E = kE_ALIAS ? reinterpret_cast<float*>(kz) : reinterpret_cast<float*>(p);
-  if (!kE_ALIAS) p += al128((size_t)Ts * Wb * 4);
-  float* sc_part = reinterpret_cast<float*>(p);
+  if (!kE_ALIAS) p += al128((size_t)Tr * Wb * 4);
+  T* qps = reinterpret_cast<T*>(p);
+  T* vs = qps + Wb;
+  float* dcs = reinterpret_cast<float*>(vs + Wb);
+  float* sc_part = dcs + WHb;
   float* dal_part = sc_part + Tp;
   float* sc = dal_part + Tp;
   float* dal = sc + Tp;
   float* al = dal + Tp;
   float* dsv = al + Tp;
-  float* qps = dsv + Tp;
-  float* vs = qps + Wb;
-  float* dcs = vs + Wb;
+  float* red = Tr >= 2 * P ? E : dsv + Tp;
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
+  ECHO_PHASE(0);
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int k = 0; k < TMA_CHUNKS; ++k) mbar_init(&bar[k], 1);
     fence_mbar_init();
+    SmallCopy sm{{qps, vs, dcs}, {qp + (long)b * A + g.a0, v + g.a0, dctx + (long)b * Hk + g.h0},
+                 {recompute ? (uint32_t)(W * sizeof(T)) : 0u, (uint32_t)(W * sizeof(T)), (uint32_t)WH * 4u}};
+    issue_chunks(bar, n, R, kz, &mK, g.a0, hs, &mH, g.h0, b, Wb * sizeof(T), WHb * sizeof(T), sm);
   }
+  // values only the epilogue / softmax need are fetched now so their latency hides under the
+  // staging wait (W <= 128 < ATT_THREADS: one column per thread, see tma_cluster)
+  const float dv_old = tid < W ? dv_part[(long)b * A + g.a0 + tid] : 0.0f;
+  if (!recompute)
+    for (int s = tid; s < n; s += ATT_THREADS) al[s] = alpha_st[(long)b * Ts + s];
   __syncthreads();
-  if (tid == 0) {                                             // four TMA instructions stage everything
-    mbar_expect_tx(&bar[0], (uint32_t)((size_t)Ts * (Wb + WHb) * sizeof(T)));
-    tma_load_3d(kz, &mK, g.a0, b, 0, &bar[0]);
-    tma_load_3d(hs, &mH, g.h0, b, 0, &bar[0]);
-    mbar_expect_tx(&bar[1], (uint32_t)((size_t)Ts * (Wb + WHb) * 4));
-    tma_load_3d(dk, &mdK, g.a0, b, 0, &bar[1]);
-    tma_load_3d(dh, &mdH, g.h0, b, 0, &bar[1]);
-  }
-  if (recompute) stage_slice<T>(qps, qp + (long)b * A + g.a0, W, tid);
-  stage_slice<T>(vs, v + g.a0, W, tid);
-  for (int i = tid; i < WH; i += ATT_THREADS) dcs[i] = dctx[(long)b * Hk + g.h0 + i];
-  __syncthreads();
-  mbar_wait(&bar[0], 0);
+  ECHO_PHASE(1);
+  if (n > 0) mbar_wait(&bar[0], 0);
+  ECHO_PHASE(2);
   // phase 1: E = tanh(z) into smem (fp32), partial scores (RECOMPUTE) and partial dalpha
   for (int s = w; s < n; s += ATT_WARPS) {
+    mbar_wait(&bar[s / R], 0);
     const float ps = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, recompute, nullptr, E + (size_t)s * Wb);
     float acc = 0.0f;
     const T* hrow = hs + (size_t)s * WHb;
@@ -754,15 +816,27 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, co
       dal_part[s] = acc;
     }
   }
+  // L2 prefetch of the dKp / dH_s tiles phase 4 streams, issued by thread 0 once this CTA's loads
+  // have landed so the reads overlap the exchange / softmax phases instead of phase 4
+#ifndef ECHO_A6_NO_PREFETCH
+  if (tid == 0) {
+    for (int k = 0; k * R < n; ++k) mbar_wait(&bar[k], 0);
+    for (int k = 0; k * R < n; ++k) {
+      if (W > 0) tma_prefetch_3d(&mdK, g.a0, b, k * R);
+      if (WH > 0) tma_prefetch_3d(&mdH, g.h0, b, k * R);
+    }
+  }
+#endif
+  ECHO_PHASE(3);
   cl.sync();
+  ECHO_PHASE(4);
   if (recompute) gather_sum(cl, sc_part, sc, n, g.C, tid);
   gather_sum(cl, dal_part, dal, n, g.C, tid);
   cluster_arrive();
   __syncthreads();
+  ECHO_PHASE(5);
   if (w == 0) {
-    if (recompute) softmax_row_warp(sc, al, n, lane);
-    else
-      for (int s = lane; s < n; s += 32) al[s] = alpha_st[(long)b * Ts + s];
+    if (recompute) softmax_row_warp(sc, al, n, lane);      // STASH: al[] was loaded at the start
     __syncwarp();
     float acc = 0.0f;                                          // dot = sum_s alpha_s dalpha_s (fixed order)
     for (int s = lane; s < n; s += 32) acc = __fmaf_rn(al[s], dal[s], acc);
@@ -770,44 +844,96 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_tma(echo_attn_desc d, co
     for (int s = lane; s < n; s += 32) dsv[s] = __fmul_rn(al[s], __fsub_rn(dal[s], acc));
   }
   __syncthreads();
+  ECHO_PHASE(6);
   if (recompute && ctx_regen) ctx_columns<T>(hs, WHb, WH, al, n, ctx_regen + (long)b * Hk + g.h0, tid);
-  mbar_wait(&bar[1], 0);
-  // phase 4 (column-local, all operands in shared memory):
+  ECHO_PHASE(7);
+  // phase 4 (column-local).  Thread -> (column group gi of 4, position phase ph); phase ph takes
+  // s = ph, ph + P, ... in increasing order and the P phase partials are combined in rank order.
   //   A columns : dKp += dE ; dqp = sum_s dE ; dv_part += sum_s ds E   with dE = ds v (1 - E^2)
   //   Hk columns: dHs += alpha_s dctx
-  for (int i = tid; i < W + WH; i += ATT_THREADS) {
-    if (i < W) {
-      const int c = i;
-      const float vc = vs[c];
-      float dq = 0.0f, dvv = 0.0f;
-      for (int s = 0; s < n; ++s) {
-        const float e = E[(size_t)s * Wb + c];
-        const float ds = dsv[s];
-        const float dE = __fmul_rn(__fmul_rn(ds, vc), __fsub_rn(1.0f, __fmul_rn(e, e)));
-        dk[(size_t)s * Wb + c] = __fadd_rn(dk[(size_t)s * Wb + c], dE);
-        dq = __fadd_rn(dq, dE);
-        dvv = __fmaf_rn(ds, e, dvv);
+  const int GA = Wb / 4, G = (Wb + WHb) / 4;
+  const int gi = tid % G, ph = tid / G;
+  float dq[4] = {0.0f, 0.0f, 0.0f, 0.0f}, dvv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  constexpr int U = 4;                                         // rows in flight per thread
+  if (ph < P && gi < GA && gi * 4 < W) {
+    const int c = gi * 4;
+    float vc[4];
+    lds4(vs + c, vc);
+    float* base = dKp + (long)b * d.kp_stride_b + g.a0 + c;
+    for (int s0 = ph; s0 < n; s0 += U * P) {
+      float4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + u * P;
+        if (s < n) x[u] = *reinterpret_cast<const float4*>(base + (long)s * d.kp_stride_s);
       }
-      const long o = (long)b * A + g.a0 + c;
-      dqp[o] = dq;
-      dv_part[o] = __fadd_rn(dv_part[o], dvv);
-    } else {
-      const int c = i - W;
-      const float dcv = dcs[c];
-      for (int s = 0; s < n; ++s) dh[(size_t)s * WHb + c] = __fmaf_rn(al[s], dcv, dh[(size_t)s * WHb + c]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + u * P;
+        if (s < n) {
+          float e[4], xv[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+          lds4(E + (size_t)s * Wb + c, e);
+          const float ds = dsv[s];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float dE = __fmul_rn(__fmul_rn(ds, vc[k]), __fsub_rn(1.0f, __fmul_rn(e[k], e[k])));
+            xv[k] = __fadd_rn(xv[k], dE);
+            dq[k] = __fadd_rn(dq[k], dE);
+            dvv[k] = __fmaf_rn(ds, e[k], dvv[k]);
+          }
+          stg4(base + (long)s * d.kp_stride_s, xv);
+        }
+      }
+    }
+  } else if (ph < P && gi >= GA && (gi - GA) * 4 < WH) {
+    const int c = (gi - GA) * 4;
+    float dc[4];
+    lds4(dcs + c, dc);
+    float* base = dHs + (long)b * d.hs_stride_b + g.h0 + c;
+    for (int s0 = ph; s0 < n; s0 += U * P) {
+      float4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + u * P;
+        if (s < n) x[u] = *reinterpret_cast<const float4*>(base + (long)s * d.hs_stride_s);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + u * P;
+        if (s < n) {
+          const float a = al[s];
+          float xv[4] = {__fmaf_rn(a, dc[0], x[u].x), __fmaf_rn(a, dc[1], x[u].y), __fmaf_rn(a, dc[2], x[u].z),
+                         __fmaf_rn(a, dc[3], x[u].w)};
+          stg4(base + (long)s * d.hs_stride_s, xv);
+        }
+      }
     }
   }
-  fence_proxy_async();                                         // smem writes -> visible to the TMA engine
-  __syncthreads();
-  if (tid == 0) {                                              // two TMA stores write the accumulators back
-    tma_store_3d(&mdK, g.a0, b, 0, dk);
-    tma_store_3d(&mdH, g.h0, b, 0, dh);
-    tma_store_commit_wait();
+  __syncthreads();                                             // E reads done: red may alias it
+  ECHO_PHASE(8);
+  if (ph < P && gi < GA) {
+    *reinterpret_cast<float4*>(red + (size_t)ph * Wb + gi * 4) = make_float4(dq[0], dq[1], dq[2], dq[3]);
+    *reinterpret_cast<float4*>(red + (size_t)(P + ph) * Wb + gi * 4) = make_float4(dvv[0], dvv[1], dvv[2], dvv[3]);
   }
+  __syncthreads();
+  if (tid < W) {
+    const int c = tid;
+    float q = 0.0f, x = 0.0f;
+    for (int k = 0; k < P; ++k) {
+      q = __fadd_rn(q, red[(size_t)k * Wb + c]);
+      x = __fadd_rn(x, red[(size_t)(P + k) * Wb + c]);
+    }
+    const long o = (long)b * A + g.a0 + c;
+    dqp[o] = q;
+    dv_part[o] = __fadd_rn(dv_old, x);
+  }
+  ECHO_PHASE(9);
   cluster_wait();
+  ECHO_PHASE(10);
 }
 
 __global__ void dv_reduce_kernel(int B, int A, const float* __restrict__ part, float* __restrict__ dv, int acc) {
+  pdl_wait();
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= A) return;
   float x = acc ? dv[a] : 0.0f;
@@ -834,18 +960,21 @@ static size_t bwd_smem(const echo_attn_desc* d) {
 
 // TMA path: cluster size and shared-memory footprint; returns false if the generic path must run
 static size_t al128h(size_t b) { return (b + 127) & ~(size_t)127; }
-static bool tma_params(const echo_attn_desc* d, int* C, size_t* smem_fwd, size_t* smem_bwd) {
+static bool tma_params(const echo_attn_desc* d, int* C, int* rows, size_t* smem_fwd, size_t* smem_bwd) {
   const size_t sT = d->dtype == ECHO_FP32 ? 4 : 2;
   if (d->A > 1024 || d->Hk > 1024 || d->Ts > 256) return false;
   const int c = tma_cluster(d->A, d->Hk);
   const size_t W = tma_width(d->A, c), WH = tma_width(d->Hk, c);
   const size_t Tp = (d->Ts + 3) & ~3;
-  const size_t Ts = d->Ts;
-  const size_t fwd = al128h(Ts * W * sT) + al128h(Ts * WH * sT) + (3 * Tp + 2 * W) * 4;
-  const size_t bwd = al128h(Ts * W * 4) + al128h(Ts * WH * 4) + al128h(Ts * W * sT) + al128h(Ts * WH * sT) +
-                     (sT == 4 ? 0 : al128h(Ts * W * 4)) + (6 * Tp + 2 * W + WH) * 4;
+  const int R = tma_rows(d->Ts, (int)W, (int)WH, (int)sT);
+  const size_t Ts = (size_t)tma_tile_rows(d->Ts, R);        // rows allocated per tile
+  const size_t fwd = al128h(Ts * W * sT) + al128h(Ts * WH * sT) + 2 * W * sT + 3 * Tp * 4;
+  const size_t P = tma_phases((int)W, (int)WH);
+  const size_t bwd = al128h(Ts * W * sT) + al128h(Ts * WH * sT) + (sT == 4 ? 0 : al128h(Ts * W * 4)) +
+                     2 * W * sT + (6 * Tp + WH) * 4 + (Ts >= 2 * P ? 0 : 2 * P * W * 4);
   if (bwd > 220 * 1024) return false;
   *C = c;
+  *rows = R;
   *smem_fwd = fwd;
   *smem_bwd = bwd;
   return true;
@@ -866,15 +995,15 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// 3-D map over a [Ts][B][X]-strided tensor: dims {X, B, Ts}, box {boxX, 1, Ts}
+// 3-D map over a [Ts][B][X]-strided tensor: dims {X, B, Ts}, box {boxX, 1, R}
 static bool map3d(CUtensorMap* m, const void* base, bool bf16, uint64_t X, uint64_t B, uint64_t Ts, int64_t stride_b,
-                  int64_t stride_s, uint32_t boxX) {
+                  int64_t stride_s, uint32_t boxX, int boxR) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
   const uint64_t es = bf16 ? 2 : 4;
   cuuint64_t dims[3] = {X, B, Ts};
   cuuint64_t strides[2] = {(cuuint64_t)stride_b * es, (cuuint64_t)stride_s * es};
-  cuuint32_t box[3] = {boxX, 1, (cuuint32_t)Ts};
+  cuuint32_t box[3] = {boxX, 1, (cuuint32_t)boxR};   // one chunk of positions
   cuuint32_t el[3] = {1, 1, 1};
   return fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
             strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -883,19 +1012,7 @@ static bool map3d(CUtensorMap* m, const void* base, bool bf16, uint64_t X, uint6
 
 template <typename Kern, typename... Args>
 static cudaError_t launch_cluster(Kern kern, int C, int B, size_t smem, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C, B, 1);
-  cfg.blockDim = dim3(ATT_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args...);
+  return launch(kern, dim3(C, B, 1), dim3(ATT_THREADS, 1, 1), smem, st, C, args...);
 }
 
 static echo_status check_attn(const char* fn, const echo_attn_desc* d) {
@@ -954,13 +1071,13 @@ extern "C" echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, co
   cudaStream_t st = (cudaStream_t)stream;
   const int C = att_cluster(d->Ts), chunk = att_chunk(d->Ts, C);
   cudaError_t e;
-  int tC;
+  int tC, tR;
   size_t sf, sb;
   CUtensorMap mK, mH;
   const bool bfd = d->dtype == ECHO_BF16;
-  if (tma_params(d, &tC, &sf, &sb) &&
-      map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC)) &&
-      map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC))) {
+  if (tma_params(d, &tC, &tR, &sf, &sb) &&
+      map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC), tR) &&
+      map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC), tR)) {
     if (d->dtype == ECHO_FP32) {
       if ((s = set_smem((const void*)attn_fwd_tma<float>, sf, fn))) return s;
       e = launch_cluster(attn_fwd_tma<float>, tC, d->B, sf, st, *d, mK, mH, (const float*)qp, (const float*)v, src_len,
@@ -1016,26 +1133,26 @@ extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, co
   cudaStream_t st = (cudaStream_t)stream;
   const int C = att_cluster(d->Ts), chunk = att_chunk(d->Ts, C);
   cudaError_t e;
-  int tC;
+  int tC, tR;
   size_t sf, sb;
   CUtensorMap mK, mH, mdK, mdH;
   const bool bfd = d->dtype == ECHO_BF16;
   const bool rec = d->mode == ECHO_RECOMPUTE;
-  if (tma_params(d, &tC, &sf, &sb) &&
-      (rec ? map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC))
-           : map3d(&mK, E_st, bfd, d->A, d->B, d->Ts, (int64_t)d->Ts * d->A, d->A, tma_width(d->A, tC))) &&
-      map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC)) &&
-      map3d(&mdK, dKp, false, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC)) &&
-      map3d(&mdH, dHs, false, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC))) {
+  if (tma_params(d, &tC, &tR, &sf, &sb) &&
+      (rec ? map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC), tR)
+           : map3d(&mK, E_st, bfd, d->A, d->B, d->Ts, (int64_t)d->Ts * d->A, d->A, tma_width(d->A, tC), tR)) &&
+      map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC), tR) &&
+      map3d(&mdK, dKp, false, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC), tR) &&
+      map3d(&mdH, dHs, false, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC), tR)) {
     if (d->dtype == ECHO_FP32) {
       if ((s = set_smem((const void*)attn_bwd_tma<float>, sb, fn))) return s;
-      e = launch_cluster(attn_bwd_tma<float>, tC, d->B, sb, st, *d, mK, mH, mdK, mdH, (const float*)qp, (const float*)v,
-                         src_len, rec, alpha_st, dctx, dqp, dv_part, (float*)ctx_regen);
+      e = launch_cluster(attn_bwd_tma<float>, tC, d->B, sb, st, *d, mK, mH, mdK, mdH, (const float*)qp, (const float*)v, src_len,
+                         rec, alpha_st, dctx, dqp, dKp, dHs, dv_part, (float*)ctx_regen);
     } else {
       typedef __nv_bfloat16 bf;
       if ((s = set_smem((const void*)attn_bwd_tma<bf>, sb, fn))) return s;
-      e = launch_cluster(attn_bwd_tma<bf>, tC, d->B, sb, st, *d, mK, mH, mdK, mdH, (const bf*)qp, (const bf*)v, src_len,
-                         rec, alpha_st, dctx, dqp, dv_part, (bf*)ctx_regen);
+      e = launch_cluster(attn_bwd_tma<bf>, tC, d->B, sb, st, *d, mK, mH, mdK, mdH, (const bf*)qp, (const bf*)v, src_len, rec,
+                         alpha_st, dctx, dqp, dKp, dHs, dv_part, (bf*)ctx_regen);
     }
     if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
     return check_launch(fn);
@@ -1058,6 +1175,14 @@ extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, co
 }
 
 #ifdef ECHO_PHASE_TIMING
+namespace echo {
+__global__ void stamp_kernel(int slot) {
+  unsigned long long gt;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+  g_echo_phase[13][slot] = gt;
+}
+}  // namespace echo
+extern "C" void echo_debug_stamp(int slot, void* stream) { echo::stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(slot); }
 extern "C" int echo_debug_phase_times(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, echo::g_echo_phase, sizeof(unsigned long long) * (size_t)n);
 }
@@ -1068,6 +1193,8 @@ extern "C" echo_status echo_attn_dv_reduce(int32_t B, int32_t A, const float* dv
   const char* fn = "echo_attn_dv_reduce";
   if (B <= 0 || A <= 0) return fail(ECHO_ERR_INVALID, "%s: B=%d A=%d must be > 0", fn, B, A);
   if (!dv_part || !dv) return fail(ECHO_ERR_INVALID, "%s: NULL pointer", fn);
-  dv_reduce_kernel<<<(A + 127) / 128, 128, 0, (cudaStream_t)stream>>>(B, A, dv_part, dv, accumulate);
+  const cudaError_t e = launch(dv_reduce_kernel, dim3((A + 127) / 128), dim3(128), 0, (cudaStream_t)stream, 1, B, A,
+                               dv_part, dv, accumulate);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);
 }

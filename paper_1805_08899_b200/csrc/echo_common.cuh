@@ -14,6 +14,9 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/echo.h"
 
@@ -25,6 +28,48 @@ echo_status fail(echo_status s, const char* fmt, ...);
 echo_status check_launch(const char* what);
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------------ launches
+// ECHO_PDL=1 launches every libecho kernel with programmatic stream serialization (PDL): the grid
+// may be scheduled while its stream predecessor drains, and pdl_wait() -- the first statement of
+// every kernel -- blocks until the predecessor has completed and its writes are visible, so results
+// do not change.  Off by default: measured on the C2 step (CUDA graph, cuBLAS predecessors that
+// never trigger early) it gained nothing (8.82 vs 8.86 ms bf16).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ECHO_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  unsigned na = 0;
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------ storage types
 template <typename T> struct St;

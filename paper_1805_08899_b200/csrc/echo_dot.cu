@@ -98,6 +98,7 @@ template <typename T, int CH>
 __global__ void __launch_bounds__(256) dot_fwd_kernel(echo_dot_desc d, uint32_t thr, float inv_keep,
                                                       const T* __restrict__ S, T* __restrict__ Pd,
                                                       T* __restrict__ P_st, uint8_t* __restrict__ mask) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
   const int L = d.L;
@@ -131,6 +132,7 @@ template <typename T, int CH>
 __global__ void __launch_bounds__(256) dot_bwd_kernel(echo_dot_desc d, float inv_keep, const T* __restrict__ S,
                                                       const T* __restrict__ P_st, const uint8_t* __restrict__ mask,
                                                       const T* dPd, T* dS, T* __restrict__ Pd_regen) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
   const int L = d.L;
@@ -226,7 +228,8 @@ static void launch_fwd(const echo_dot_desc* d, uint32_t thr, float ik, const voi
                        uint8_t* mask, cudaStream_t st) {
   const int ch = (d->L + 255) / 256;
   const int grid = dot_grid(d->R);
-#define L_(CH) dot_fwd_kernel<T, CH><<<grid, 256, 0, st>>>(*d, thr, ik, (const T*)S, (T*)Pd, (T*)P_st, mask)
+#define L_(CH) (void)launch(dot_fwd_kernel<T, CH>, dim3(grid), dim3(256), 0, st, 1, *d, thr, ik, (const T*)S, (T*)Pd, \
+                         (T*)P_st, mask)
   if (ch <= 1) L_(1); else if (ch <= 2) L_(2); else if (ch <= 4) L_(4); else L_(8);
 #undef L_
 }
@@ -235,7 +238,8 @@ static void launch_bwd(const echo_dot_desc* d, float ik, const void* S, const vo
                        const void* dPd, void* dS, void* Pdr, cudaStream_t st) {
   const int ch = (d->L + 255) / 256;
   const int grid = dot_grid(d->R);
-#define L_(CH) dot_bwd_kernel<T, CH><<<grid, 256, 0, st>>>(*d, ik, (const T*)S, (const T*)P_st, mask, (const T*)dPd, (T*)dS, (T*)Pdr)
+#define L_(CH) (void)launch(dot_bwd_kernel<T, CH>, dim3(grid), dim3(256), 0, st, 1, *d, ik, (const T*)S, \
+                         (const T*)P_st, mask, (const T*)dPd, (T*)dS, (T*)Pdr)
   if (ch <= 1) L_(1); else if (ch <= 2) L_(2); else if (ch <= 4) L_(4); else L_(8);
 #undef L_
 }

@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(128) lstm_fwd_kernel(int B, int H, const T* gx
                                                        const float* __restrict__ c_prev, T* gates,
                                                        float* __restrict__ c_out, T* __restrict__ tc_out,
                                                        T* __restrict__ h_out) {
+  pdl_wait();
   constexpr int V = St<T>::VEC;
   const int nvec = H / V;
   const long total = (long)B * nvec;
@@ -95,6 +96,7 @@ template <typename T, int U>
 __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, const T* __restrict__ gates,
                                                          const float* __restrict__ c0, float* __restrict__ cws,
                                                          T* __restrict__ hws) {
+  pdl_wait();
   constexpr int V = St<T>::VEC;
   const int nvec = H / V;
   const long total = (long)B * nvec;
@@ -145,6 +147,7 @@ __global__ void __launch_bounds__(128) lstm_bwd_kernel(int B, int H, const T* ga
                                                        const float* __restrict__ c_t, const T* __restrict__ tc_st,
                                                        const float* __restrict__ dh, float* dc, T* dA,
                                                        T* __restrict__ h_regen) {
+  pdl_wait();
   constexpr int V = St<T>::VEC;
   const int nvec = H / V;
   const long total = (long)B * nvec;
@@ -237,14 +240,15 @@ extern "C" echo_status echo_lstm_fwd(const echo_lstm_desc* d, const void* gx_t, 
   cudaStream_t st = (cudaStream_t)stream;
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
   const int grid = grid_for((long)d->B * d->H / V, 128);
+  cudaError_t e_;
   if (d->dtype == ECHO_FP32)
-    lstm_fwd_kernel<float><<<grid, 128, 0, st>>>(d->B, d->H, (const float*)gx_t, (const float*)gh_t, bias, c_prev,
-                                                 (float*)gates_t, c_out, (float*)tc_t, (float*)h_out);
+    e_ = launch(lstm_fwd_kernel<float>, dim3(grid), dim3(128), 0, st, 1, d->B, d->H, (const float*)gx_t,
+                (const float*)gh_t, bias, c_prev, (float*)gates_t, c_out, (float*)tc_t, (float*)h_out);
   else
-    lstm_fwd_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(d->B, d->H, (const __nv_bfloat16*)gx_t,
-                                                         (const __nv_bfloat16*)gh_t, bias, c_prev,
-                                                         (__nv_bfloat16*)gates_t, c_out, (__nv_bfloat16*)tc_t,
-                                                         (__nv_bfloat16*)h_out);
+    e_ = launch(lstm_fwd_kernel<__nv_bfloat16>, dim3(grid), dim3(128), 0, st, 1, d->B, d->H,
+                (const __nv_bfloat16*)gx_t, (const __nv_bfloat16*)gh_t, bias, c_prev, (__nv_bfloat16*)gates_t, c_out,
+                (__nv_bfloat16*)tc_t, (__nv_bfloat16*)h_out);
+  if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
   return check_launch(fn);
 }
 
@@ -261,11 +265,14 @@ extern "C" echo_status echo_lstm_cscan(const echo_lstm_desc* d, int32_t T, const
   cudaStream_t st = (cudaStream_t)stream;
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
   const int grid = grid_for((long)d->B * d->H / V, 128);
+  cudaError_t e_;
   if (d->dtype == ECHO_FP32)
-    lstm_cscan_kernel<float, 8><<<grid, 128, 0, st>>>(T, d->B, d->H, (const float*)gates, c0, c_ws, (float*)h_ws);
+    e_ = launch(lstm_cscan_kernel<float, 8>, dim3(grid), dim3(128), 0, st, 1, T, d->B, d->H, (const float*)gates, c0,
+                c_ws, (float*)h_ws);
   else
-    lstm_cscan_kernel<__nv_bfloat16, 4><<<grid, 128, 0, st>>>(T, d->B, d->H, (const __nv_bfloat16*)gates, c0, c_ws,
-                                                              (__nv_bfloat16*)h_ws);
+    e_ = launch(lstm_cscan_kernel<__nv_bfloat16, 4>, dim3(grid), dim3(128), 0, st, 1, T, d->B, d->H,
+                (const __nv_bfloat16*)gates, c0, c_ws, (__nv_bfloat16*)h_ws);
+  if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
   return check_launch(fn);
 }
 
@@ -292,12 +299,14 @@ extern "C" echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_
   cudaStream_t st = (cudaStream_t)stream;
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
   const int grid = grid_for((long)d->B * d->H / V, 128);
+  cudaError_t e_;
   if (d->dtype == ECHO_FP32)
-    lstm_bwd_kernel<float><<<grid, 128, 0, st>>>(d->B, d->H, (const float*)gates_t, c_prev, c_t, (const float*)tc_t,
-                                                 dh_t, dc, (float*)dA_t, (float*)h_regen);
+    e_ = launch(lstm_bwd_kernel<float>, dim3(grid), dim3(128), 0, st, 1, d->B, d->H, (const float*)gates_t, c_prev,
+                c_t, (const float*)tc_t, dh_t, dc, (float*)dA_t, (float*)h_regen);
   else
-    lstm_bwd_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(d->B, d->H, (const __nv_bfloat16*)gates_t, c_prev, c_t,
-                                                         (const __nv_bfloat16*)tc_t, dh_t, dc,
-                                                         (__nv_bfloat16*)dA_t, (__nv_bfloat16*)h_regen);
+    e_ = launch(lstm_bwd_kernel<__nv_bfloat16>, dim3(grid), dim3(128), 0, st, 1, d->B, d->H,
+                (const __nv_bfloat16*)gates_t, c_prev, c_t, (const __nv_bfloat16*)tc_t, dh_t, dc, (__nv_bfloat16*)dA_t,
+                (__nv_bfloat16*)h_regen);
+  if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
   return check_launch(fn);
 }

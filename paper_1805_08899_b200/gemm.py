@@ -8,6 +8,8 @@ in fp32 for both storage dtypes.
 """
 from __future__ import annotations
 
+from contextlib import contextmanager
+
 import torch
 
 
@@ -25,3 +27,19 @@ def addmm_(c, a, b):
     else:
         torch.addmm(c, a, b, out_dtype=c.dtype, out=c)
     return c
+
+
+@contextmanager
+def tf32(enabled: bool):
+    """Let cuBLAS run fp32-operand GEMMs on TF32 tensor cores inside the block (bf16 storage only:
+    TF32's 10-bit mantissa is finer than the bf16 storage rounding these gradients already carry;
+    fp32 storage keeps IEEE fp32 GEMMs).  Read at launch time, so CUDA-graph capture records it."""
+    if not enabled:
+        yield
+        return
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        yield
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev

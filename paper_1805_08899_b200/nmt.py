@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import abi
-from .gemm import mm, addmm_
+from .gemm import mm, addmm_, tf32
 from .lstm import LSTMLayer, TORCH_DTYPE
 from synth.data import nmt_param_shapes
 
@@ -318,19 +318,22 @@ class NMTModel:
         # per-step backward-data GEMMs of the attention block use the fp32 master weights, so
         # the fp32 gradient signals dpre / dqp are not rounded to the storage dtype (no-op in fp32)
         Wcc32, Wch32, Wq32 = self.P["att.Wcc"], self.P["att.Wch"], self.P["att.Wq"]
+        lowp = sd != torch.float32                               # bf16 storage: TF32 for the fp32 GEMMs
         for t in reversed(range(Td)):
             at = Aall[t].float()
             torch.mul(dAout[t], 1.0 - at * at, out=dPRE[t])      # tanh' = 1 - a^2
-            torch.mm(dPRE[t], Wcc32, out=dctx)
             top = dHdec[-1][t]
-            top.addmm_(dPRE[t], Wch32)
+            with tf32(lowp):
+                torch.mm(dPRE[t], Wcc32, out=dctx)
+                top.addmm_(dPRE[t], Wch32)
             if md == abi.STASH:
                 abi.echo_attn_bwd(adesc, None, None, v, Hs, sl, a["E_st"][t], a["al_st"][t], dctx, dQP[t], dKp, dHs,
                                   dv_part, None)
             else:                                                # a6 regenerates E, scores, alpha, ctx
                 abi.echo_attn_bwd(adesc, a["qp_st"][t], Kp, v, Hs, sl, None, None, dctx, dQP[t], dKp, dHs,
                                   dv_part, ctx_all[t])
-            top.addmm_(dQP[t], Wq32)
+            with tf32(lowp):
+                top.addmm_(dQP[t], Wq32)
             for l in reversed(range(Ld)):
                 L = dec[l]
                 L.bwd_step(t, dHdec[l][t], dcs[l])               # a3 (fused recompute in RECOMPUTE)
@@ -347,9 +350,10 @@ class NMTModel:
         f32 = lambda x: x if x.dtype == torch.float32 else x.float()
         qall = f32(dec[-1].h_for_grad().reshape(N, H))
         dPREs = dPRE.view(N, H)
-        gi(G["att.Wcc"], dPREs.t(), f32(ctx_all.view(N, H)))
-        gi(G["att.Wch"], dPREs.t(), qall)
-        gi(G["att.Wq"], dQP.view(N, A).t(), qall)
+        with tf32(lowp):
+            gi(G["att.Wcc"], dPREs.t(), f32(ctx_all.view(N, H)))
+            gi(G["att.Wch"], dPREs.t(), qall)
+            gi(G["att.Wq"], dQP.view(N, A).t(), qall)
         abi.echo_attn_dv_reduce(B, A, dv_part, G["att.v"], 0)
         del qall
         del dPREs, dPRE, dQP
@@ -381,8 +385,9 @@ class NMTModel:
         dKpf = dKp.view(Ts * B, A)
         torch.sum(dKpf, dim=0, out=G["att.bq"])
         Hs32 = Hs.reshape(Ts * B, H)
-        gi(G["att.Wk"], dKpf.t(), Hs32 if Hs32.dtype == torch.float32 else Hs32.float())
-        dHs.view(Ts * B, H).addmm_(dKpf, self.P["att.Wk"])
+        with tf32(lowp):
+            gi(G["att.Wk"], dKpf.t(), Hs32 if Hs32.dtype == torch.float32 else Hs32.float())
+            dHs.view(Ts * B, H).addmm_(dKpf, self.P["att.Wk"])
         dKps = None
         del Hs, Hs32
         del dKp, dKpf, dKps

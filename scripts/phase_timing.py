@@ -26,11 +26,15 @@ buf = np.zeros((16, 8192), dtype=np.uint64)
 fn(buf.ctypes.data, 16 * 8192)
 ncta = B * 4
 t = buf[:, :ncta].astype(np.int64)
-names = ["start->staged", "staged->tma_done", "tma_done->phase1_end", "phase1->clsync", "clsync->gathered", "gathered->softmax", "softmax->ctx", "ctx->phase4_end", "phase4->cluster_wait"]
-for k in range(9):
+names = ["start->issued", "issued->tma_done", "tma_done->phase1_end", "phase1->clsync", "clsync->gathered",
+         "gathered->softmax", "softmax->ctx", "ctx->phase4_end", "phase4->reduced", "reduced->cluster_wait"]
+for k in range(10):
     dd = t[k + 1] - t[k]
     print(f"{names[k]:24s} mean {dd.mean():8.0f} cyc  p50 {np.median(dd):8.0f}  max {dd.max():8.0f}")
-tot = t[9] - t[0]
+tot = t[10] - t[0]
 print("CTA lifetime cycles mean", tot.mean(), "max", tot.max())
 gt = buf[15, :ncta].astype(np.int64); gt -= gt.min()
 print("CTA start spread (ns): p50", np.median(gt), "max", gt.max())
+ge = buf[14, :ncta].astype(np.int64) - buf[15, :ncta].astype(np.int64).min()
+print("globaltimer: first start -> last end (ns)", ge.max(), " per-CTA lifetime ns p50",
+      np.median(buf[14, :ncta].astype(np.int64) - buf[15, :ncta].astype(np.int64)))
