@@ -708,11 +708,15 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, co
   }
   __syncthreads();                                            // barrier init visible before anyone waits
   mbar_wait(&bar[0], 0);                                      // chunk 0 + the qp / v slices
-  for (int s = w; s < n; s += ATT_WARPS) {
-    mbar_wait(&bar[s / R], 0);
-    T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
-    const float p = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, true, z_out, nullptr);
-    if (lane == 0) sc_part[s] = p;
+  for (int k = 0, s = w; k * R < n; ++k) {                   // chunk by chunk: one wait per chunk
+    const int s1 = min(n, (k + 1) * R);
+    if (s >= s1) continue;
+    mbar_wait(&bar[k], 0);
+    for (; s < s1; s += ATT_WARPS) {
+      T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
+      const float p = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, true, z_out, nullptr);
+      if (lane == 0) sc_part[s] = p;
+    }
   }
   if (Z_st) {                                                 // masked positions: zeros in this slice
     float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -799,21 +803,25 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   if (n > 0) mbar_wait(&bar[0], 0);
   ECHO_PHASE(2);
   // phase 1: E = tanh(z) into smem (fp32), partial scores (RECOMPUTE) and partial dalpha
-  for (int s = w; s < n; s += ATT_WARPS) {
-    mbar_wait(&bar[s / R], 0);
-    const float ps = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, recompute, nullptr, E + (size_t)s * Wb);
-    float acc = 0.0f;
-    const T* hrow = hs + (size_t)s * WHb;
-    for (int c4 = lane; c4 < WH / 4; c4 += 32) {
-      float h4[4];
-      lds4(hrow + c4 * 4, h4);
+  for (int k = 0, s = w; k * R < n; ++k) {                   // chunk by chunk: one wait per chunk
+    const int s1 = min(n, (k + 1) * R);
+    if (s >= s1) continue;
+    mbar_wait(&bar[k], 0);
+    for (; s < s1; s += ATT_WARPS) {
+      const float ps = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, recompute, nullptr, E + (size_t)s * Wb);
+      float acc = 0.0f;
+      const T* hrow = hs + (size_t)s * WHb;
+      for (int c4 = lane; c4 < WH / 4; c4 += 32) {
+        float h4[4];
+        lds4(hrow + c4 * 4, h4);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc = __fmaf_rn(dcs[c4 * 4 + k], h4[k], acc);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      sc_part[s] = ps;
-      dal_part[s] = acc;
+        for (int q = 0; q < 4; ++q) acc = __fmaf_rn(dcs[c4 * 4 + q], h4[q], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        sc_part[s] = ps;
+        dal_part[s] = acc;
+      }
     }
   }
   // L2 prefetch of the dKp / dH_s tiles phase 4 streams, issued by thread 0 once this CTA's loads

@@ -22,6 +22,8 @@ the real activation footprint.
 """
 from __future__ import annotations
 
+from contextlib import contextmanager
+
 import numpy as np
 import torch
 
@@ -75,6 +77,8 @@ class NMTModel:
         self.stash = {}
         self.graph = None
         self.grad_hook = None          # e.g. dp.allreduce_mean_ (called on the flat fp32 gradient)
+        self.probe = None              # timing-event capture (see capture(probe=True))
+        self.probe_events = None
 
     # ------------------------------------------------------------ parameters / io
     def w(self, name):
@@ -119,9 +123,11 @@ class NMTModel:
                 self.sflat.copy_(self.master)
 
     # ------------------------------------------------------------ CUDA graph of the whole step
-    def capture(self, lr=0.1, warmup=2):
+    def capture(self, lr=0.1, warmup=2, probe=False):
         """Record forward + backward (+ allreduce hook) + SGD into one CUDA graph.  The static
-        input buffers (self.inputs) are read by the graph; replay() runs one training step."""
+        input buffers (self.inputs) are read by the graph; replay() runs one training step.
+        probe=True also records timing events (graph event-record nodes) around every a5 / a6
+        launch; after a replay, kernel_times() returns their durations for that step."""
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
@@ -130,10 +136,29 @@ class NMTModel:
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
         self.graph = torch.cuda.CUDAGraph()
+        self.probe = {} if probe else None
         with torch.cuda.graph(self.graph):
             self.step(lr)
+        self.probe_events, self.probe = self.probe, None
         torch.cuda.synchronize(self.device)
         return self.graph
+
+    @contextmanager
+    def _timed(self, name):
+        if self.probe is None:
+            yield
+            return
+        e0 = torch.cuda.Event(enable_timing=True, external=True)
+        e1 = torch.cuda.Event(enable_timing=True, external=True)
+        e0.record()
+        yield
+        e1.record()
+        self.probe.setdefault(name, []).append((e0, e1))
+
+    def kernel_times(self):
+        """{name: [ms per launch]} of the probed launches in the most recent replay (synchronizes)."""
+        torch.cuda.synchronize(self.device)
+        return {k: [a.elapsed_time(b) for a, b in v] for k, v in (self.probe_events or {}).items()}
 
     def replay(self):
         self.graph.replay()
@@ -204,12 +229,13 @@ class NMTModel:
             q = dec[-1].h_slot(t)
             qp = qp_buf if md == abi.STASH else a["qp_st"][t]
             torch.mm(q, Wq.t(), out=qp)
-            if md == abi.STASH:
-                ctx = a["ctx_st"][t]
-                abi.echo_attn_fwd(adesc, qp, Kp, v, Hs, sl, ctx, a["E_st"][t], a["al_st"][t])
-            else:
-                ctx = ctx_tmp
-                abi.echo_attn_fwd(adesc, qp, Kp, v, Hs, sl, ctx, None, None)
+            with self._timed("attn_fwd"):
+                if md == abi.STASH:
+                    ctx = a["ctx_st"][t]
+                    abi.echo_attn_fwd(adesc, qp, Kp, v, Hs, sl, ctx, a["E_st"][t], a["al_st"][t])
+                else:
+                    ctx = ctx_tmp
+                    abi.echo_attn_fwd(adesc, qp, Kp, v, Hs, sl, ctx, None, None)
             torch.mm(ctx, Wcc.t(), out=pre)
             addmm_(pre, q, Wch.t())
             torch.tanh(pre, out=Aall[t])
@@ -326,12 +352,13 @@ class NMTModel:
             with tf32(lowp):
                 torch.mm(dPRE[t], Wcc32, out=dctx)
                 top.addmm_(dPRE[t], Wch32)
-            if md == abi.STASH:
-                abi.echo_attn_bwd(adesc, None, None, v, Hs, sl, a["E_st"][t], a["al_st"][t], dctx, dQP[t], dKp, dHs,
-                                  dv_part, None)
-            else:                                                # a6 regenerates E, scores, alpha, ctx
-                abi.echo_attn_bwd(adesc, a["qp_st"][t], Kp, v, Hs, sl, None, None, dctx, dQP[t], dKp, dHs,
-                                  dv_part, ctx_all[t])
+            with self._timed("attn_bwd"):
+                if md == abi.STASH:
+                    abi.echo_attn_bwd(adesc, None, None, v, Hs, sl, a["E_st"][t], a["al_st"][t], dctx, dQP[t], dKp,
+                                      dHs, dv_part, None)
+                else:                                            # a6 regenerates E, scores, alpha, ctx
+                    abi.echo_attn_bwd(adesc, a["qp_st"][t], Kp, v, Hs, sl, None, None, dctx, dQP[t], dKp, dHs,
+                                      dv_part, ctx_all[t])
             with tf32(lowp):
                 top.addmm_(dQP[t], Wq32)
             for l in reversed(range(Ld)):
