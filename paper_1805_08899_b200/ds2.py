@@ -15,13 +15,13 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import abi
+from . import abi, probe
 from .gemm import mm, addmm_
 from .lstm import LSTMLayer, TORCH_DTYPE
 from synth.data import ds2_param_shapes
 
 
-class DS2Model:
+class DS2Model(probe.GraphStep):
     def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda"):
         abi.load()
         self.cfg, self.dtype, self.mode = cfg, dtype, mode
@@ -48,7 +48,9 @@ class DS2Model:
         self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.stash = {}
         self.grad_hook = None
-        self.graph = None
+        # the two directions of a layer are independent recurrences: the reverse one runs on a side
+        # stream (a parallel branch of the step's CUDA graph), joined before anything reads both
+        self.side = torch.cuda.Stream(device=self.device)
 
     def load_params(self, params):
         for name, _ in self.shapes:
@@ -92,22 +94,15 @@ class DS2Model:
             if self.sflat is not self.master:
                 self.sflat.copy_(self.master)
 
-    def capture(self, lr=0.1, warmup=2):
-        s = torch.cuda.Stream(device=self.device)
-        s.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(s):
-            for _ in range(warmup):
-                self.step(lr)
-        torch.cuda.current_stream(self.device).wait_stream(s)
-        torch.cuda.synchronize(self.device)
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self.step(lr)
-        torch.cuda.synchronize(self.device)
-        return self.graph
-
-    def replay(self):
-        self.graph.replay()
+    def _both(self, fw, bw):
+        """Run fw() on the current stream and bw() on the side stream; join; return both results."""
+        cur = torch.cuda.current_stream(self.device)
+        self.side.wait_stream(cur)
+        r_fw = fw()
+        with torch.cuda.stream(self.side):
+            r_bw = bw()
+        cur.wait_stream(self.side)
+        return r_fw, r_bw
 
     def _inputs(self, l, low):
         """(X_i, W_i) input projections of layer l for one direction's Wx."""
@@ -120,13 +115,14 @@ class DS2Model:
         layers = []
         low = None
         for l in range(c.layers):
-            pair = []
-            for d, rev in (("fw", False), ("bw", True)):
-                L = LSTMLayer(T, B, H, self.dtype, md, dev, reverse=rev)
+            pair = [LSTMLayer(T, B, H, self.dtype, md, dev, reverse=rev) for rev in (False, True)]
+
+            def run(d, L, l=l, low=low):
                 Wx = self.S[f"l{l}.{d}.Wx"]
                 ins = [(self.x, Wx)] if l == 0 else [(low[0].h, Wx[:, :H]), (low[1].h, Wx[:, H:])]
                 L.forward_multi(ins, self.S[f"l{l}.{d}.Wh"], self.P[f"l{l}.{d}.b"], self.zero_h, self.zero_c)
-                pair.append(L)
+
+            self._both(lambda: run("fw", pair[0]), lambda: run("bw", pair[1]))
             if md == abi.RECOMPUTE and low is not None:
                 low[0].h = low[1].h = None                    # lower outputs only fed the input FCs
             layers.append(pair)
@@ -168,15 +164,22 @@ class DS2Model:
         above = None                                          # (layer pair, its weights) awaiting input dW
         for l in reversed(range(c.layers)):
             pair = layers[l]
-            dX = None
-            for j, (d, L) in enumerate(zip(("fw", "bw"), pair)):
+
+            def run(j, l=l, pair=pair, dH=dH):
+                d = ("fw", "bw")[j]
                 Wx = self.S[f"l{l}.{d}.Wx"]
                 ins = [(None, Wx)] if l == 0 else [(None, Wx[:, :H]), (None, Wx[:, H:])]
-                r = L.backward_multi(ins, self.S[f"l{l}.{d}.Wh"], dH[j], need_dX=l > 0, need_dW=False, release=False)
+                return pair[j].backward_multi(ins, self.S[f"l{l}.{d}.Wh"], dH[j], need_dX=l > 0, need_dW=False,
+                                              release=False)
+
+            rs = self._both(lambda: run(0), lambda: run(1))
+            dX = None
+            for d, r in zip(("fw", "bw"), rs):                  # joined: combine in fixed order
                 G[f"l{l}.{d}.Wh"].copy_(r["dWh"])
                 G[f"l{l}.{d}.b"].copy_(r["db"])
                 if l > 0:
                     dX = r["dX"] if dX is None else [dX[0].add_(r["dX"][0]), dX[1].add_(r["dX"][1])]
+            del rs
             outs = [pair[0].h_time(), pair[1].h_time()]         # stashed, or regenerated by a3
             if above is None:                                  # output FC (deferred dW, Eq. 2)
                 G["out.W"][:, :H].copy_(mm(dlog_s.t(), outs[0].reshape(N, H), torch.float32))

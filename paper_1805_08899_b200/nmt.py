@@ -22,12 +22,10 @@ the real activation footprint.
 """
 from __future__ import annotations
 
-from contextlib import contextmanager
-
 import numpy as np
 import torch
 
-from . import abi
+from . import abi, probe
 from .gemm import mm, addmm_, tf32
 from .lstm import LSTMLayer, TORCH_DTYPE
 from synth.data import nmt_param_shapes
@@ -43,7 +41,7 @@ def _det_index_add(dst, idx, src):
         torch.use_deterministic_algorithms(prev, warn_only=True)
 
 
-class NMTModel:
+class NMTModel(probe.GraphStep):
     def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda"):
         abi.load()
         self.cfg = cfg
@@ -75,10 +73,7 @@ class NMTModel:
         }
         self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.stash = {}
-        self.graph = None
         self.grad_hook = None          # e.g. dp.allreduce_mean_ (called on the flat fp32 gradient)
-        self.probe = None              # timing-event capture (see capture(probe=True))
-        self.probe_events = None
 
     # ------------------------------------------------------------ parameters / io
     def w(self, name):
@@ -121,47 +116,6 @@ class NMTModel:
             self.master.add_(self.gflat, alpha=-lr)
             if self.sflat is not self.master:
                 self.sflat.copy_(self.master)
-
-    # ------------------------------------------------------------ CUDA graph of the whole step
-    def capture(self, lr=0.1, warmup=2, probe=False):
-        """Record forward + backward (+ allreduce hook) + SGD into one CUDA graph.  The static
-        input buffers (self.inputs) are read by the graph; replay() runs one training step.
-        probe=True also records timing events (graph event-record nodes) around every a5 / a6
-        launch; after a replay, kernel_times() returns their durations for that step."""
-        s = torch.cuda.Stream(device=self.device)
-        s.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(s):
-            for _ in range(warmup):
-                self.step(lr)
-        torch.cuda.current_stream(self.device).wait_stream(s)
-        torch.cuda.synchronize(self.device)
-        self.graph = torch.cuda.CUDAGraph()
-        self.probe = {} if probe else None
-        with torch.cuda.graph(self.graph):
-            self.step(lr)
-        self.probe_events, self.probe = self.probe, None
-        torch.cuda.synchronize(self.device)
-        return self.graph
-
-    @contextmanager
-    def _timed(self, name):
-        if self.probe is None:
-            yield
-            return
-        e0 = torch.cuda.Event(enable_timing=True, external=True)
-        e1 = torch.cuda.Event(enable_timing=True, external=True)
-        e0.record()
-        yield
-        e1.record()
-        self.probe.setdefault(name, []).append((e0, e1))
-
-    def kernel_times(self):
-        """{name: [ms per launch]} of the probed launches in the most recent replay (synchronizes)."""
-        torch.cuda.synchronize(self.device)
-        return {k: [a.elapsed_time(b) for a, b in v] for k, v in (self.probe_events or {}).items()}
-
-    def replay(self):
-        self.graph.replay()
 
     # ------------------------------------------------------------ forward
     def _forward(self):
@@ -229,7 +183,7 @@ class NMTModel:
             q = dec[-1].h_slot(t)
             qp = qp_buf if md == abi.STASH else a["qp_st"][t]
             torch.mm(q, Wq.t(), out=qp)
-            with self._timed("attn_fwd"):
+            with probe.timed("attn_fwd"):
                 if md == abi.STASH:
                     ctx = a["ctx_st"][t]
                     abi.echo_attn_fwd(adesc, qp, Kp, v, Hs, sl, ctx, a["E_st"][t], a["al_st"][t])
@@ -352,7 +306,7 @@ class NMTModel:
             with tf32(lowp):
                 torch.mm(dPRE[t], Wcc32, out=dctx)
                 top.addmm_(dPRE[t], Wch32)
-            with self._timed("attn_bwd"):
+            with probe.timed("attn_bwd"):
                 if md == abi.STASH:
                     abi.echo_attn_bwd(adesc, None, None, v, Hs, sl, a["E_st"][t], a["al_st"][t], dctx, dQP[t], dKp,
                                       dHs, dv_part, None)

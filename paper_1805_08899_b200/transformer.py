@@ -20,13 +20,13 @@ import math
 import numpy as np
 import torch
 
-from . import abi
+from . import abi, probe
 from .gemm import mm
 from .lstm import TORCH_DTYPE
 from synth.data import tx_param_shapes
 
 
-class TXModel:
+class TXModel(probe.GraphStep):
     def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda"):
         abi.load()
         self.cfg, self.dtype, self.mode = cfg, dtype, mode
@@ -50,7 +50,6 @@ class TXModel:
         self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.stash = {}
         self.grad_hook = None
-        self.graph = None
 
     def load_params(self, params):
         for name, _ in self.shapes:
@@ -107,23 +106,6 @@ class TXModel:
             if self.sflat is not self.master:
                 self.sflat.copy_(self.master)
 
-    def capture(self, lr=0.1, warmup=2):
-        s = torch.cuda.Stream(device=self.device)
-        s.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(s):
-            for _ in range(warmup):
-                self.step(lr)
-        torch.cuda.current_stream(self.device).wait_stream(s)
-        torch.cuda.synchronize(self.device)
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self.step(lr)
-        torch.cuda.synchronize(self.device)
-        return self.graph
-
-    def replay(self):
-        self.graph.replay()
-
     def _forward(self):
         c, sd, dev, md = self.cfg, self.sd, self.device, self.mode
         R, L = c.B * c.heads * c.L, c.L
@@ -142,7 +124,8 @@ class TXModel:
             else:
                 P = None
                 mask = torch.empty(R * L // 8, dtype=torch.uint8, device=dev)
-            abi.echo_dot_softmax_fwd(self.desc(k), S, Pd, P, mask)
+            with probe.timed("dot_fwd"):
+                abi.echo_dot_softmax_fwd(self.desc(k), S, Pd, P, mask)
             O = self._merge(torch.matmul(Pd, vh))
             y = torch.addmm(x, O, self.S[f"b{k}.Wo"].t())               # residual
             blk = {"x": x, "qh": qh, "kh": kh, "vh": vh, "mask": mask, "O": O}
@@ -180,11 +163,13 @@ class TXModel:
             dOh = self._heads(mm(dys, self.S[f"b{k}.Wo"], torch.float32).to(sd))
             dPd = torch.matmul(dOh, vh.transpose(-1, -2))
             if md == abi.STASH:
-                abi.echo_dot_softmax_bwd(self.desc(k), None, blk["P"], blk["mask"], dPd, dPd, None)
+                with probe.timed("dot_bwd"):
+                    abi.echo_dot_softmax_bwd(self.desc(k), None, blk["P"], blk["mask"], dPd, dPd, None)
                 Pd = blk["Pd"]
             else:
                 Pd = torch.empty_like(dPd)
-                abi.echo_dot_softmax_bwd(self.desc(k), blk["S"], None, blk["mask"], dPd, dPd, Pd)
+                with probe.timed("dot_bwd"):
+                    abi.echo_dot_softmax_bwd(self.desc(k), blk["S"], None, blk["mask"], dPd, dPd, Pd)
             dS = dPd                                                   # dS written in place (scale included)
             dV = self._merge(torch.matmul(Pd.transpose(-1, -2), dOh))
             dQ = self._merge(torch.matmul(dS, kh))
