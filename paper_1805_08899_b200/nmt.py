@@ -22,6 +22,8 @@ the real activation footprint.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -99,6 +101,22 @@ class NMTModel(probe.GraphStep):
     def input_bytes(self):
         return sum(t.numel() * t.element_size() for t in self.inputs.values())
 
+    # ------------------------------------------------------------ encoder wavefront helpers
+    def _chunks(self, T):
+        """Wavefront chunk boundaries over the encoder's time axis.  Measured on C2 (bench, CUDA
+        graph): fp32 29.9 -> 28.1 ms/step with 5 chunks (its SIMT GEMMs leave most SMs idle, so two
+        layers' recurrences overlap well); bf16 8.91 -> 9.09 ms (tensor-core GEMMs already fill the
+        GPU; the cross-stream waits cost more than the overlap gains) -> 1 chunk (back to back)."""
+        n = int(os.environ.get("ECHO_ENC_CHUNKS", "5" if self.sd == torch.float32 else "1"))
+        n = max(1, min(n, T))
+        return [(T * i) // n for i in range(n + 1)]
+
+    def _layer_streams(self, n):
+        """[current stream] + n-1 side streams (created once) for per-layer wavefronts."""
+        if not hasattr(self, "_side") or len(self._side) < n - 1:
+            self._side = [torch.cuda.Stream(device=self.device) for _ in range(n - 1)]
+        return [torch.cuda.current_stream(self.device)] + self._side[: n - 1]
+
     # ------------------------------------------------------------ one training step
     def train_step(self, inputs=None, lr=0.1):
         """Forward + backward + SGD.  Returns the loss as a float (one D2H read)."""
@@ -126,19 +144,31 @@ class NMTModel(probe.GraphStep):
         # encoder ------------------------------------------------------------
         X0 = self.w("emb_src").index_select(0, inp["src"].t().reshape(-1)).view(Ts, B, E)
         a["X0"] = X0
-        enc = []
-        X = X0
-        for l in range(cfg.enc_layers):
-            L = LSTMLayer(Ts, B, H, self.dtype, md, dev)
-            L.forward_seq(X, self.w(f"enc{l}.Wx"), self.w(f"enc{l}.Wh"), self.P[f"enc{l}.b"], self.zero_h, self.zero_c)
-            if md == abi.RECOMPUTE and l > 0:
-                enc[l - 1].h = None                              # lower layer's output was only the FC input
-            enc.append(L)
-            X = L.h
-            if l == 0 and md == abi.RECOMPUTE:
-                a["X0"] = None                                   # embeddings: recomputed from the tokens
+        enc = [LSTMLayer(Ts, B, H, self.dtype, md, dev) for _ in range(cfg.enc_layers)]
+        # wavefront: layer l runs on its own stream and starts chunk c as soon as layer l-1 finished
+        # it (per-chunk events); the layers' recurrences overlap instead of running back to back
+        bounds = self._chunks(Ts)
+        streams = self._layer_streams(len(enc))
+        done = [[torch.cuda.Event() for _ in bounds[:-1]] for _ in enc]
+        for st in streams[1:]:
+            st.wait_stream(streams[0])
+        for l, L in enumerate(enc):
+            X = X0 if l == 0 else enc[l - 1].h
+            with torch.cuda.stream(streams[l]):
+                for c in range(len(bounds) - 1):
+                    if l > 0:
+                        streams[l].wait_event(done[l - 1][c])
+                    L.forward_range(bounds[c], bounds[c + 1], X, self.w(f"enc{l}.Wx"), self.w(f"enc{l}.Wh"),
+                                    self.P[f"enc{l}.b"], self.zero_h, self.zero_c)
+                    done[l][c].record(streams[l])
+        for st in streams[1:]:
+            streams[0].wait_stream(st)
+        if md == abi.RECOMPUTE:
+            for L in enc[:-1]:
+                L.h = None                                       # lower layers' outputs only fed the FCs
+            a["X0"] = None                                       # embeddings: recomputed from the tokens
         a["enc"] = enc
-        Hs = X                                                   # [Ts,B,H] s-major source hidden state
+        Hs = enc[-1].h                                           # [Ts,B,H] s-major source hidden state
         a["Hs"] = Hs
         Kp = torch.empty(Ts, B, A, dtype=sd, device=dev)        # Kp = Hs W_k^T + b_q (bias folded, R3)
         torch.addmm(self.P["att.bq"].to(sd), Hs.view(Ts * B, H), self.w("att.Wk").t(), out=Kp.view(Ts * B, A))
@@ -372,19 +402,47 @@ class NMTModel(probe.GraphStep):
         dKps = None
         del Hs, Hs32
         del dKp, dKpf, dKps
-        # encoder, top-down; dW_x of layer l+1 needs this layer's h (stashed or regenerated) ---
+        # encoder, top-down wavefront: layer l (its own stream) runs chunk c of its backward once
+        # layer l+1 finished chunk c; dH_l[t] = dA_{l+1}[t] W_x^{l+1} is accumulated per chunk (the
+        # recurrent term of a chunk's first step lands first at chunk boundaries: fixed order, both
+        # modes).  dW_x of layer l+1 needs this layer's h (stashed or regenerated) ---------------
         Le = len(enc)
         n = Ts * B
-        dH = dHs
+        bounds = self._chunks(Ts)
+        nch = len(bounds) - 1
+        streams = self._layer_streams(Le)                        # [current, side...]; top layer on current
+        done = [[torch.cuda.Event() for _ in range(nch)] for _ in range(Le)]
+        for st in streams[1:]:                                   # fork after dH_s is complete
+            st.wait_stream(streams[0])
+        dHl = [None] * Le
+        dHl[Le - 1] = dHs
         for l in reversed(range(Le)):
             L = enc[l]
-            L.prepare_backward()
-            dc = torch.zeros(B, H, dtype=torch.float32, device=dev)
-            Wh = self.w(f"enc{l}.Wh")
-            for t in reversed(range(Ts)):
-                L.bwd_step(t, dH[t], dc)
-                if t > 0:
-                    addmm_(dH[t - 1], L.gates[t], Wh)
+            st = streams[Le - 1 - l]
+            with torch.cuda.stream(st):
+                L.prepare_backward()
+                dc = torch.zeros(B, H, dtype=torch.float32, device=dev)
+                Wh = self.w(f"enc{l}.Wh")
+                if l < Le - 1:
+                    dHl[l] = torch.zeros(Ts, B, H, dtype=torch.float32, device=dev)
+                dH = dHl[l]
+                for c in reversed(range(nch)):
+                    t0, t1 = bounds[c], bounds[c + 1]
+                    if l < Le - 1:
+                        st.wait_event(done[l + 1][c])
+                        up = enc[l + 1]
+                        addmm_(dH[t0:t1].view((t1 - t0) * B, H), up.gates[t0:t1].view((t1 - t0) * B, 4 * H),
+                               self.w(f"enc{l + 1}.Wx"))
+                    for t in reversed(range(t0, t1)):
+                        L.bwd_step(t, dH[t], dc)
+                        if t > 0:
+                            addmm_(dH[t - 1], L.gates[t], Wh)
+                    done[l][c].record(st)
+        for st in streams[1:]:
+            streams[0].wait_stream(st)
+        del dHl
+        for l in reversed(range(Le)):
+            L = enc[l]
             dAl = L.gates.view(n, 4 * H)
             hg = L.h_for_grad()
             G[f"enc{l}.b"].copy_(dAl.float().sum(0))
@@ -394,8 +452,8 @@ class NMTModel(probe.GraphStep):
                 up = enc[l + 1]
                 gi(G[f"enc{l + 1}.Wx"], up.gates.view(n, 4 * H).t(), hg.reshape(n, H))
                 enc[l + 1] = None
-            dX = mm(dAl, self.w(f"enc{l}.Wx"), torch.float32).view(Ts, B, -1)
             if l == 0:
+                dX = mm(dAl, self.w(f"enc{l}.Wx"), torch.float32).view(Ts, B, -1)
                 X0 = a["X0"] if md == abi.STASH else \
                     self.w("emb_src").index_select(0, self.inputs["src"].t().reshape(-1))      # recomputed
                 gi(G["enc0.Wx"], dAl.t(), X0.view(n, E))
@@ -403,5 +461,4 @@ class NMTModel(probe.GraphStep):
                 _det_index_add(G["emb_src"], self.inputs["src"].t().reshape(-1), dX.view(n, E))
                 enc[0] = None
             L.release_backward()
-            dH = dX
         a["enc"] = None

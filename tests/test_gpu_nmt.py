@@ -66,6 +66,32 @@ def test_nmt_run_to_run_bitwise(cuda_dev):
 
 
 @pytest.mark.parametrize("storage", ["fp32", "bf16"])
+def test_nmt_c2_eager_graph_bitwise(storage, cuda_dev):
+    """C2: the eager step, a second eager step and the CUDA-graph replay (the bench launch path,
+    encoder wavefront on two streams) give bit-identical gradients — a cross-stream race or a
+    capture bug shows up here."""
+    from paper_1805_08899_b200 import abi
+    from paper_1805_08899_b200.nmt import NMTModel
+    cfg = C2
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    params = nmt_params(5, cfg, storage)
+    batch = nmt_batch(6, cfg)
+    m = NMTModel(cfg, dtype=dt, mode=abi.RECOMPUTE)
+    m.load_params(params)
+    m.upload_batch(batch)
+    m.step(0.0)
+    g1 = m.gflat.clone()
+    m.step(0.0)
+    g2 = m.gflat.clone()
+    m.capture(0.0)
+    m.gflat.zero_()
+    m.replay()
+    torch.cuda.synchronize()
+    assert bits_equal(g1, g2)
+    assert bits_equal(g1, m.gflat)
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
 def test_nmt_c2_full_size_parity(storage, cuda_dev):
     """C2 (B=128, T=50, H=512, V=8192) one step vs the fp64 oracle (all gradients), RECOMPUTE,
     in the launch configuration bench.py times."""
