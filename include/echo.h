@@ -194,6 +194,23 @@ echo_status echo_dot_softmax_bwd(const echo_dot_desc* d, const void* S, const vo
                                  const uint8_t* mask, const void* dPd, void* dS, void* Pd_regen,
                                  void* stream);
 
+/* ===================================================================== output layer
+ * Fused softmax cross-entropy of the model's output layer (§2; reading
+ * R10: mean CE over the N = B*Td target tokens).  Outside the Echo decision (its probabilities
+ * are kept in both modes) -- one pass instead of the ~10 framework launches of the plain form.
+ *  N, V          rows (tokens) and classes; V <= 51200
+ *  logits        [N, V] fp32, row-major, IN: x W^T (bias not yet added); OUT: overwritten in
+ *                place with dLoss/dlogits = (softmax(x + bias) - onehot(label)) / N
+ *  bias          [V] fp32 or NULL
+ *  labels        [N] int64 in [0, V) (not checked on the device)
+ *  row_loss      [N] fp32 OUT: logsumexp(x + b) - (x + b)[label]; the loss is their mean
+ *  dlogits_bf16  [N, V] bf16 OUT copy of dLoss/dlogits (round to nearest) or NULL
+ * All device pointers; 16-byte aligned logits / bias (8-byte bf16 output) when V % 4 == 0.
+ * Deterministic (fixed-order block reductions).  Errors: ECHO_ERR_INVALID, ECHO_ERR_CAPACITY.  */
+echo_status echo_xent_fwd_bwd(int32_t N, int32_t V, float* logits, const float* bias,
+                              const int64_t* labels, float* row_loss, void* dlogits_bf16,
+                              void* stream);
+
 /* ===================================================================== footprint estimator
  * Host-only, integer, deterministic.  Runs the adjusted pass pipeline of
  * Fig. 14: Gradient -> InferShape&Type -> EdgeUseRef ->

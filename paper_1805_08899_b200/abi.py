@@ -20,7 +20,7 @@ STASH, RECOMPUTE = 0, 1
 
 EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_cscan", "echo_lstm_bwd",
             "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
-            "echo_dot_softmax_bwd", "echo_footprint_estimate")
+            "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_footprint_estimate")
 
 
 class EchoError(RuntimeError):
@@ -73,6 +73,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_attn_dv_reduce": [i32, i32, vp, vp, i32, vp],
         "echo_dot_softmax_fwd": [ctypes.POINTER(DotDesc)] + [vp] * 5,
         "echo_dot_softmax_bwd": [ctypes.POINTER(DotDesc)] + [vp] * 7,
+        "echo_xent_fwd_bwd": [i32, i32, vp, vp, vp, vp, vp, vp],
         "echo_footprint_estimate": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)],
     }
     for name, args in sigs.items():
@@ -151,6 +152,12 @@ def echo_attn_dv_reduce(B, A, dv_part, dv, accumulate, stream=None):
 def echo_dot_softmax_fwd(d, S, Pd, P_st, mask, stream=None):
     LAUNCHES["count"] += 1
     _check(load().echo_dot_softmax_fwd(ctypes.byref(d), _p(S), _p(Pd), _p(P_st), _p(mask), _stream(stream)))
+
+
+def echo_xent_fwd_bwd(N, V, logits, bias, labels, row_loss, dlogits_bf16=None, stream=None):
+    LAUNCHES["count"] += 1
+    _check(load().echo_xent_fwd_bwd(N, V, _p(logits), _p(bias), _p(labels), _p(row_loss), _p(dlogits_bf16),
+                                    _stream(stream)))
 
 
 def echo_dot_softmax_bwd(d, S, P_st, mask, dPd, dS, Pd_regen, stream=None):

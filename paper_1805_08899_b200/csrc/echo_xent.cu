@@ -1,0 +1,120 @@
+// echo_xent.cu — fused output-layer softmax cross-entropy (forward loss + dLoss/dlogits).
+//
+// Not an Echo feature map decision (the CE probabilities are kept in both modes);
+// it is the model's output layer (§2, reading R10: mean CE over the B*Td
+// target tokens) fused into one pass so the step does not spend ~10 torch elementwise / reduce
+// launches and ~2 GB of HBM traffic on it at C2.
+//
+// One CTA per row: the row (+ bias) is staged in shared memory once, max and sum(exp) are fixed-
+// order block reductions, then the row is overwritten in place with (softmax - onehot) / N
+// (fp32, the CE feature map) and optionally also written in bf16 for the backward GEMMs.
+#include "echo_common.cuh"
+
+#include <math.h>
+
+namespace echo {
+
+constexpr int XENT_THREADS = 256;
+
+__device__ __forceinline__ float block_reduce(float v, float* red, bool is_max) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = is_max ? warp_max(v) : warp_sum(v);
+  __syncthreads();                       // red[] reuse across calls
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  float r = red[0];
+  for (int i = 1; i < XENT_THREADS / 32; ++i) r = is_max ? fmaxf(r, red[i]) : __fadd_rn(r, red[i]);
+  return r;
+}
+
+__global__ void __launch_bounds__(XENT_THREADS) xent_kernel(int N, int V, const float* __restrict__ bias,
+                                                            float* __restrict__ logits,
+                                                            const int64_t* __restrict__ labels,
+                                                            float* __restrict__ row_loss,
+                                                            __nv_bfloat16* __restrict__ dlog_bf16) {
+  pdl_wait();
+  extern __shared__ float xrow[];
+  __shared__ float red[XENT_THREADS / 32];
+  const int tid = threadIdx.x;
+  const bool vec = (V & 3) == 0;
+  const float fn = (float)N;
+  for (int r = blockIdx.x; r < N; r += gridDim.x) {
+    float* x = logits + (size_t)r * V;
+    float m = -INFINITY;
+    if (vec) {
+      for (int i = tid; i < V / 4; i += XENT_THREADS) {
+        float4 a = *reinterpret_cast<const float4*>(x + 4 * i);
+        if (bias) {
+          const float4 bb = *reinterpret_cast<const float4*>(bias + 4 * i);
+          a.x = __fadd_rn(a.x, bb.x); a.y = __fadd_rn(a.y, bb.y); a.z = __fadd_rn(a.z, bb.z); a.w = __fadd_rn(a.w, bb.w);
+        }
+        *reinterpret_cast<float4*>(xrow + 4 * i) = a;
+        m = fmaxf(m, fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)));
+      }
+    } else {
+      for (int i = tid; i < V; i += XENT_THREADS) {
+        const float a = bias ? __fadd_rn(x[i], bias[i]) : x[i];
+        xrow[i] = a;
+        m = fmaxf(m, a);
+      }
+    }
+    m = block_reduce(m, red, true);
+    float s = 0.0f;
+    for (int i = tid; i < V; i += XENT_THREADS) s = __fadd_rn(s, expf(__fsub_rn(xrow[i], m)));
+    s = block_reduce(s, red, false);
+    const float lse = __fadd_rn(m, logf(s));
+    const int64_t y = labels[r];
+    if (tid == 0) row_loss[r] = __fsub_rn(lse, xrow[y]);
+    __nv_bfloat16* ob = dlog_bf16 ? dlog_bf16 + (size_t)r * V : nullptr;
+    if (vec) {
+      for (int i = tid; i < V / 4; i += XENT_THREADS) {
+        const float4 a = *reinterpret_cast<const float4*>(xrow + 4 * i);
+        float p[4] = {expf(__fsub_rn(a.x, lse)), expf(__fsub_rn(a.y, lse)), expf(__fsub_rn(a.z, lse)),
+                      expf(__fsub_rn(a.w, lse))};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p[k] = __fdiv_rn(4 * i + k == y ? __fsub_rn(p[k], 1.0f) : p[k], fn);
+        *reinterpret_cast<float4*>(x + 4 * i) = make_float4(p[0], p[1], p[2], p[3]);
+        if (ob) {
+          uint2 u;
+          *reinterpret_cast<__nv_bfloat162*>(&u.x) = __floats2bfloat162_rn(p[0], p[1]);
+          *reinterpret_cast<__nv_bfloat162*>(&u.y) = __floats2bfloat162_rn(p[2], p[3]);
+          *reinterpret_cast<uint2*>(ob + 4 * i) = u;
+        }
+      }
+    } else {
+      for (int i = tid; i < V; i += XENT_THREADS) {
+        float p = expf(__fsub_rn(xrow[i], lse));
+        p = __fdiv_rn(i == y ? __fsub_rn(p, 1.0f) : p, fn);
+        x[i] = p;
+        if (ob) ob[i] = __float2bfloat16_rn(p);
+      }
+    }
+    __syncthreads();                     // xrow reuse by the next row
+  }
+}
+
+}  // namespace echo
+
+using namespace echo;
+
+extern "C" echo_status echo_xent_fwd_bwd(int32_t N, int32_t V, float* logits, const float* bias,
+                                         const int64_t* labels, float* row_loss, void* dlogits_bf16,
+                                         void* stream) {
+  const char* fn = "echo_xent_fwd_bwd";
+  if (N <= 0 || V <= 0) return fail(ECHO_ERR_INVALID, "%s: N=%d V=%d must be > 0", fn, N, V);
+  if (!logits || !labels || !row_loss) return fail(ECHO_ERR_INVALID, "%s: NULL logits / labels / row_loss", fn);
+  if ((V & 3) == 0 && (!aligned16(logits) || (bias && !aligned16(bias)) || (dlogits_bf16 && ((uintptr_t)dlogits_bf16 & 7))))
+    return fail(ECHO_ERR_INVALID, "%s: logits / bias must be 16-byte (bf16 output 8-byte) aligned", fn);
+  const size_t smem = (size_t)V * sizeof(float);
+  if (smem > 200 * 1024) return fail(ECHO_ERR_CAPACITY, "%s: V=%d exceeds the shared-memory row (51200)", fn, V);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute((const void*)xent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+    if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: cudaFuncSetAttribute: %s", fn, cudaGetErrorString(e));
+  }
+  const int grid = N < 148 * 16 ? N : 148 * 16;
+  const cudaError_t e = launch(xent_kernel, dim3(grid), dim3(XENT_THREADS), smem, (cudaStream_t)stream, 1, N, V, bias,
+                               logits, labels, row_loss, (__nv_bfloat16*)dlogits_bf16);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
+}

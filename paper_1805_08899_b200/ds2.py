@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import abi, probe
-from .gemm import mm, addmm_
+from .gemm import mm, addmm_, colsum as _colsum
 from .lstm import LSTMLayer, TORCH_DTYPE
 from synth.data import ds2_param_shapes
 
@@ -131,16 +131,11 @@ class DS2Model(probe.GraphStep):
         Wo = self.S["out.W"]
         logits = mm(low[0].h.reshape(N, H), Wo[:, :H].t(), torch.float32)
         logits.add_(mm(low[1].h.reshape(N, H), Wo[:, H:].t(), torch.float32))
-        logits.add_(self.P["out.b"])
         if md == abi.RECOMPUTE:
             low[0].h = low[1].h = None
-        y = self.labels
-        lse = torch.logsumexp(logits, dim=1)
-        torch.sub(lse.sum(), logits.gather(1, y[:, None]).sum(), out=self.loss)
-        self.loss.div_(N)
-        logits.sub_(lse[:, None]).exp_()
-        logits.scatter_add_(1, y[:, None], torch.full((N, 1), -1.0, device=dev))
-        logits.div_(N)
+        row_loss = torch.empty(N, dtype=torch.float32, device=dev)
+        abi.echo_xent_fwd_bwd(N, V, logits, self.P["out.b"], self.labels, row_loss, None)   # in place -> dlogits
+        torch.div(row_loss.sum(), N, out=self.loss)
         reg = {"x": self.x, "h0": self.zero_h, "c0": self.zero_c, "ce_probs": logits}
         for l, pair in enumerate(layers):
             for d, L in zip(("fw", "bw"), pair):
@@ -157,7 +152,7 @@ class DS2Model(probe.GraphStep):
         self.gflat.zero_()
         dlog = a["dlogits"]
         dlog_s = dlog if sd == torch.float32 else dlog.to(sd)
-        G["out.b"].copy_(dlog.sum(0))
+        G["out.b"].copy_(_colsum(dlog))
         Wo = self.S["out.W"]
         dH = [mm(dlog_s, Wo[:, :H], torch.float32).view(T, B, H), mm(dlog_s, Wo[:, H:], torch.float32).view(T, B, H)]
         layers = a["layers"]

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import abi, probe
-from .gemm import mm, addmm_, tf32
+from .gemm import mm, addmm_, tf32, colsum as _colsum
 from .lstm import LSTMLayer, TORCH_DTYPE
 from synth.data import nmt_param_shapes
 
@@ -234,14 +234,12 @@ class NMTModel(probe.GraphStep):
         # output layer + CE; logits are overwritten in place by dlogits (the CE's fp32 feature map)
         N = B * Td
         logits = mm(Aall.view(N, H), self.w("out.Wo").t(), torch.float32)
-        logits.add_(self.P["out.bo"])
         y = inp["tgt_out"].t().reshape(-1)
-        lse = torch.logsumexp(logits, dim=1)
-        torch.sub(lse.sum(), logits.gather(1, y[:, None]).sum(), out=self.loss)
-        self.loss.div_(N)
-        logits.sub_(lse[:, None]).exp_()
-        logits.scatter_add_(1, y[:, None], torch.full((N, 1), -1.0, device=dev))
-        logits.div_(N)
+        row_loss = torch.empty(N, dtype=torch.float32, device=dev)
+        # fused bias + softmax-CE: logits become dLoss/dlogits in place (the kept fp32 feature map;
+        # the storage-dtype copy for the backward GEMMs is made in the backward, not kept)
+        abi.echo_xent_fwd_bwd(N, V, logits, self.P["out.bo"], y, row_loss, None)
+        torch.div(row_loss.sum(), N, out=self.loss)
         a["dlogits"] = logits
         self.stash = self._stash_registry(a)
         return a
@@ -297,7 +295,7 @@ class NMTModel(probe.GraphStep):
         # output layer (Eq. 2: needs its input a_t and W_o, not its output)
         dlog_s = self._to_s(a["dlogits"])
         gi(G["out.Wo"], dlog_s.t(), Aall.view(N, H))
-        torch.sum(a["dlogits"], dim=0, out=G["out.bo"])
+        G["out.bo"].copy_(_colsum(a["dlogits"]))
         dAout = mm(dlog_s, self.w("out.Wo"), torch.float32).view(Td, B, H)    # dLoss/da_t (+ carry added below)
         del dlog_s
         a["dlogits"] = None
@@ -371,7 +369,7 @@ class NMTModel(probe.GraphStep):
         for l in range(Ld):
             L = dec[l]
             dAl = L.gates.view(N, 4 * H)
-            G[f"dec{l}.b"].copy_(dAl.float().sum(0))
+            G[f"dec{l}.b"].copy_(_colsum(dAl))
             hg = L.h_for_grad()
             if Td > 1:
                 gi(G[f"dec{l}.Wh"], L.gates[1:].reshape((Td - 1) * B, 4 * H).t(), hg[: Td - 1].reshape((Td - 1) * B, H))
@@ -394,7 +392,7 @@ class NMTModel(probe.GraphStep):
         a["dec"] = None
         # attention key projection Kp = Hs W_k^T + b_q --------------------------------------
         dKpf = dKp.view(Ts * B, A)
-        torch.sum(dKpf, dim=0, out=G["att.bq"])
+        G["att.bq"].copy_(_colsum(dKpf))
         Hs32 = Hs.reshape(Ts * B, H)
         with tf32(lowp):
             gi(G["att.Wk"], dKpf.t(), Hs32 if Hs32.dtype == torch.float32 else Hs32.float())
@@ -445,7 +443,7 @@ class NMTModel(probe.GraphStep):
             L = enc[l]
             dAl = L.gates.view(n, 4 * H)
             hg = L.h_for_grad()
-            G[f"enc{l}.b"].copy_(dAl.float().sum(0))
+            G[f"enc{l}.b"].copy_(_colsum(dAl))
             if Ts > 1:
                 gi(G[f"enc{l}.Wh"], L.gates[1:].reshape((Ts - 1) * B, 4 * H).t(), hg[: Ts - 1].reshape((Ts - 1) * B, H))
             if l < Le - 1:
