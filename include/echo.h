@@ -211,6 +211,14 @@ echo_status echo_xent_fwd_bwd(int32_t N, int32_t V, float* logits, const float* 
                               const int64_t* labels, float* row_loss, void* dlogits_bf16,
                               void* stream);
 
+/* Column sums out[c] (+)= sum_r x[r*ld + c] of a [rows, cols] fp32 / bf16 matrix, accumulated in
+ * fp64 in a fixed order and rounded once to fp32: the bias gradients (Eq. 2, PAPER.md:389-391,
+ * db = sum over every row of the batch of dY), which are cancellation-dominated sums of 10^4-10^5
+ * terms (reading R14).  dtype: ECHO_FP32 / ECHO_BF16 (an echo_dtype); accumulate: 0 overwrite,
+ * 1 add.  Deterministic.  Errors: ECHO_ERR_INVALID.                                         */
+echo_status echo_colsum(int32_t rows, int32_t cols, int64_t ld, int32_t dtype, const void* x, float* out,
+                        int32_t accumulate, void* stream);
+
 /* ===================================================================== footprint estimator
  * Host-only, integer, deterministic.  Runs the adjusted pass pipeline of
  * Fig. 14: Gradient -> InferShape&Type -> EdgeUseRef ->

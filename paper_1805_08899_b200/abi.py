@@ -20,7 +20,8 @@ STASH, RECOMPUTE = 0, 1
 
 EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_cscan", "echo_lstm_bwd",
             "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
-            "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_footprint_estimate")
+            "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum",
+            "echo_footprint_estimate")
 
 
 class EchoError(RuntimeError):
@@ -74,6 +75,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_dot_softmax_fwd": [ctypes.POINTER(DotDesc)] + [vp] * 5,
         "echo_dot_softmax_bwd": [ctypes.POINTER(DotDesc)] + [vp] * 7,
         "echo_xent_fwd_bwd": [i32, i32, vp, vp, vp, vp, vp, vp],
+        "echo_colsum": [i32, i32, ctypes.c_int64, i32, vp, vp, i32, vp],
         "echo_footprint_estimate": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)],
     }
     for name, args in sigs.items():
@@ -158,6 +160,15 @@ def echo_xent_fwd_bwd(N, V, logits, bias, labels, row_loss, dlogits_bf16=None, s
     LAUNCHES["count"] += 1
     _check(load().echo_xent_fwd_bwd(N, V, _p(logits), _p(bias), _p(labels), _p(row_loss), _p(dlogits_bf16),
                                     _stream(stream)))
+
+
+def echo_colsum(x, out, accumulate=0, stream=None):
+    """out (fp32 [cols]) (+)= column sums of the 2-D fp32 / bf16 tensor x (unit column stride)."""
+    import torch
+    assert x.dim() == 2 and x.stride(1) == 1 and out.dtype == torch.float32
+    LAUNCHES["count"] += 1
+    dt = FP32 if x.dtype == torch.float32 else BF16
+    _check(load().echo_colsum(x.shape[0], x.shape[1], x.stride(0), dt, _p(x), _p(out), accumulate, _stream(stream)))
 
 
 def echo_dot_softmax_bwd(d, S, P_st, mask, dPd, dS, Pd_regen, stream=None):

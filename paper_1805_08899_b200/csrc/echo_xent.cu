@@ -1,4 +1,5 @@
-// echo_xent.cu — fused output-layer softmax cross-entropy (forward loss + dLoss/dlogits).
+// echo_xent.cu — fused output-layer softmax cross-entropy (forward loss + dLoss/dlogits) and
+// the fp64-accumulated column sums used for bias gradients.
 //
 // Not an Echo feature map decision (the CE probabilities are kept in both modes);
 // it is the model's output layer (§2, reading R10: mean CE over the B*Td
@@ -93,9 +94,57 @@ __global__ void __launch_bounds__(XENT_THREADS) xent_kernel(int N, int V, const 
   }
 }
 
+// Column sums of a [rows, cols] fp32 / bf16 matrix (row stride ld) accumulated in fp64, rounded
+// once to fp32.  Block = 32 columns x 32 row phases; phase p sums rows p, p+32, ... in order and
+// the 32 phase partials are combined in rank order: deterministic, no atomics, no workspace.
+template <typename T>
+__global__ void __launch_bounds__(1024) colsum_kernel(int rows, int cols, long ld, const T* __restrict__ x,
+                                                      float* __restrict__ out, int accumulate) {
+  pdl_wait();
+  __shared__ double part[32][33];
+  const int c = blockIdx.x * 32 + threadIdx.x, p = threadIdx.y;
+  double acc = 0.0;
+  if (c < cols) {
+    int r = p;
+    for (; r + 96 < rows; r += 128) {                           // 4 independent loads in flight
+      const float a0 = to_f(x[(long)r * ld + c]), a1 = to_f(x[(long)(r + 32) * ld + c]);
+      const float a2 = to_f(x[(long)(r + 64) * ld + c]), a3 = to_f(x[(long)(r + 96) * ld + c]);
+      acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, (double)a0), (double)a1), (double)a2), (double)a3);
+    }
+    for (; r < rows; r += 32) acc = __dadd_rn(acc, (double)to_f(x[(long)r * ld + c]));
+  }
+  part[p][threadIdx.x] = acc;
+  __syncthreads();
+  if (p == 0 && c < cols) {
+    double t = 0.0;
+    for (int k = 0; k < 32; ++k) t = __dadd_rn(t, part[k][threadIdx.x]);
+    const float v = (float)t;
+    out[c] = accumulate ? __fadd_rn(out[c], v) : v;
+  }
+}
+
 }  // namespace echo
 
 using namespace echo;
+
+extern "C" echo_status echo_colsum(int32_t rows, int32_t cols, int64_t ld, int32_t dtype, const void* x, float* out,
+                                   int32_t accumulate, void* stream) {
+  const char* fn = "echo_colsum";
+  if (rows <= 0 || cols <= 0 || ld < cols) return fail(ECHO_ERR_INVALID, "%s: rows=%d cols=%d ld=%lld", fn, rows, cols,
+                                                      (long long)ld);
+  if (!x || !out) return fail(ECHO_ERR_INVALID, "%s: NULL x / out", fn);
+  if (dtype != ECHO_FP32 && dtype != ECHO_BF16) return fail(ECHO_ERR_INVALID, "%s: bad dtype %d", fn, dtype);
+  const dim3 grid((cols + 31) / 32), block(32, 32);
+  cudaError_t e;
+  if (dtype == ECHO_FP32)
+    e = launch(colsum_kernel<float>, grid, block, 0, (cudaStream_t)stream, 1, rows, cols, (long)ld, (const float*)x,
+               out, accumulate);
+  else
+    e = launch(colsum_kernel<__nv_bfloat16>, grid, block, 0, (cudaStream_t)stream, 1, rows, cols, (long)ld,
+               (const __nv_bfloat16*)x, out, accumulate);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
+}
 
 extern "C" echo_status echo_xent_fwd_bwd(int32_t N, int32_t V, float* logits, const float* bias,
                                          const int64_t* labels, float* row_loss, void* dlogits_bf16,

@@ -45,9 +45,13 @@ def tf32(enabled: bool):
         torch.backends.cuda.matmul.allow_tf32 = prev
 
 
+
 def colsum(x):
     """Column sums of a [rows, n] gradient (bias gradients: a sum over every token / row of the
-    batch) accumulated in fp64 and rounded once to fp32.  These are cancellation-dominated sums of
-    10^4-10^5 terms; an fp32 tree sum contributes ~log2(rows) eps sum|x| of error, which at C2
-    reaches the 1e-4 bound on d/db_q alone (reading R14)."""
-    return x.sum(dim=0, dtype=torch.float64).to(torch.float32)
+    batch) with fp64 accumulation in libecho (echo_colsum), rounded once to fp32.  These are
+    cancellation-dominated sums of 10^4-10^5 terms; an fp32 tree sum contributes ~log2(rows) eps
+    sum|x| of error, which at C2 reaches the 1e-4 bound on d/db_q alone (reading R14)."""
+    from . import abi
+    out = torch.empty(x.shape[1], dtype=torch.float32, device=x.device)
+    abi.echo_colsum(x, out)
+    return out

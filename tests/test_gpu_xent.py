@@ -44,3 +44,27 @@ def test_xent_matches_reference(N, V, bias, copy, cuda_dev):
     rl2 = torch.empty(N, device="cuda")
     abi.echo_xent_fwd_bwd(N, V, lg2, bb, yy, rl2, None)
     assert torch.equal(lg, lg2) and torch.equal(rl, rl2)
+
+
+@pytest.mark.parametrize("rows,cols,dtype", [(6400, 512, "fp32"), (33, 29, "fp32"), (1000, 2048, "bf16"),
+                                             (1, 7, "fp32")])
+def test_colsum_fp64_accumulation(rows, cols, dtype, cuda_dev):
+    """echo_colsum equals the fp64 column sum rounded once to fp32 (within 1 ulp), including a
+    cancellation-heavy case where an fp32 sum is visibly off."""
+    from paper_1805_08899_b200 import abi
+    rng = np.random.default_rng(rows + cols)
+    x = rng.standard_normal((rows, cols)).astype(np.float32) * 1e3
+    x[-1] = -x[:-1].astype(np.float64).sum(axis=0) + rng.standard_normal(cols)   # sums ~ N(0,1): cancellation
+    t = torch.from_numpy(x).cuda()
+    if dtype == "bf16":
+        t = t.to(torch.bfloat16)
+        x = t.float().cpu().numpy()
+    ref = x.astype(np.float64).sum(axis=0).astype(np.float32)
+    out = torch.empty(cols, device="cuda")
+    abi.echo_colsum(t, out)
+    got = out.cpu().numpy()
+    ulp = np.spacing(np.abs(ref))
+    assert np.all(np.abs(got - ref) <= ulp), np.max(np.abs(got - ref) / ulp)
+    out2 = torch.ones(cols, device="cuda")
+    abi.echo_colsum(t, out2, accumulate=1)
+    assert torch.allclose(out2, out + 1.0)
