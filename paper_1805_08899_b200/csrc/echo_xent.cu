@@ -11,10 +11,12 @@
 // (fp32, the CE feature map) and optionally also written in bf16 for the backward GEMMs.
 #include "echo_common.cuh"
 
+#include <cooperative_groups.h>
 #include <math.h>
 
 namespace echo {
 
+namespace cg = cooperative_groups;
 constexpr int XENT_THREADS = 256;
 
 __device__ __forceinline__ float block_reduce(float v, float* red, bool is_max) {
@@ -95,37 +97,69 @@ __global__ void __launch_bounds__(XENT_THREADS) xent_kernel(int N, int V, const 
 }
 
 // Column sums of a [rows, cols] fp32 / bf16 matrix (row stride ld) accumulated in fp64, rounded
-// once to fp32.  Block = 32 columns x 32 row phases; phase p sums rows p, p+32, ... in order and
-// the 32 phase partials are combined in rank order: deterministic, no atomics, no workspace.
+// once to fp32.  A cluster of COLSUM_SEGS CTAs shares one 32-column strip: CTA k takes the k-th
+// row segment; inside a CTA, 32 row phases (threadIdx.y) sum their rows in order and are combined
+// in rank order; CTA 0 then adds the segments' partials from distributed shared memory in rank
+// order.  Deterministic, no atomics, no workspace.
+constexpr int COLSUM_SEGS = 8;
 template <typename T>
 __global__ void __launch_bounds__(1024) colsum_kernel(int rows, int cols, long ld, const T* __restrict__ x,
                                                       float* __restrict__ out, int accumulate) {
   pdl_wait();
+  cg::cluster_group cl = cg::this_cluster();
   __shared__ double part[32][33];
+  __shared__ double seg[32];
   const int c = blockIdx.x * 32 + threadIdx.x, p = threadIdx.y;
+  const int k = (int)cl.block_rank();
+  const int per = (rows + COLSUM_SEGS - 1) / COLSUM_SEGS;
+  const int r0 = k * per, r1 = min(rows, r0 + per);
   double acc = 0.0;
   if (c < cols) {
-    int r = p;
-    for (; r + 96 < rows; r += 128) {                           // 4 independent loads in flight
+    int r = r0 + p;
+    for (; r + 96 < r1; r += 128) {                             // 4 independent loads in flight
       const float a0 = to_f(x[(long)r * ld + c]), a1 = to_f(x[(long)(r + 32) * ld + c]);
       const float a2 = to_f(x[(long)(r + 64) * ld + c]), a3 = to_f(x[(long)(r + 96) * ld + c]);
       acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, (double)a0), (double)a1), (double)a2), (double)a3);
     }
-    for (; r < rows; r += 32) acc = __dadd_rn(acc, (double)to_f(x[(long)r * ld + c]));
+    for (; r < r1; r += 32) acc = __dadd_rn(acc, (double)to_f(x[(long)r * ld + c]));
   }
   part[p][threadIdx.x] = acc;
   __syncthreads();
-  if (p == 0 && c < cols) {
+  if (p == 0) {
     double t = 0.0;
-    for (int k = 0; k < 32; ++k) t = __dadd_rn(t, part[k][threadIdx.x]);
+    for (int q = 0; q < 32; ++q) t = __dadd_rn(t, part[q][threadIdx.x]);
+    seg[threadIdx.x] = t;
+  }
+  cl.sync();
+  if (k == 0 && p == 0 && c < cols) {
+    double t = 0.0;
+    for (int q = 0; q < COLSUM_SEGS; ++q) t = __dadd_rn(t, cl.map_shared_rank(seg, q)[threadIdx.x]);
     const float v = (float)t;
     out[c] = accumulate ? __fadd_rn(out[c], v) : v;
   }
+  cl.sync();                                                     // keep seg[] alive for the remote reads
 }
 
 }  // namespace echo
 
 using namespace echo;
+
+// cluster of COLSUM_SEGS CTAs along grid y
+template <typename Kern, typename... Args>
+static cudaError_t launch_cluster_y(Kern kern, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = COLSUM_SEGS;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 extern "C" echo_status echo_colsum(int32_t rows, int32_t cols, int64_t ld, int32_t dtype, const void* x, float* out,
                                    int32_t accumulate, void* stream) {
@@ -134,14 +168,14 @@ extern "C" echo_status echo_colsum(int32_t rows, int32_t cols, int64_t ld, int32
                                                       (long long)ld);
   if (!x || !out) return fail(ECHO_ERR_INVALID, "%s: NULL x / out", fn);
   if (dtype != ECHO_FP32 && dtype != ECHO_BF16) return fail(ECHO_ERR_INVALID, "%s: bad dtype %d", fn, dtype);
-  const dim3 grid((cols + 31) / 32), block(32, 32);
+  const dim3 grid((cols + 31) / 32, COLSUM_SEGS), block(32, 32);
   cudaError_t e;
   if (dtype == ECHO_FP32)
-    e = launch(colsum_kernel<float>, grid, block, 0, (cudaStream_t)stream, 1, rows, cols, (long)ld, (const float*)x,
-               out, accumulate);
+    e = launch_cluster_y(colsum_kernel<float>, grid, block, (cudaStream_t)stream, rows, cols, (long)ld,
+                         (const float*)x, out, accumulate);
   else
-    e = launch(colsum_kernel<__nv_bfloat16>, grid, block, 0, (cudaStream_t)stream, 1, rows, cols, (long)ld,
-               (const __nv_bfloat16*)x, out, accumulate);
+    e = launch_cluster_y(colsum_kernel<__nv_bfloat16>, grid, block, (cudaStream_t)stream, rows, cols, (long)ld,
+                         (const __nv_bfloat16*)x, out, accumulate);
   if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);
 }
