@@ -58,3 +58,33 @@ def test_ds2_stash_bytes_equal_estimator(cfg, storage, cuda_dev):
         acts = m._forward()
         assert m.stash_bytes() == rep["stash_bytes"], (strat, m.stash_bytes(), rep["stash_bytes"])
         del acts
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+def test_ds2_c3_full_bitwise_and_graph(storage, cuda_dev):
+    """Full C3 (5 bidirectional layers, T=400, B=32, H=800) in the bench launch configuration:
+    STASH == RECOMPUTE bitwise (loss and every gradient), and the CUDA-graph replay (the two
+    directions as parallel branches) == the eager step bitwise."""
+    from paper_1805_08899_b200 import abi
+    from paper_1805_08899_b200.ds2 import DS2Model
+    params = ds2_params(7, C3, storage)
+    batch = ds2_batch(8, C3, storage)
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    res = {}
+    for mode in (abi.STASH, abi.RECOMPUTE):
+        m = DS2Model(C3, dt, mode)
+        m.load_params(params)
+        m.upload_batch(batch)
+        m.step(0.0)
+        res[mode] = (m.gflat.clone(), m.loss.clone())
+        if mode == abi.RECOMPUTE:
+            m.capture(0.0)
+            m.gflat.zero_()
+            m.replay()
+            torch.cuda.synchronize()
+            assert bits_equal(m.gflat, res[mode][0])
+        del m
+        torch.cuda.empty_cache()
+    assert bits_equal(res[abi.STASH][0], res[abi.RECOMPUTE][0])
+    assert bits_equal(res[abi.STASH][1], res[abi.RECOMPUTE][1])
+    assert torch.isfinite(res[abi.STASH][0]).all()

@@ -64,3 +64,27 @@ def test_tx_stash_bytes_equal_estimator(cfg, storage, cuda_dev):
         acts = m._forward()
         assert m.stash_bytes() == rep["stash_bytes"], (strat, m.stash_bytes(), rep["stash_bytes"])
         del acts
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+def test_tx_c4_full_bitwise_and_graph(storage, cuda_dev):
+    """Full C4 (6 blocks, B=64, L=256, d=512, 8 heads, dropout 0.1): STASH == RECOMPUTE bitwise and
+    graph replay == eager bitwise."""
+    from paper_1805_08899_b200 import abi
+    params = tx_params(3, C4, storage)
+    batch = tx_batch(4, C4, storage)
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    res = {}
+    for mode in (abi.STASH, abi.RECOMPUTE):
+        m, loss = _run(C4, params, batch, dt, mode)
+        res[mode] = (m.gflat.clone(), m.loss.clone())
+        if mode == abi.RECOMPUTE:
+            m.capture(0.0)
+            m.gflat.zero_()
+            m.replay()
+            torch.cuda.synchronize()
+            assert bits_equal(m.gflat, res[mode][0])
+        del m
+        torch.cuda.empty_cache()
+    assert bits_equal(res[abi.STASH][0], res[abi.RECOMPUTE][0])
+    assert bits_equal(res[abi.STASH][1], res[abi.RECOMPUTE][1])
