@@ -101,6 +101,31 @@ echo_status echo_lstm_fwd(const echo_lstm_desc* d, const void* gx_t, const void*
 echo_status echo_lstm_cscan(const echo_lstm_desc* d, int32_t T, const void* gates,
                             const float* c0, float* c_ws, void* h_ws, void* stream);
 
+/* a1 fused over the recurrence (Echo-dagger fusion): steps
+ * k0..k1-1 of one layer (direction) in ONE cooperative launch.  Per step:
+ *   gates_k = a1( round_s(gx[t] + h_{k-1} W_h^T) + bias, c_{k-1} ),  t = reverse ? T-1-k : k,
+ * i.e. the per-step path (cuBLAS GEMM into gx with beta = 1, then echo_lstm_fwd) with the recurrent
+ * product computed inside the kernel (fp32 accumulation, fixed k order) and a grid barrier between
+ * steps.  Same rounding points and the same pointwise device functions as a1; results differ from
+ * the per-step path only by the GEMM's accumulation order, and are identical for STASH / RECOMPUTE.
+ *  T        steps of the layer;  [k0, k1) the processing steps this launch runs (0 <= k0 < k1 <= T)
+ *  gx       [T,B,4H] s  x_t W_x^T by TIME t (no bias); may alias gates when !reverse
+ *  Wh       [4H,H] s    recurrent weights (row-major, gate blocks i|f|g|o)
+ *  bias     [4H] fp32;  h0 [B,H] s, c0 [B,H] fp32 (state before processing step 0)
+ *  gates    [T,B,4H] s  OUT activated gates by processing step k (a1's gates_t)
+ *  c        fp32 OUT: STASH / c_ring == 0: [T,B,H] c_k by step; c_ring != 0: [2,B,H] ring (slot k%2).
+ *           For k0 > 0 the state c_{k0-1} is read from the same buffer.
+ *  tc       [T,B,H] s OUT tanh(c_k) (STASH) or NULL (RECOMPUTE)
+ *  h        [T,B,H] s OUT h by TIME t (read back as h_{k-1} by later steps)
+ * Errors: ECHO_ERR_INVALID; ECHO_ERR_UNSUPPORTED when no co-resident tile exists for (B, H) — the
+ * caller then uses the per-step path (echo_lstm_seq_supported() asks first).                  */
+echo_status echo_lstm_seq_fwd(const echo_lstm_desc* d, int32_t T, int32_t k0, int32_t k1, int32_t reverse,
+                              const void* gx, const void* Wh, const float* bias, const void* h0,
+                              const float* c0, void* gates, float* c, int32_t c_ring, void* tc, void* h,
+                              void* stream);
+/* 1 if echo_lstm_seq_fwd has a co-resident tile for this (B, H, dtype) on the current device. */
+int32_t echo_lstm_seq_supported(int32_t B, int32_t H, int32_t dtype);
+
 /* a3 — backward step with fused recomputation (Echo-dagger fusion).
  *  gates_t [B,4H] s    stashed i|f|g|o
  *  c_prev  [B,H] fp32  c_{t-1} (c_0, the STASH c buffer, or the a2 workspace)

@@ -20,7 +20,8 @@ STASH, RECOMPUTE = 0, 1
 
 EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_cscan", "echo_lstm_bwd",
             "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
-            "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum",
+            "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum", "echo_lstm_seq_fwd",
+            "echo_lstm_seq_supported",
             "echo_footprint_estimate")
 
 
@@ -75,6 +76,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_dot_softmax_fwd": [ctypes.POINTER(DotDesc)] + [vp] * 5,
         "echo_dot_softmax_bwd": [ctypes.POINTER(DotDesc)] + [vp] * 7,
         "echo_xent_fwd_bwd": [i32, i32, vp, vp, vp, vp, vp, vp],
+        "echo_lstm_seq_fwd": [ctypes.POINTER(LstmDesc), i32, i32, i32, i32] + [vp] * 7 + [i32, vp, vp, vp],
         "echo_colsum": [i32, i32, ctypes.c_int64, i32, vp, vp, i32, vp],
         "echo_footprint_estimate": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)],
     }
@@ -154,6 +156,19 @@ def echo_attn_dv_reduce(B, A, dv_part, dv, accumulate, stream=None):
 def echo_dot_softmax_fwd(d, S, Pd, P_st, mask, stream=None):
     LAUNCHES["count"] += 1
     _check(load().echo_dot_softmax_fwd(ctypes.byref(d), _p(S), _p(Pd), _p(P_st), _p(mask), _stream(stream)))
+
+
+def echo_lstm_seq_supported(B, H, dtype):
+    lib = load()
+    lib.echo_lstm_seq_supported.restype = ctypes.c_int32
+    lib.echo_lstm_seq_supported.argtypes = [ctypes.c_int32] * 3
+    return bool(lib.echo_lstm_seq_supported(B, H, dtype))
+
+
+def echo_lstm_seq_fwd(d, T, k0, k1, reverse, gx, Wh, bias, h0, c0, gates, c, c_ring, tc, h, stream=None):
+    LAUNCHES["count"] += 1
+    _check(load().echo_lstm_seq_fwd(ctypes.byref(d), T, k0, k1, int(reverse), _p(gx), _p(Wh), _p(bias), _p(h0), _p(c0),
+                                    _p(gates), _p(c), int(c_ring), _p(tc), _p(h), _stream(stream)))
 
 
 def echo_xent_fwd_bwd(N, V, logits, bias, labels, row_loss, dlogits_bf16=None, stream=None):

@@ -112,6 +112,20 @@ __device__ __forceinline__ void ld16_stream(const __nv_bfloat16* p, float (&o)[8
     o[2 * i] = f.x; o[2 * i + 1] = f.y;
   }
 }
+// L2-coherent variant (ld.global.cg: skips L1), for data another CTA wrote in this launch
+__device__ __forceinline__ void ld16_cg(const float* p, float (&o)[4]) {
+  float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void ld16_cg(const __nv_bfloat16* p, float (&o)[8]) {
+  uint4 v = __ldcg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x; o[2 * i + 1] = f.y;
+  }
+}
 // store VEC floats (already rounded to T) as storage T
 __device__ __forceinline__ void st16(float* p, const float (&v)[4]) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);

@@ -11,7 +11,11 @@
 // registers across t and keeps U time steps of loads in flight.
 #include "echo_common.cuh"
 
+#include <cooperative_groups.h>
+
 namespace echo {
+
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------- shared device functions
 // The ONE definition of the cell-state update used by a1 (forward) and a2
@@ -197,6 +201,196 @@ __global__ void __launch_bounds__(128) lstm_bwd_kernel(int B, int H, const T* ga
   }
 }
 
+// ---------------------------------------------------------------- a1 fused over the recurrence
+// One cooperative (persistent) launch runs steps k0..k1-1 of a layer: per step each CTA computes
+// the recurrent product h_{k-1} W_h^T for its tile (RB batch rows x 4*UPC gate columns = the four
+// gates of UPC hidden units) in fp32 FFMA from shared memory, adds the precomputed x_t W_x^T and
+// the bias with the same rounding points as the per-step path (round_s(gx + h W_h^T), then + b),
+// applies the a1 pointwise functions (cell_update / tanh_c / hidden: bit-identical device code),
+// carries c in registers and publishes h_t; a grid barrier separates the steps (every tile reads
+// all of h_{k-1}).  Replaces 2 launches + 1 cuBLAS GEMM per step (latency-bound at C2).
+constexpr int SEQ_THREADS = 256;
+#ifdef ECHO_PHASE_TIMING
+__device__ unsigned long long g_seq_phase[5][1024];   // per CTA: stage, gemm, epilogue, sync cycles; steps
+#define SEQ_T(v) long long v = clock64()
+#define SEQ_ACC(i, a, b) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_seq_phase[i][blockIdx.x] += (b) - (a); } while (0)
+#else
+#define SEQ_T(v) do { } while (0)
+#define SEQ_ACC(i, a, b) do { } while (0)
+#endif
+
+struct SeqGeom {
+  int RB, UPC, NB, CPT, hsp;      // rows / units per CTA, CTAs, gate columns per thread, h row stride
+  size_t smem;
+};
+
+static __host__ __device__ __forceinline__ SeqGeom seq_geom(int B, int H, int RB, int UPC) {
+  SeqGeom g;
+  g.RB = RB;
+  g.UPC = UPC;
+  g.NB = (B / RB) * (H / UPC);
+  g.CPT = 4 * UPC * RB / SEQ_THREADS;
+  g.hsp = H + 4;
+  g.smem = sizeof(float) * ((size_t)RB * g.hsp + (size_t)H * 4 * UPC + (size_t)RB * 4 * UPC);
+  return g;
+}
+
+template <typename T, int CPT>
+__global__ void __launch_bounds__(SEQ_THREADS, 1) lstm_seq_fwd_kernel(int k0, int k1, int T_, int B, int H, int RB,
+                                                                      int UPC, int reverse, const T* gx,
+                                                                      const T* __restrict__ Wh,
+                                                                      const float* __restrict__ bias,
+                                                                      const T* __restrict__ h0,
+                                                                      const float* __restrict__ c0, T* gates,
+                                                                      float* __restrict__ c_out, int c_ring,
+                                                                      T* __restrict__ tc_out, T* __restrict__ h_out) {
+  pdl_wait();
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) float sm[];
+  const int hsp = H + 4, WC = 4 * UPC;
+  float* hs = sm;                                   // [RB][hsp]   h_{k-1} rows of this tile (fp32)
+  float* Ws = hs + (size_t)RB * hsp;                // [H][WC]     W_h rows of this tile's gate columns, k-major
+  float* Gs = Ws + (size_t)H * WC;                  // [RB][WC]    recurrent products
+  const int tid = threadIdx.x;
+  const int nub = H / UPC;
+  const int r0 = (blockIdx.x / nub) * RB, j0 = (blockIdx.x % nub) * UPC;
+  // W_h slice, once: column q = g * UPC + u  <->  W_h row g * H + j0 + u
+  for (int i = tid; i < WC * H; i += SEQ_THREADS) {
+    const int q = i / H, k = i - q * H;
+    const int g = q / UPC, u = q - g * UPC;
+    Ws[(size_t)k * WC + q] = to_f(Wh[(size_t)(g * H + j0 + u) * H + k]);
+  }
+  // pointwise ownership: (row, unit) pairs e = tid + m * SEQ_THREADS; c carried in registers
+  constexpr int MAXP = 4;
+  const int npair = RB * UPC;
+  float creg[MAXP];
+#pragma unroll
+  for (int m = 0; m < MAXP; ++m) {
+    const int e = tid + m * SEQ_THREADS;
+    if (e < npair) {
+      const int r = e / UPC, u = e - r * UPC;
+      creg[m] = (k0 == 0) ? c0[(size_t)(r0 + r) * H + j0 + u]
+                          : c_out[(size_t)(c_ring ? (k0 - 1) % 2 : k0 - 1) * B * H + (size_t)(r0 + r) * H + j0 + u];
+    }
+  }
+  const int gr = tid % RB, cgp = tid / RB;          // GEMM: row gr, gate columns cgp*CPT .. +CPT
+  const size_t BH = (size_t)B * H, B4H = (size_t)B * 4 * H;
+  for (int k = k0; k < k1; ++k) {
+    const int t = reverse ? T_ - 1 - k : k;
+    SEQ_T(p0);
+    const T* hp = (k == 0) ? h0 : h_out + (size_t)(reverse ? T_ - k : k - 1) * BH;
+    // stage h_{k-1}[r0 .. r0+RB) as fp32 (L2-coherent loads: other CTAs wrote it last step)
+    constexpr int V = St<T>::VEC;
+    for (int i = tid; i < RB * (H / V); i += SEQ_THREADS) {
+      const int r = i / (H / V), c = (i - r * (H / V)) * V;
+      float v[V];
+      ld16_cg(hp + (size_t)(r0 + r) * H + c, v);
+#pragma unroll
+      for (int q = 0; q < V; q += 4)
+        *reinterpret_cast<float4*>(hs + (size_t)r * hsp + c + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+    }
+    __syncthreads();
+    SEQ_T(p1);
+    float acc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[c] = 0.0f;
+    const float* hrow = hs + (size_t)gr * hsp;
+    const float* wcol = Ws + cgp * CPT;
+    for (int kk = 0; kk < H; kk += 4) {
+      const float4 hv = *reinterpret_cast<const float4*>(hrow + kk);
+      const float hx[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* wr = wcol + (size_t)(kk + q) * WC;
+#pragma unroll
+        for (int c = 0; c < CPT; c += 4) {
+          const float4 w = *reinterpret_cast<const float4*>(wr + c);
+          acc[c] = __fmaf_rn(hx[q], w.x, acc[c]);
+          acc[c + 1] = __fmaf_rn(hx[q], w.y, acc[c + 1]);
+          acc[c + 2] = __fmaf_rn(hx[q], w.z, acc[c + 2]);
+          acc[c + 3] = __fmaf_rn(hx[q], w.w, acc[c + 3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) Gs[(size_t)gr * WC + cgp * CPT + c] = acc[c];
+    __syncthreads();
+    SEQ_T(p2);
+    const T* gxt = gx + (size_t)t * B4H;
+    T* gk = gates + (size_t)k * B4H;
+#pragma unroll
+    for (int m = 0; m < MAXP; ++m) {
+      const int e = tid + m * SEQ_THREADS;
+      if (e < npair) {
+        const int r = e / UPC, u = e - r * UPC;
+        const size_t row4 = (size_t)(r0 + r) * 4 * H, row = (size_t)(r0 + r) * H + j0 + u;
+        float a[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          // same rounding points as the per-step path: round_s(gx + h W_h^T) (cuBLAS beta = 1 into
+          // storage dtype), then + b in fp32
+          const float pre = St<T>::round(__fadd_rn(to_f(gxt[row4 + g * H + j0 + u]), Gs[(size_t)r * WC + g * UPC + u]));
+          a[g] = __fadd_rn(pre, bias[g * H + j0 + u]);
+        }
+        const float gi = St<T>::round(sigmoidf_(a[0])), gf = St<T>::round(sigmoidf_(a[1]));
+        const float gg = St<T>::round(tanhf(a[2])), go = St<T>::round(sigmoidf_(a[3]));
+        const float c = cell_update(gf, creg[m], gi, gg);
+        const float tc = tanh_c<T>(c);
+        const float h = hidden<T>(go, tc);
+        creg[m] = c;
+        gk[row4 + 0 * H + j0 + u] = from_f<T>(gi);
+        gk[row4 + 1 * H + j0 + u] = from_f<T>(gf);
+        gk[row4 + 2 * H + j0 + u] = from_f<T>(gg);
+        gk[row4 + 3 * H + j0 + u] = from_f<T>(go);
+        c_out[(size_t)(c_ring ? k % 2 : k) * BH + row] = c;
+        if (tc_out) tc_out[(size_t)k * BH + row] = from_f<T>(tc);
+        h_out[(size_t)t * BH + row] = from_f<T>(h);
+      }
+    }
+    SEQ_T(p3);
+    __threadfence();
+    grid.sync();                                      // h_t complete before anyone stages it
+    SEQ_T(p4);
+    SEQ_ACC(0, p0, p1);
+    SEQ_ACC(1, p1, p2);
+    SEQ_ACC(2, p2, p3);
+    SEQ_ACC(3, p3, p4);
+    SEQ_ACC(4, 0, 1);
+  }
+}
+
+// host: pick the tile (RB rows x UPC units) and check co-residency; false = use the per-step path
+static bool seq_plan(int B, int H, int dtype, SeqGeom* out, const void** kern) {
+  int RB = B % 64 == 0 ? 64 : (B % 32 == 0 ? 32 : 0);
+  if (!RB) return false;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int UPC = 2; UPC <= 16; UPC *= 2) {
+    if (H % UPC) continue;
+    SeqGeom g = seq_geom(B, H, RB, UPC);
+    if (g.CPT != 4 && g.CPT != 8) continue;
+    if (g.smem > 220 * 1024) continue;
+    const void* k = nullptr;
+    if (dtype == ECHO_FP32) k = g.CPT == 4 ? (const void*)lstm_seq_fwd_kernel<float, 4> : (const void*)lstm_seq_fwd_kernel<float, 8>;
+    else k = g.CPT == 4 ? (const void*)lstm_seq_fwd_kernel<__nv_bfloat16, 4> : (const void*)lstm_seq_fwd_kernel<__nv_bfloat16, 8>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, SEQ_THREADS, g.smem) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (g.NB > per * sms || RB * UPC > 4 * SEQ_THREADS) continue;
+    *out = g;
+    *kern = k;
+    return true;
+  }
+  return false;
+}
+
 // ---------------------------------------------------------------- validation
 static echo_status check_desc(const echo_lstm_desc* d) {
   if (!d) return fail(ECHO_ERR_INVALID, "lstm: desc is NULL");
@@ -310,3 +504,75 @@ extern "C" echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_
   if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
   return check_launch(fn);
 }
+
+extern "C" echo_status echo_lstm_seq_fwd(const echo_lstm_desc* d, int32_t T, int32_t k0, int32_t k1, int32_t reverse,
+                                         const void* gx, const void* Wh, const float* bias, const void* h0,
+                                         const float* c0, void* gates, float* c, int32_t c_ring, void* tc, void* h,
+                                         void* stream) {
+  const char* fn = "echo_lstm_seq_fwd";
+  echo_status s = check_desc(d);
+  if (s) return s;
+  if (T <= 0 || k0 < 0 || k1 > T || k0 >= k1) return fail(ECHO_ERR_INVALID, "%s: steps [%d, %d) of T=%d", fn, k0, k1, T);
+  ECHO_REQ(gx, "gx");
+  ECHO_REQ(Wh, "Wh");
+  ECHO_REQ(bias, "bias");
+  ECHO_REQ(h0, "h0");
+  ECHO_REQ(c0, "c0");
+  ECHO_REQ(gates, "gates");
+  ECHO_REQ(c, "c");
+  ECHO_REQ(h, "h");
+  if (d->mode == ECHO_STASH) { ECHO_REQ(tc, "tc"); }
+  else if (tc) return fail(ECHO_ERR_INVALID, "%s: tc must be NULL in RECOMPUTE mode", fn);
+  if (reverse && gx == gates) return fail(ECHO_ERR_INVALID, "%s: a reverse layer's gx must not alias gates", fn);
+  SeqGeom g;
+  const void* kern = nullptr;
+  if (!seq_plan(d->B, d->H, d->dtype, &g, &kern))
+    return fail(ECHO_ERR_UNSUPPORTED, "%s: no co-resident tile for B=%d H=%d (use the per-step path)", fn, d->B, d->H);
+  int B = d->B, H = d->H, RB = g.RB, UPC = g.UPC, ring = c_ring ? 1 : 0, rev = reverse ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.NB);
+  cfg.blockDim = dim3(SEQ_THREADS);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (d->dtype == ECHO_FP32) {
+    if (g.CPT == 4)
+      e = cudaLaunchKernelEx(&cfg, lstm_seq_fwd_kernel<float, 4>, k0, k1, T, B, H, RB, UPC, rev, (const float*)gx,
+                             (const float*)Wh, bias, (const float*)h0, c0, (float*)gates, c, ring, (float*)tc, (float*)h);
+    else
+      e = cudaLaunchKernelEx(&cfg, lstm_seq_fwd_kernel<float, 8>, k0, k1, T, B, H, RB, UPC, rev, (const float*)gx,
+                             (const float*)Wh, bias, (const float*)h0, c0, (float*)gates, c, ring, (float*)tc, (float*)h);
+  } else {
+    typedef __nv_bfloat16 bf;
+    if (g.CPT == 4)
+      e = cudaLaunchKernelEx(&cfg, lstm_seq_fwd_kernel<bf, 4>, k0, k1, T, B, H, RB, UPC, rev, (const bf*)gx,
+                             (const bf*)Wh, bias, (const bf*)h0, c0, (bf*)gates, c, ring, (bf*)tc, (bf*)h);
+    else
+      e = cudaLaunchKernelEx(&cfg, lstm_seq_fwd_kernel<bf, 8>, k0, k1, T, B, H, RB, UPC, rev, (const bf*)gx,
+                             (const bf*)Wh, bias, (const bf*)h0, c0, (bf*)gates, c, ring, (bf*)tc, (bf*)h);
+  }
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
+}
+
+extern "C" int32_t echo_lstm_seq_supported(int32_t B, int32_t H, int32_t dtype) {
+  SeqGeom g;
+  const void* k = nullptr;
+  return seq_plan(B, H, dtype, &g, &k) ? 1 : 0;
+}
+
+#ifdef ECHO_PHASE_TIMING
+extern "C" int echo_debug_seq_phase(unsigned long long* host, int reset) {
+  int e = (int)cudaMemcpyFromSymbol(host, echo::g_seq_phase, sizeof(unsigned long long) * 5 * 1024);
+  if (reset) {
+    static unsigned long long zero[5 * 1024] = {0};
+    cudaMemcpyToSymbol(echo::g_seq_phase, zero, sizeof(zero));
+  }
+  return e;
+}
+#endif
