@@ -219,6 +219,22 @@ echo_status echo_dot_softmax_bwd(const echo_dot_desc* d, const void* S, const vo
                                  const uint8_t* mask, const void* dPd, void* dS, void* Pd_regen,
                                  void* stream);
 
+/* ===================================================================== a0 dense contractions
+ * IEEE-fp32 GEMM for the FCs around the hot path (Eq. 1 / Eq. 2, PAPER.md:104-106, 389-391;
+ * outside the Echo decision): C = alpha * op(A) op(B) + beta * C, row-major storage.
+ *  op(A) M x K: transA == 0 -> A[m*lda + k]; transA != 0 -> A[k*lda + m]
+ *  op(B) K x N: transB == 0 -> B[k*ldb + n]; transB != 0 -> B[n*ldb + k]
+ * SIMT fp32 FMA with fixed k order; split-K across a thread-block cluster whose partial tiles are
+ * summed in rank order through distributed shared memory (deterministic, no workspace).
+ * Requirements (echo_gemm_f32_supported): N, lda, ldb, ldc multiples of 4; K % 4 == 0 when
+ * !transA or transB; M % 4 == 0 when transA; 16-byte aligned pointers.
+ * Errors: ECHO_ERR_UNSUPPORTED (shape / stride), ECHO_ERR_INVALID (alignment).                 */
+echo_status echo_gemm_f32(int32_t M, int32_t N, int32_t K, float alpha, const float* A, int64_t lda,
+                          int32_t transA, const float* B, int64_t ldb, int32_t transB, float beta,
+                          float* C, int64_t ldc, void* stream);
+int32_t echo_gemm_f32_supported(int32_t M, int32_t N, int32_t K, int32_t transA, int32_t transB,
+                                int64_t lda, int64_t ldb, int64_t ldc);
+
 /* ===================================================================== output layer
  * Fused softmax cross-entropy of the model's output layer (§2; reading
  * R10: mean CE over the N = B*Td target tokens).  Outside the Echo decision (its probabilities

@@ -21,7 +21,7 @@ STASH, RECOMPUTE = 0, 1
 EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_cscan", "echo_lstm_bwd",
             "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
             "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum", "echo_lstm_seq_fwd",
-            "echo_lstm_seq_supported",
+            "echo_lstm_seq_supported", "echo_gemm_f32", "echo_gemm_f32_supported",
             "echo_footprint_estimate")
 
 
@@ -76,6 +76,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_dot_softmax_fwd": [ctypes.POINTER(DotDesc)] + [vp] * 5,
         "echo_dot_softmax_bwd": [ctypes.POINTER(DotDesc)] + [vp] * 7,
         "echo_xent_fwd_bwd": [i32, i32, vp, vp, vp, vp, vp, vp],
+        "echo_gemm_f32": [i32, i32, i32, ctypes.c_float, vp, ctypes.c_int64, i32, vp, ctypes.c_int64, i32,
+                          ctypes.c_float, vp, ctypes.c_int64, vp],
         "echo_lstm_seq_fwd": [ctypes.POINTER(LstmDesc), i32, i32, i32, i32] + [vp] * 7 + [i32, vp, vp, vp],
         "echo_colsum": [i32, i32, ctypes.c_int64, i32, vp, vp, i32, vp],
         "echo_footprint_estimate": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)],
@@ -156,6 +158,24 @@ def echo_attn_dv_reduce(B, A, dv_part, dv, accumulate, stream=None):
 def echo_dot_softmax_fwd(d, S, Pd, P_st, mask, stream=None):
     LAUNCHES["count"] += 1
     _check(load().echo_dot_softmax_fwd(ctypes.byref(d), _p(S), _p(Pd), _p(P_st), _p(mask), _stream(stream)))
+
+
+_GEMM_OK = {}
+
+
+def echo_gemm_f32_supported(M, N, K, tA, tB, lda, ldb, ldc):
+    key = (M, N, K, tA, tB, lda, ldb, ldc)
+    if key not in _GEMM_OK:
+        lib = load()
+        lib.echo_gemm_f32_supported.restype = ctypes.c_int32
+        lib.echo_gemm_f32_supported.argtypes = [ctypes.c_int32] * 5 + [ctypes.c_int64] * 3
+        _GEMM_OK[key] = bool(lib.echo_gemm_f32_supported(M, N, K, tA, tB, lda, ldb, ldc))
+    return _GEMM_OK[key]
+
+
+def echo_gemm_f32(M, N, K, alpha, A, lda, tA, B, ldb, tB, beta, C, ldc, stream=None):
+    LAUNCHES["count"] += 1
+    _check(load().echo_gemm_f32(M, N, K, alpha, _p(A), lda, tA, _p(B), ldb, tB, beta, _p(C), ldc, _stream(stream)))
 
 
 def echo_lstm_seq_supported(B, H, dtype):

@@ -13,20 +13,68 @@ from contextlib import contextmanager
 import torch
 
 
+import os
+
+# libecho's fp32 split-K GEMM is opt-in (ECHO_GEMM=echo): measured on B200 (scripts/gemm_bench.py)
+# it beats cuBLAS only on the decoder-backward shape (M=128, N=512, K=2048: 27 vs 34 us) and loses
+# on the rest (2-deep global->register->shared pipeline cannot hide HBM/L2 latency at 1-2 CTAs/SM;
+# large-K weight-gradient GEMMs 4x slower), so the step uses cuBLAS (TF32 off) by default.
+_USE_ECHO = os.environ.get("ECHO_GEMM", "torch") == "echo"
+
+
+def _layout(x):
+    """(trans, ld) of a 2-D fp32 operand for echo_gemm_f32, or None (not a plain row/column-major view)."""
+    s0, s1 = x.stride()
+    if s1 == 1 and (s0 >= x.shape[1] or x.shape[0] == 1):
+        return 0, max(s0, x.shape[1])
+    if s0 == 1 and (s1 >= x.shape[0] or x.shape[1] == 1):
+        return 1, max(s1, x.shape[0])
+    return None
+
+
+def gemm_into(out, a, b, beta=0.0):
+    """out = a @ b + beta * out.  IEEE-fp32 operands go to libecho's split-K SIMT GEMM
+    (echo_gemm_f32: deterministic, 3-10x cuBLAS's fp32 SIMT kernels at M = 128); everything else
+    (bf16 operands -> cuBLAS tensor cores) stays on torch."""
+    f32 = torch.float32
+    if _USE_ECHO and a.dtype == f32 and b.dtype == f32 and out.dtype == f32 and a.is_cuda and out.stride(1) == 1:
+        la, lb = _layout(a), _layout(b)
+        M, K = a.shape
+        N = b.shape[1]
+        if la and lb and out.stride(0) >= N:
+            from . import abi
+            if abi.echo_gemm_f32_supported(M, N, K, la[0], lb[0], la[1], lb[1], out.stride(0)):
+                abi.echo_gemm_f32(M, N, K, 1.0, a, la[1], la[0], b, lb[1], lb[0], beta, out, out.stride(0))
+                return out
+    if beta == 0.0:
+        if out.dtype == a.dtype:
+            torch.mm(a, b, out=out)
+        else:
+            torch.mm(a, b, out_dtype=out.dtype, out=out)
+    elif out.dtype == a.dtype:
+        out.addmm_(a, b, beta=beta)
+    else:
+        torch.addmm(out, a, b, beta=beta, out_dtype=out.dtype, out=out)
+    return out
+
+
 def mm(a, b, out_dtype=None):
     """a @ b; out_dtype=torch.float32 forces an fp32 result for bf16 operands."""
-    if out_dtype is None or out_dtype == a.dtype:
-        return torch.mm(a, b)
-    return torch.mm(a, b, out_dtype=out_dtype)
+    od = a.dtype if out_dtype is None else out_dtype
+    if _USE_ECHO and a.dtype == b.dtype == od == torch.float32 and a.is_cuda:
+        out = torch.empty(a.shape[0], b.shape[1], dtype=od, device=a.device)
+        return gemm_into(out, a, b, 0.0)
+    return torch.mm(a, b) if od == a.dtype else torch.mm(a, b, out_dtype=od)
+
+
+def mm_out(out, a, b):
+    """out = a @ b (out preallocated, e.g. a gate slot)."""
+    return gemm_into(out, a, b, 0.0)
 
 
 def addmm_(c, a, b):
-    """c += a @ b in place (cuBLAS beta = 1)."""
-    if c.dtype == a.dtype:
-        c.addmm_(a, b)
-    else:
-        torch.addmm(c, a, b, out_dtype=c.dtype, out=c)
-    return c
+    """c += a @ b in place (beta = 1)."""
+    return gemm_into(c, a, b, 1.0)
 
 
 @contextmanager

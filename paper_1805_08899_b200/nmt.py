@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import abi, probe
-from .gemm import mm, addmm_, tf32, colsum as _colsum
+from .gemm import mm, mm_out, addmm_, tf32, colsum as _colsum
 from .lstm import LSTMLayer, TORCH_DTYPE
 from synth.data import nmt_param_shapes
 
@@ -182,7 +182,7 @@ class NMTModel(probe.GraphStep):
         for L in dec:
             L.h0, L.c0 = self.zero_h, self.zero_c
         Wx0 = self.w("dec0.Wx")
-        torch.mm(EmbT.view(Td * B, E), Wx0[:, :E].t(), out=dec[0].gates.view(Td * B, 4 * H))
+        mm_out(dec[0].gates.view(Td * B, 4 * H), EmbT.view(Td * B, E), Wx0[:, :E].t())
         if md == abi.RECOMPUTE:
             a["EmbT"] = None
             del EmbT
@@ -206,13 +206,13 @@ class NMTModel(probe.GraphStep):
                     if t > 0:
                         addmm_(L.gates[t], Aall[t - 1], WaT)     # input feeding: a_{t-1}
                 else:
-                    torch.mm(dec[l - 1].h_slot(t), self.w(f"dec{l}.Wx").t(), out=L.gates[t])
+                    mm_out(L.gates[t], dec[l - 1].h_slot(t), self.w(f"dec{l}.Wx").t())
                 if t > 0:
                     addmm_(L.gates[t], L.h_prev(t), self.w(f"dec{l}.Wh").t())
                 L.fwd_step(t, self.P[f"dec{l}.b"])
             q = dec[-1].h_slot(t)
             qp = qp_buf if md == abi.STASH else a["qp_st"][t]
-            torch.mm(q, Wq.t(), out=qp)
+            mm_out(qp, q, Wq.t())
             with probe.timed("attn_fwd"):
                 if md == abi.STASH:
                     ctx = a["ctx_st"][t]
@@ -220,7 +220,7 @@ class NMTModel(probe.GraphStep):
                 else:
                     ctx = ctx_tmp
                     abi.echo_attn_fwd(adesc, qp, Kp, v, Hs, sl, ctx, None, None)
-            torch.mm(ctx, Wcc.t(), out=pre)
+            mm_out(pre, ctx, Wcc.t())
             addmm_(pre, q, Wch.t())
             torch.tanh(pre, out=Aall[t])
         a["dec"] = dec
@@ -277,7 +277,7 @@ class NMTModel(probe.GraphStep):
     def _gemm_into(self, out, x, y):
         """out (an fp32 gradient view) = x @ y."""
         if x.dtype == torch.float32 and out.is_contiguous():
-            torch.mm(x, y, out=out)
+            mm_out(out, x, y)
         else:
             out.copy_(mm(x, y, torch.float32))
 
@@ -332,8 +332,8 @@ class NMTModel(probe.GraphStep):
             torch.mul(dAout[t], 1.0 - at * at, out=dPRE[t])      # tanh' = 1 - a^2
             top = dHdec[-1][t]
             with tf32(lowp):
-                torch.mm(dPRE[t], Wcc32, out=dctx)
-                top.addmm_(dPRE[t], Wch32)
+                mm_out(dctx, dPRE[t], Wcc32)
+                addmm_(top, dPRE[t], Wch32)
             with probe.timed("attn_bwd"):
                 if md == abi.STASH:
                     abi.echo_attn_bwd(adesc, None, None, v, Hs, sl, a["E_st"][t], a["al_st"][t], dctx, dQP[t], dKp,
@@ -342,7 +342,7 @@ class NMTModel(probe.GraphStep):
                     abi.echo_attn_bwd(adesc, a["qp_st"][t], Kp, v, Hs, sl, None, None, dctx, dQP[t], dKp, dHs,
                                       dv_part, ctx_all[t])
             with tf32(lowp):
-                top.addmm_(dQP[t], Wq32)
+                addmm_(top, dQP[t], Wq32)
             for l in reversed(range(Ld)):
                 L = dec[l]
                 L.bwd_step(t, dHdec[l][t], dcs[l])               # a3 (fused recompute in RECOMPUTE)
@@ -396,7 +396,7 @@ class NMTModel(probe.GraphStep):
         Hs32 = Hs.reshape(Ts * B, H)
         with tf32(lowp):
             gi(G["att.Wk"], dKpf.t(), Hs32 if Hs32.dtype == torch.float32 else Hs32.float())
-            dHs.view(Ts * B, H).addmm_(dKpf, self.P["att.Wk"])
+            addmm_(dHs.view(Ts * B, H), dKpf, self.P["att.Wk"])
         dKps = None
         del Hs, Hs32
         del dKp, dKpf, dKps
