@@ -297,20 +297,34 @@ def run_ours(args):
     def build(mode):
         m = NMTModel(cfg, dtype=dtype, mode=mode, device=dev)
         m.load_params(params)
-        if ws > 1:
-            m.grad_hook = dp.allreduce_mean_
         m.upload_batch(pinned[0])
         return m
+
+    def runner(m, use_graph):
+        """One training step.  N = 1: the whole step (fwd + bwd + SGD) is one CUDA graph.  N > 1:
+        the graph holds fwd + bwd; the NCCL allreduce of the flat gradient and the SGD update run
+        after it on the same stream (NCCL is kept out of graph capture)."""
+        if ws == 1:
+            return m.replay if use_graph else (lambda: m.step(lr))
+
+        def step():
+            if use_graph:
+                m.replay()
+            else:
+                m.step(0.0)
+            dp.allreduce_mean_(m.gflat)
+            m.apply_update(lr)
+        return step
 
     def timed(m, use_graph, K, W):
         """Device-timed K steps (inputs resident in HBM); returns ms per step (max over ranks)."""
         abi.LAUNCHES["count"] = 0
         if use_graph:
-            m.capture(lr)
+            m.capture(lr if ws == 1 else 0.0)
         launches_per_step = abi.LAUNCHES["count"]
         if use_graph:
             launches_per_step = launches_per_step // 3       # capture() = 2 warm-up steps + 1 captured
-        run = m.replay if use_graph else (lambda: m.step(lr))
+        run = runner(m, use_graph)
         for _ in range(W):
             run()
         torch.cuda.synchronize()
@@ -330,7 +344,7 @@ def run_ours(args):
     def e2e(m, use_graph, K):
         """Same metric through the public API with host buffers: per step H2D of the batch from pinned
         memory, the step, and a D2H read of the loss."""
-        run = m.replay if use_graph else (lambda: m.step(lr))
+        run = runner(m, use_graph)
         torch.cuda.synchronize()
         dp.barrier()
         t0 = time.perf_counter()
@@ -375,7 +389,7 @@ def run_ours(args):
     sampler = ClockSampler(local)
     sampler.start()
     # clocks are sampled over a second identical timed region (the first one followed the capture)
-    run = model.replay if use_graph else (lambda: model.step(lr))
+    run = runner(model, use_graph)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
@@ -395,7 +409,7 @@ def run_ours(args):
         """In-step kernel timing: the step graph re-captured with timing events around every a5 / a6
         launch (event-record nodes on the launch stream); K replays, durations read after each."""
         m = build(mode)
-        m.capture(lr, probe=True)
+        m.capture(lr, with_probe=True)
         for _ in range(W):
             m.replay()
         per = {}

@@ -21,11 +21,17 @@ def world():
 def init(backend=None):
     """Initialise the default process group from torchrun's environment (no-op for world size 1)."""
     ws, rank, local = world()
+    if torch.cuda.is_available() and torch.cuda.device_count() > 0:
+        local = local % torch.cuda.device_count()      # (a multi-rank smoke test on a 1-GPU box shares it)
     if ws > 1 and not dist.is_initialized():
         if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = os.environ.get("ECHO_DP_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend=backend, rank=rank, world_size=ws)
+        kw = {}
+        if backend == "nccl":
+            torch.cuda.set_device(local)                 # bind the rank to its GPU before NCCL starts
+            kw["device_id"] = torch.device("cuda", local)
+        dist.init_process_group(backend=backend, rank=rank, world_size=ws, **kw)
     return ws, rank, local
 
 

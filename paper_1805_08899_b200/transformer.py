@@ -102,9 +102,13 @@ class TXModel(probe.GraphStep):
         if self.grad_hook is not None:
             self.grad_hook(self.gflat)
         if lr != 0.0:
-            self.master.add_(self.gflat, alpha=-lr)
-            if self.sflat is not self.master:
-                self.sflat.copy_(self.master)
+            self.apply_update(lr)
+
+    def apply_update(self, lr):
+        """Plain SGD on the fp32 master weights, then refresh the storage-dtype copy."""
+        self.master.add_(self.gflat, alpha=-lr)
+        if self.sflat is not self.master:
+            self.sflat.copy_(self.master)
 
     def _forward(self):
         c, sd, dev, md = self.cfg, self.sd, self.device, self.mode
