@@ -186,6 +186,33 @@ echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, const void* K
                           const float* alpha_st, const float* dctx, float* dqp, float* dKp,
                           float* dHs, float* dv_part, void* ctx_regen, void* stream);
 
+/* a6, deferred accumulation (the algorithmic-minimum variant).  The same step as
+ * echo_attn_bwd without the per-step dKp / dH_s read-modify-write: it writes this step's
+ * softmax-backward rows instead and echo_attn_bwd_finish accumulates dKp / dH_s over all steps
+ * once, with the per-step expressions in the per-step order (t = Td-1 .. 0): results are
+ * bit-identical to calling echo_attn_bwd every step.
+ *  ds_out     [B,Ts] fp32 OUT  ds_s = alpha_s (dalpha_s - sum alpha dalpha) (0 for s >= len_b)
+ *  alpha_out  [B,Ts] fp32 OUT  regenerated alpha (RECOMPUTE; NULL in STASH, where alpha is stashed)
+ * Other arguments as echo_attn_bwd.  Errors as echo_attn_bwd; ECHO_ERR_UNSUPPORTED where only the
+ * generic (non-TMA) kernel fits (Ts > 256).                                                      */
+echo_status echo_attn_bwd_deferred(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
+                                   const void* Hs, const int32_t* src_len, const void* E_st,
+                                   const float* alpha_st, const float* dctx, float* dqp, float* dv_part,
+                                   void* ctx_regen, float* ds_out, float* alpha_out, void* stream);
+
+/* Finish the deferred accumulations over the Td steps of one backward pass:
+ *   dKp[b,s,:] = sum_{t=Td-1..0} (ds_t[b,s] v) (1 - tanh(z_t[b,s,:])^2),
+ *   z_t = round_s(qp_t[b,:] + Kp[b,s,:]) (RECOMPUTE) or the stashed z_t (STASH)
+ *   dHs[b,s,:] = sum_{t=Td-1..0} alpha_t[b,s] dctx_t[b,:]          (both OVERWRITTEN)
+ *  qp_all [Td,B,A] s (RECOMPUTE) | E_st_all [Td,B,Ts,A] s (STASH); Kp as in echo_attn_bwd
+ *  ds_all, alpha_all [Td,B,Ts] fp32 (the per-step ds_out / alpha_out, or the stashed alpha)
+ *  dctx_all [Td,B,Hk] fp32 (the per-step dctx)
+ * Errors: ECHO_ERR_INVALID, ECHO_ERR_CAPACITY (Td*Ts too large for the staged rows).               */
+echo_status echo_attn_bwd_finish(const echo_attn_desc* d, int32_t Td, const void* qp_all, const void* Kp,
+                                 const void* E_st_all, const void* v, const int32_t* src_len,
+                                 const float* ds_all, const float* alpha_all, const float* dctx_all,
+                                 float* dKp, float* dHs, void* stream);
+
 /* dv[a] (+)= sum_b dv_part[b,a] in ascending b (deterministic).  accumulate != 0 adds to dv. */
 echo_status echo_attn_dv_reduce(int32_t B, int32_t A, const float* dv_part, float* dv,
                                 int32_t accumulate, void* stream);

@@ -22,6 +22,7 @@ EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_c
             "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
             "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum", "echo_lstm_seq_fwd",
             "echo_lstm_seq_supported", "echo_gemm_f32", "echo_gemm_f32_supported",
+            "echo_attn_bwd_deferred", "echo_attn_bwd_finish",
             "echo_footprint_estimate")
 
 
@@ -73,6 +74,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_attn_fwd": [ctypes.POINTER(AttnDesc)] + [vp] * 9,
         "echo_attn_bwd": [ctypes.POINTER(AttnDesc)] + [vp] * 14,
         "echo_attn_dv_reduce": [i32, i32, vp, vp, i32, vp],
+        "echo_attn_bwd_deferred": [ctypes.POINTER(AttnDesc)] + [vp] * 14,
+        "echo_attn_bwd_finish": [ctypes.POINTER(AttnDesc), i32] + [vp] * 11,
         "echo_dot_softmax_fwd": [ctypes.POINTER(DotDesc)] + [vp] * 5,
         "echo_dot_softmax_bwd": [ctypes.POINTER(DotDesc)] + [vp] * 7,
         "echo_xent_fwd_bwd": [i32, i32, vp, vp, vp, vp, vp, vp],
@@ -189,6 +192,20 @@ def echo_lstm_seq_fwd(d, T, k0, k1, reverse, gx, Wh, bias, h0, c0, gates, c, c_r
     LAUNCHES["count"] += 1
     _check(load().echo_lstm_seq_fwd(ctypes.byref(d), T, k0, k1, int(reverse), _p(gx), _p(Wh), _p(bias), _p(h0), _p(c0),
                                     _p(gates), _p(c), int(c_ring), _p(tc), _p(h), _stream(stream)))
+
+
+def echo_attn_bwd_deferred(d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, dv_part, ctx_regen, ds_out,
+                           alpha_out, stream=None):
+    LAUNCHES["count"] += 1
+    _check(load().echo_attn_bwd_deferred(ctypes.byref(d), _p(qp), _p(Kp), _p(v), _p(Hs), _p(src_len), _p(E_st),
+                                         _p(alpha_st), _p(dctx), _p(dqp), _p(dv_part), _p(ctx_regen), _p(ds_out),
+                                         _p(alpha_out), _stream(stream)))
+
+
+def echo_attn_bwd_finish(d, Td, qp_all, Kp, E_st_all, v, src_len, ds_all, alpha_all, dctx_all, dKp, dHs, stream=None):
+    LAUNCHES["count"] += 2
+    _check(load().echo_attn_bwd_finish(ctypes.byref(d), Td, _p(qp_all), _p(Kp), _p(E_st_all), _p(v), _p(src_len),
+                                       _p(ds_all), _p(alpha_all), _p(dctx_all), _p(dKp), _p(dHs), _stream(stream)))
 
 
 def echo_xent_fwd_bwd(N, V, logits, bias, labels, row_loss, dlogits_bf16=None, stream=None):

@@ -487,6 +487,20 @@ static __host__ __device__ __forceinline__ int tma_cluster(int A, int Hk) {
   return C;
 }
 static __host__ __device__ __forceinline__ int tma_width(int X, int C) { return ((X + C - 1) / C + 7) / 8 * 8; }
+// launch geometry computed once on the host (no integer divisions per CTA)
+struct TmaGeo {
+  int C, Wb, WHb, R, Tr, P;   // cluster size, box widths, chunk rows, tile rows, phase-4 phases
+};
+__device__ __forceinline__ Slice make_slice_g(const TmaGeo& q, int A, int Hk, int r) {
+  Slice g;
+  g.C = q.C;
+  g.r = r;
+  g.a0 = min(A, r * q.Wb);
+  g.a1 = min(A, g.a0 + q.Wb);
+  g.h0 = min(Hk, r * q.WHb);
+  g.h1 = min(Hk, g.h0 + q.WHb);
+  return g;
+}
 __device__ __forceinline__ Slice make_slice(int A, int Hk, int C, int r) {
   Slice g;
   g.C = C;
@@ -674,7 +688,8 @@ __device__ __forceinline__ void issue_chunks(uint64_t* bar, int n, int R, void* 
 
 // Shared-memory tiles: [Tr][box width] per tensor for this CTA's column slice.
 template <typename T>
-__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, const __grid_constant__ CUtensorMap mK,
+__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, TmaGeo q,
+                                                            const __grid_constant__ CUtensorMap mK,
                                                             const __grid_constant__ CUtensorMap mH,
                                                             const T* __restrict__ qp, const T* __restrict__ v,
                                                             const int32_t* __restrict__ src_len, T* __restrict__ ctx,
@@ -684,11 +699,11 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, co
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar[TMA_CHUNKS];
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
-  const Slice g = make_slice(A, Hk, (int)cl.num_blocks(), (int)cl.block_rank());
+  const Slice g = make_slice_g(q, A, Hk, (int)cl.block_rank());
   const int W = g.a1 - g.a0, WH = g.h1 - g.h0;               // valid widths
-  const int Wb = tma_width(A, g.C), WHb = tma_width(Hk, g.C);  // box widths (smem row strides)
+  const int Wb = q.Wb, WHb = q.WHb;                           // box widths (smem row strides)
   const int Tp = (Ts + 3) & ~3;
-  const int R = tma_rows(Ts, Wb, WHb, (int)sizeof(T)), Tr = tma_tile_rows(Ts, R);
+  const int R = q.R, Tr = q.Tr;
   T* kz = reinterpret_cast<T*>(smraw);                                         // [Tr][Wb]
   T* hs = reinterpret_cast<T*>(smraw + al128((size_t)Tr * Wb * sizeof(T)));    // [Tr][WHb]
   T* qps = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(hs) + al128((size_t)Tr * WHb * sizeof(T)));
@@ -742,7 +757,8 @@ static __host__ __device__ __forceinline__ int tma_phases(int W, int WH) { retur
 // dKp / dH_s are NOT staged: phase 4 streams them through registers (16-byte vectors, rows s < n
 // only), so the shared footprint is the K/Z and H_s slices alone and four CTAs fit per SM.
 template <typename T>
-__global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d, const __grid_constant__ CUtensorMap mK,
+__global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d, TmaGeo q,
+                                                               const __grid_constant__ CUtensorMap mK,
                                                                const __grid_constant__ CUtensorMap mH,
                                                                const __grid_constant__ CUtensorMap mdK,
                                                                const __grid_constant__ CUtensorMap mdH,
@@ -751,18 +767,21 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
                                                                const float* __restrict__ alpha_st,
                                                                const float* __restrict__ dctx, float* __restrict__ dqp,
                                                                float* __restrict__ dKp, float* __restrict__ dHs,
-                                                               float* __restrict__ dv_part, T* __restrict__ ctx_regen) {
+                                                               float* __restrict__ dv_part, T* __restrict__ ctx_regen,
+                                                               float* __restrict__ ds_out, float* __restrict__ al_out) {
+  // deferred (dKp == NULL): no dKp / dH_s read-modify-write; this step's ds (and alpha) rows go to
+  // ds_out / al_out and echo_attn_bwd_finish accumulates dKp / dH_s over all steps afterwards
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar[TMA_CHUNKS];
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
-  const Slice g = make_slice(A, Hk, (int)cl.num_blocks(), (int)cl.block_rank());
+  const Slice g = make_slice_g(q, A, Hk, (int)cl.block_rank());
   const int W = g.a1 - g.a0, WH = g.h1 - g.h0;
-  const int Wb = tma_width(A, g.C), WHb = tma_width(Hk, g.C);
+  const int Wb = q.Wb, WHb = q.WHb;
   const int Tp = (Ts + 3) & ~3;
-  const int P = tma_phases(Wb, WHb);
-  const int R = tma_rows(Ts, Wb, WHb, (int)sizeof(T)), Tr = tma_tile_rows(Ts, R);
+  const int P = q.P;
+  const int R = q.R, Tr = q.Tr;
   // kz [Tr][Wb] T (E overwrites it in place for fp32) | hs [Tr][WHb] T | E [Tr][Wb] f32 (bf16 only)
   // | floats | phase partials [2][P][Wb] (aliased onto E when it fits)
   constexpr bool kE_ALIAS = sizeof(T) == sizeof(float);
@@ -827,7 +846,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   // L2 prefetch of the dKp / dH_s tiles phase 4 streams, issued by thread 0 once this CTA's loads
   // have landed so the reads overlap the exchange / softmax phases instead of phase 4
 #ifndef ECHO_A6_NO_PREFETCH
-  if (tid == 0) {
+  if (tid == 0 && dKp) {
     for (int k = 0; k * R < n; ++k) mbar_wait(&bar[k], 0);
     for (int k = 0; k * R < n; ++k) {
       if (W > 0) tma_prefetch_3d(&mdK, g.a0, b, k * R);
@@ -852,6 +871,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     for (int s = lane; s < n; s += 32) dsv[s] = __fmul_rn(al[s], __fsub_rn(dal[s], acc));
   }
   __syncthreads();
+  if (ds_out && g.r == 0)                                       // deferred: publish this step's rows
+    for (int s = tid; s < Ts; s += ATT_THREADS) {
+      ds_out[(long)b * Ts + s] = s < n ? dsv[s] : 0.0f;
+      if (al_out) al_out[(long)b * Ts + s] = s < n ? al[s] : 0.0f;
+    }
   ECHO_PHASE(6);
   if (recompute && ctx_regen) ctx_columns<T>(hs, WHb, WH, al, n, ctx_regen + (long)b * Hk + g.h0, tid);
   ECHO_PHASE(7);
@@ -867,13 +891,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     const int c = gi * 4;
     float vc[4];
     lds4(vs + c, vc);
-    float* base = dKp + (long)b * d.kp_stride_b + g.a0 + c;
+    float* base = dKp ? dKp + (long)b * d.kp_stride_b + g.a0 + c : nullptr;
     for (int s0 = ph; s0 < n; s0 += U * P) {
       float4 x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int s = s0 + u * P;
-        if (s < n) x[u] = *reinterpret_cast<const float4*>(base + (long)s * d.kp_stride_s);
+        if (s < n && dKp) x[u] = *reinterpret_cast<const float4*>(base + (long)s * d.kp_stride_s);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -889,11 +913,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
             dq[k] = __fadd_rn(dq[k], dE);
             dvv[k] = __fmaf_rn(ds, e[k], dvv[k]);
           }
-          stg4(base + (long)s * d.kp_stride_s, xv);
+          if (dKp) stg4(base + (long)s * d.kp_stride_s, xv);
         }
       }
     }
-  } else if (ph < P && gi >= GA && (gi - GA) * 4 < WH) {
+  } else if (dHs && ph < P && gi >= GA && (gi - GA) * 4 < WH) {
     const int c = (gi - GA) * 4;
     float dc[4];
     lds4(dcs + c, dc);
@@ -940,6 +964,85 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   ECHO_PHASE(10);
 }
 
+// ---------------------------------------------------------------- a6 deferred accumulations
+// dKp[b,s,:] = sum over t = Td-1 .. 0 of dE_t and dH_s[b,s,:] = sum over t = Td-1 .. 0 of
+// alpha_t[b,s] dctx_t[b,:], with dE_t = (ds_t v) (1 - E_t^2) and E_t = tanh(z_t), evaluated with
+// exactly the expressions and the t order the per-step read-modify-write used: bit-identical to
+// it.  One CTA per (row b, 64-column block); thread = (column, position phase).
+constexpr int FIN_COLS = 64;
+template <typename T>
+__global__ void __launch_bounds__(256) attn_dkp_finish_kernel(echo_attn_desc d, int Td, const T* __restrict__ qp_all,
+                                                              const T* __restrict__ Kp, const T* __restrict__ Z_all,
+                                                              const T* __restrict__ v,
+                                                              const int32_t* __restrict__ src_len,
+                                                              const float* __restrict__ ds_all, float* __restrict__ dKp) {
+  pdl_wait();
+  extern __shared__ float fsm[];
+  const int A = d.A, Ts = d.Ts, B = d.B;
+  float* qs = fsm;                                  // [Td][FIN_COLS] qp (RECOMPUTE)
+  float* dss = qs + (size_t)Td * FIN_COLS;          // [Td][Ts] ds
+  const int b = blockIdx.y, a0 = blockIdx.x * FIN_COLS, tid = threadIdx.x;
+  const int n = row_len(src_len, b, Ts);
+  const bool rec = Z_all == nullptr;
+  for (int i = tid; i < Td * FIN_COLS; i += 256) {
+    const int t = i / FIN_COLS, c = i - t * FIN_COLS;
+    qs[i] = (rec && a0 + c < A) ? to_f(qp_all[((long)t * B + b) * A + a0 + c]) : 0.0f;
+  }
+  for (int i = tid; i < Td * Ts; i += 256) {
+    const int t = i / Ts, s = i - t * Ts;
+    dss[i] = ds_all[((long)t * B + b) * Ts + s];
+  }
+  __syncthreads();
+  const int c = tid % FIN_COLS, a = a0 + c;
+  if (a >= A) return;
+  const float vc = to_f(v[a]);
+  for (int s = tid / FIN_COLS; s < Ts; s += 256 / FIN_COLS) {
+    float acc = 0.0f;
+    if (s < n) {
+      const float kz = rec ? to_f(Kp[(long)b * d.kp_stride_b + (long)s * d.kp_stride_s + a]) : 0.0f;
+      for (int t = Td - 1; t >= 0; --t) {
+        const float z = rec ? St<T>::round(__fadd_rn(qs[t * FIN_COLS + c], kz))
+                            : to_f(Z_all[(((long)t * B + b) * Ts + s) * A + a]);
+        const float e = tanhf(z);
+        const float dE = __fmul_rn(__fmul_rn(dss[t * Ts + s], vc), __fsub_rn(1.0f, __fmul_rn(e, e)));
+        acc = __fadd_rn(acc, dE);
+      }
+    }
+    dKp[(long)b * d.kp_stride_b + (long)s * d.kp_stride_s + a] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) attn_dhs_finish_kernel(echo_attn_desc d, int Td,
+                                                              const int32_t* __restrict__ src_len,
+                                                              const float* __restrict__ al_all,
+                                                              const float* __restrict__ dctx_all,
+                                                              float* __restrict__ dHs) {
+  pdl_wait();
+  extern __shared__ float fsm[];
+  const int Hk = d.Hk, Ts = d.Ts, B = d.B;
+  float* cs = fsm;                                  // [Td][FIN_COLS] dctx
+  float* als = cs + (size_t)Td * FIN_COLS;          // [Td][Ts] alpha
+  const int b = blockIdx.y, h0 = blockIdx.x * FIN_COLS, tid = threadIdx.x;
+  const int n = row_len(src_len, b, Ts);
+  for (int i = tid; i < Td * FIN_COLS; i += 256) {
+    const int t = i / FIN_COLS, c = i - t * FIN_COLS;
+    cs[i] = h0 + c < Hk ? dctx_all[((long)t * B + b) * Hk + h0 + c] : 0.0f;
+  }
+  for (int i = tid; i < Td * Ts; i += 256) {
+    const int t = i / Ts, s = i - t * Ts;
+    als[i] = al_all[((long)t * B + b) * Ts + s];
+  }
+  __syncthreads();
+  const int c = tid % FIN_COLS, h = h0 + c;
+  if (h >= Hk) return;
+  for (int s = tid / FIN_COLS; s < Ts; s += 256 / FIN_COLS) {
+    float acc = 0.0f;
+    if (s < n)
+      for (int t = Td - 1; t >= 0; --t) acc = __fmaf_rn(als[t * Ts + s], cs[t * FIN_COLS + c], acc);
+    dHs[(long)b * d.hs_stride_b + (long)s * d.hs_stride_s + h] = acc;
+  }
+}
+
 __global__ void dv_reduce_kernel(int B, int A, const float* __restrict__ part, float* __restrict__ dv, int acc) {
   pdl_wait();
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
@@ -968,7 +1071,8 @@ static size_t bwd_smem(const echo_attn_desc* d) {
 
 // TMA path: cluster size and shared-memory footprint; returns false if the generic path must run
 static size_t al128h(size_t b) { return (b + 127) & ~(size_t)127; }
-static bool tma_params(const echo_attn_desc* d, int* C, int* rows, size_t* smem_fwd, size_t* smem_bwd) {
+static bool tma_params(const echo_attn_desc* d, int* C, int* rows, size_t* smem_fwd, size_t* smem_bwd,
+                       TmaGeo* geo) {
   const size_t sT = d->dtype == ECHO_FP32 ? 4 : 2;
   if (d->A > 1024 || d->Hk > 1024 || d->Ts > 256) return false;
   const int c = tma_cluster(d->A, d->Hk);
@@ -983,6 +1087,12 @@ static bool tma_params(const echo_attn_desc* d, int* C, int* rows, size_t* smem_
   if (bwd > 220 * 1024) return false;
   *C = c;
   *rows = R;
+  geo->C = c;
+  geo->Wb = (int)W;
+  geo->WHb = (int)WH;
+  geo->R = R;
+  geo->Tr = (int)Ts;
+  geo->P = (int)P;
   *smem_fwd = fwd;
   *smem_bwd = bwd;
   return true;
@@ -1081,19 +1191,20 @@ extern "C" echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, co
   cudaError_t e;
   int tC, tR;
   size_t sf, sb;
+  TmaGeo geo;
   CUtensorMap mK, mH;
   const bool bfd = d->dtype == ECHO_BF16;
-  if (tma_params(d, &tC, &tR, &sf, &sb) &&
+  if (tma_params(d, &tC, &tR, &sf, &sb, &geo) &&
       map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC), tR) &&
       map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC), tR)) {
     if (d->dtype == ECHO_FP32) {
       if ((s = set_smem((const void*)attn_fwd_tma<float>, sf, fn))) return s;
-      e = launch_cluster(attn_fwd_tma<float>, tC, d->B, sf, st, *d, mK, mH, (const float*)qp, (const float*)v, src_len,
+      e = launch_cluster(attn_fwd_tma<float>, tC, d->B, sf, st, *d, geo, mK, mH, (const float*)qp, (const float*)v, src_len,
                          (float*)ctx, (float*)E_st, alpha_st);
     } else {
       typedef __nv_bfloat16 bf;
       if ((s = set_smem((const void*)attn_fwd_tma<bf>, sf, fn))) return s;
-      e = launch_cluster(attn_fwd_tma<bf>, tC, d->B, sf, st, *d, mK, mH, (const bf*)qp, (const bf*)v, src_len, (bf*)ctx,
+      e = launch_cluster(attn_fwd_tma<bf>, tC, d->B, sf, st, *d, geo, mK, mH, (const bf*)qp, (const bf*)v, src_len, (bf*)ctx,
                          (bf*)E_st, alpha_st);
     }
     if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
@@ -1114,57 +1225,68 @@ extern "C" echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, co
   return check_launch(fn);
 }
 
-extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
-                                     const void* Hs, const int32_t* src_len, const void* E_st,
-                                     const float* alpha_st, const float* dctx, float* dqp, float* dKp, float* dHs,
-                                     float* dv_part, void* ctx_regen, void* stream) {
-  const char* fn = "echo_attn_bwd";
+static echo_status attn_bwd_impl(const char* fn, const echo_attn_desc* d, const void* qp, const void* Kp,
+                                 const void* v, const void* Hs, const int32_t* src_len, const void* E_st,
+                                 const float* alpha_st, const float* dctx, float* dqp, float* dKp, float* dHs,
+                                 float* dv_part, void* ctx_regen, float* ds_out, float* al_out, void* stream) {
   echo_status s = check_attn(fn, d);
   if (s) return s;
+  const bool deferred = ds_out != nullptr;
   ECHO_REQ(v, "v");
   ECHO_REQ(Hs, "Hs");
   ECHO_REQ(dctx, "dctx");
   ECHO_REQ(dqp, "dqp");
-  ECHO_REQ(dKp, "dKp");
-  ECHO_REQ(dHs, "dHs");
+  if (!deferred) {
+    ECHO_REQ(dKp, "dKp");
+    ECHO_REQ(dHs, "dHs");
+  }
   ECHO_REQ(dv_part, "dv_part");
   if (d->mode == ECHO_STASH) {
     ECHO_REQ(E_st, "E_st");
     if (!alpha_st) return fail(ECHO_ERR_INVALID, "%s: alpha_st required in STASH mode", fn);
     if (ctx_regen) return fail(ECHO_ERR_INVALID, "%s: ctx_regen must be NULL in STASH mode", fn);
+    if (al_out) return fail(ECHO_ERR_INVALID, "%s: alpha_out must be NULL in STASH mode (alpha is stashed)", fn);
   } else {
     ECHO_REQ(qp, "qp");
     ECHO_REQ(Kp, "Kp");
     if (E_st || alpha_st) return fail(ECHO_ERR_INVALID, "%s: E_st / alpha_st must be NULL in RECOMPUTE mode", fn);
     if (ctx_regen && !aligned16(ctx_regen)) return fail(ECHO_ERR_INVALID, "%s: ctx_regen not 16-byte aligned", fn);
+    if (deferred && !al_out) return fail(ECHO_ERR_INVALID, "%s: alpha_out required in deferred RECOMPUTE", fn);
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int C = att_cluster(d->Ts), chunk = att_chunk(d->Ts, C);
   cudaError_t e;
   int tC, tR;
   size_t sf, sb;
+  TmaGeo geo;
   CUtensorMap mK, mH, mdK, mdH;
   const bool bfd = d->dtype == ECHO_BF16;
   const bool rec = d->mode == ECHO_RECOMPUTE;
-  if (tma_params(d, &tC, &tR, &sf, &sb) &&
+  if (tma_params(d, &tC, &tR, &sf, &sb, &geo) &&
       (rec ? map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC), tR)
            : map3d(&mK, E_st, bfd, d->A, d->B, d->Ts, (int64_t)d->Ts * d->A, d->A, tma_width(d->A, tC), tR)) &&
       map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC), tR) &&
-      map3d(&mdK, dKp, false, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC), tR) &&
-      map3d(&mdH, dHs, false, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC), tR)) {
+      (deferred ||
+       (map3d(&mdK, dKp, false, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC), tR) &&
+        map3d(&mdH, dHs, false, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC), tR)))) {
+    if (deferred) {                                              // prefetch maps unused (no dKp / dH_s)
+      mdK = mK;
+      mdH = mH;
+    }
     if (d->dtype == ECHO_FP32) {
       if ((s = set_smem((const void*)attn_bwd_tma<float>, sb, fn))) return s;
-      e = launch_cluster(attn_bwd_tma<float>, tC, d->B, sb, st, *d, mK, mH, mdK, mdH, (const float*)qp, (const float*)v, src_len,
-                         rec, alpha_st, dctx, dqp, dKp, dHs, dv_part, (float*)ctx_regen);
+      e = launch_cluster(attn_bwd_tma<float>, tC, d->B, sb, st, *d, geo, mK, mH, mdK, mdH, (const float*)qp, (const float*)v,
+                         src_len, rec, alpha_st, dctx, dqp, dKp, dHs, dv_part, (float*)ctx_regen, ds_out, al_out);
     } else {
       typedef __nv_bfloat16 bf;
       if ((s = set_smem((const void*)attn_bwd_tma<bf>, sb, fn))) return s;
-      e = launch_cluster(attn_bwd_tma<bf>, tC, d->B, sb, st, *d, mK, mH, mdK, mdH, (const bf*)qp, (const bf*)v, src_len, rec,
-                         alpha_st, dctx, dqp, dKp, dHs, dv_part, (bf*)ctx_regen);
+      e = launch_cluster(attn_bwd_tma<bf>, tC, d->B, sb, st, *d, geo, mK, mH, mdK, mdH, (const bf*)qp, (const bf*)v,
+                         src_len, rec, alpha_st, dctx, dqp, dKp, dHs, dv_part, (bf*)ctx_regen, ds_out, al_out);
     }
     if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
     return check_launch(fn);
   }
+  if (deferred) return fail(ECHO_ERR_UNSUPPORTED, "%s: deferred mode needs the TMA path (Ts <= 256, slices fit)", fn);
   const size_t smem = bwd_smem(d);
   if (d->dtype == ECHO_FP32) {
     if ((s = set_smem((const void*)attn_bwd_kernel<float>, smem, fn))) return s;
@@ -1178,6 +1300,63 @@ extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, co
                        (const bf*)Hs, src_len, (const bf*)E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part,
                        (bf*)ctx_regen);
   }
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
+}
+
+extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
+                                     const void* Hs, const int32_t* src_len, const void* E_st,
+                                     const float* alpha_st, const float* dctx, float* dqp, float* dKp, float* dHs,
+                                     float* dv_part, void* ctx_regen, void* stream) {
+  return attn_bwd_impl("echo_attn_bwd", d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part,
+                       ctx_regen, nullptr, nullptr, stream);
+}
+
+extern "C" echo_status echo_attn_bwd_deferred(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
+                                              const void* Hs, const int32_t* src_len, const void* E_st,
+                                              const float* alpha_st, const float* dctx, float* dqp, float* dv_part,
+                                              void* ctx_regen, float* ds_out, float* alpha_out, void* stream) {
+  const char* fn = "echo_attn_bwd_deferred";
+  if (!ds_out) return fail(ECHO_ERR_INVALID, "%s: ds_out is NULL", fn);
+  return attn_bwd_impl(fn, d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, nullptr, nullptr, dv_part, ctx_regen,
+                       ds_out, alpha_out, stream);
+}
+
+extern "C" echo_status echo_attn_bwd_finish(const echo_attn_desc* d, int32_t Td, const void* qp_all, const void* Kp,
+                                            const void* E_st_all, const void* v, const int32_t* src_len,
+                                            const float* ds_all, const float* alpha_all, const float* dctx_all,
+                                            float* dKp, float* dHs, void* stream) {
+  const char* fn = "echo_attn_bwd_finish";
+  echo_status s = check_attn(fn, d);
+  if (s) return s;
+  if (Td <= 0) return fail(ECHO_ERR_INVALID, "%s: Td=%d", fn, Td);
+  if (!v || !ds_all || !alpha_all || !dctx_all || !dKp || !dHs) return fail(ECHO_ERR_INVALID, "%s: NULL pointer", fn);
+  if (d->mode == ECHO_STASH) {
+    if (!E_st_all) return fail(ECHO_ERR_INVALID, "%s: E_st_all required in STASH mode", fn);
+  } else if (!qp_all || !Kp || E_st_all) {
+    return fail(ECHO_ERR_INVALID, "%s: RECOMPUTE needs qp_all and Kp (and no E_st_all)", fn);
+  }
+  const size_t smem = sizeof(float) * ((size_t)Td * FIN_COLS + (size_t)Td * d->Ts);
+  if (smem > 200 * 1024) return fail(ECHO_ERR_CAPACITY, "%s: Td=%d x Ts=%d too large", fn, Td, d->Ts);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool rec = d->mode == ECHO_RECOMPUTE;
+  cudaError_t e;
+  if (d->dtype == ECHO_FP32) {
+    if ((s = set_smem((const void*)attn_dkp_finish_kernel<float>, smem, fn))) return s;
+    e = launch(attn_dkp_finish_kernel<float>, dim3((d->A + FIN_COLS - 1) / FIN_COLS, d->B), dim3(256), smem, st, 1, *d,
+               (int)Td, (const float*)qp_all, (const float*)Kp, rec ? nullptr : (const float*)E_st_all,
+               (const float*)v, src_len, ds_all, dKp);
+  } else {
+    typedef __nv_bfloat16 bf;
+    if ((s = set_smem((const void*)attn_dkp_finish_kernel<bf>, smem, fn))) return s;
+    e = launch(attn_dkp_finish_kernel<bf>, dim3((d->A + FIN_COLS - 1) / FIN_COLS, d->B), dim3(256), smem, st, 1, *d,
+               (int)Td, (const bf*)qp_all, (const bf*)Kp, rec ? nullptr : (const bf*)E_st_all, (const bf*)v, src_len,
+               ds_all, dKp);
+  }
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  if ((s = set_smem((const void*)attn_dhs_finish_kernel, smem, fn))) return s;
+  e = launch(attn_dhs_finish_kernel, dim3((d->Hk + FIN_COLS - 1) / FIN_COLS, d->B), dim3(256), smem, st, 1, *d,
+             (int)Td, src_len, alpha_all, dctx_all, dHs);
   if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);
 }

@@ -102,6 +102,14 @@ class NMTModel(probe.GraphStep):
         return sum(t.numel() * t.element_size() for t in self.inputs.values())
 
     # ------------------------------------------------------------ encoder wavefront helpers
+    def _a6_deferred(self):
+        """Deferred dKp / dH_s accumulation (echo_attn_bwd_deferred + echo_attn_bwd_finish; bit-
+        identical results) instead of the per-step read-modify-write?  Opt-in (ECHO_A6_DEFERRED=1):
+        it removes 2/3 of a6's HBM bytes, but a6 is latency/issue-bound, not HBM-bound, at both ends
+        of the batch range (CUPTI, C5 bf16: a6 3.14 -> 2.47 ms/step, plus 28 + 7 ms of finish
+        passes = no net gain; C2: equal within noise), so the per-step path stays the default."""
+        return os.environ.get("ECHO_A6_DEFERRED", "0") == "1"
+
     def _chunks(self, T):
         """Wavefront chunk boundaries over the encoder's time axis.  Measured on C2 (bench, CUDA
         graph): fp32 29.9 -> 28.1 ms/step with 5 chunks (its SIMT GEMMs leave most SMs idle, so two
@@ -318,11 +326,19 @@ class NMTModel(probe.GraphStep):
         dcs = [torch.zeros(B, H, dtype=torch.float32, device=dev) for _ in range(Ld)]
         dPRE = torch.empty(Td, B, H, dtype=torch.float32, device=dev)
         dQP = torch.empty(Td, B, A, dtype=torch.float32, device=dev)
-        dKp = torch.zeros(Ts, B, A, dtype=torch.float32, device=dev)
-        dHs = torch.zeros(Ts, B, H, dtype=torch.float32, device=dev)
+        deferred = self._a6_deferred()
+        if deferred:                                             # dKp / dH_s accumulated once after the loop
+            dKp = torch.empty(Ts, B, A, dtype=torch.float32, device=dev)
+            dHs = torch.empty(Ts, B, H, dtype=torch.float32, device=dev)
+            ds_all = torch.empty(Td, B, Ts, dtype=torch.float32, device=dev)
+            al_all = a["al_st"] if md == abi.STASH else torch.empty(Td, B, Ts, dtype=torch.float32, device=dev)
+            dctx_all = torch.empty(Td, B, H, dtype=torch.float32, device=dev)
+        else:
+            dKp = torch.zeros(Ts, B, A, dtype=torch.float32, device=dev)
+            dHs = torch.zeros(Ts, B, H, dtype=torch.float32, device=dev)
+            dctx1 = torch.empty(B, H, dtype=torch.float32, device=dev)
         dv_part = torch.zeros(B, A, dtype=torch.float32, device=dev)
         ctx_all = a["ctx_st"] if md == abi.STASH else torch.empty(Td, B, H, dtype=sd, device=dev)
-        dctx = torch.empty(B, H, dtype=torch.float32, device=dev)
         Wx0 = self.w("dec0.Wx")
         WxA = Wx0[:, E:]
         Wq, Wcc, Wch, v = self.w("att.Wq"), self.w("att.Wcc"), self.w("att.Wch"), self.w("att.v")
@@ -335,16 +351,20 @@ class NMTModel(probe.GraphStep):
             at = Aall[t].float()
             torch.mul(dAout[t], 1.0 - at * at, out=dPRE[t])      # tanh' = 1 - a^2
             top = dHdec[-1][t]
+            dctx = dctx_all[t] if deferred else dctx1
             with tf32(lowp):
                 mm_out(dctx, dPRE[t], Wcc32)
                 addmm_(top, dPRE[t], Wch32)
             with probe.timed("attn_bwd"):
-                if md == abi.STASH:
-                    abi.echo_attn_bwd(adesc, None, None, v, Hs, sl, a["E_st"][t], a["al_st"][t], dctx, dQP[t], dKp,
-                                      dHs, dv_part, None)
-                else:                                            # a6 regenerates E, scores, alpha, ctx
-                    abi.echo_attn_bwd(adesc, a["qp_st"][t], Kp, v, Hs, sl, None, None, dctx, dQP[t], dKp, dHs,
-                                      dv_part, ctx_all[t])
+                st = md == abi.STASH                             # RECOMPUTE: a6 regenerates E, scores, alpha, ctx
+                qp_t, Kp_t = (None, None) if st else (a["qp_st"][t], Kp)
+                E_t, al_t = (a["E_st"][t], a["al_st"][t]) if st else (None, None)
+                creg = None if st else ctx_all[t]
+                if deferred:
+                    abi.echo_attn_bwd_deferred(adesc, qp_t, Kp_t, v, Hs, sl, E_t, al_t, dctx, dQP[t], dv_part, creg,
+                                               ds_all[t], None if st else al_all[t])
+                else:
+                    abi.echo_attn_bwd(adesc, qp_t, Kp_t, v, Hs, sl, E_t, al_t, dctx, dQP[t], dKp, dHs, dv_part, creg)
             with tf32(lowp):
                 addmm_(top, dQP[t], Wq32)
             for l in reversed(range(Ld)):
@@ -368,6 +388,12 @@ class NMTModel(probe.GraphStep):
             gi(G["att.Wch"], dPREs.t(), qall)
             gi(G["att.Wq"], dQP.view(N, A).t(), qall)
         abi.echo_attn_dv_reduce(B, A, dv_part, G["att.v"], 0)
+        if deferred:
+            with probe.timed("attn_bwd_finish"):
+                abi.echo_attn_bwd_finish(adesc, Td, None if md == abi.STASH else a["qp_st"], None if md == abi.STASH else Kp,
+                                         a["E_st"] if md == abi.STASH else None, v, sl, ds_all, al_all, dctx_all, dKp,
+                                         dHs)
+            del ds_all, al_all, dctx_all
         del qall
         del dPREs, dPRE, dQP
         for l in range(Ld):

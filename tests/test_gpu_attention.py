@@ -113,3 +113,57 @@ def test_dot_softmax_dropout(storage, R, L, p, cuda_dev):
     assert bits_equal(out[abi.STASH][2], out[abi.RECOMPUTE][2])
     assert bits_equal(out[abi.RECOMPUTE][3], out[abi.RECOMPUTE][0])
     assert_close(host(out[abi.STASH][4]), ref["P"], storage, "P")
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("B,Ts,A,Hk,Td", [(5, 37, 64, 48, 4), (128, 50, 512, 512, 3)])
+def test_attention_deferred_bitwise(storage, B, Ts, A, Hk, Td, cuda_dev):
+    """echo_attn_bwd_deferred + echo_attn_bwd_finish == Td per-step echo_attn_bwd calls, bitwise
+    (dKp, dH_s, dqp, dv partials), both modes; the per-step path is itself pinned to the oracle."""
+    abi = _abi()
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    sd = torch.float32 if storage == "fp32" else torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(B + Ts)
+    rn = lambda *s, sc=1.0: (torch.randn(*s, device="cuda", generator=g) * sc).to(sd)
+    Kp, Hs, v = rn(Ts, B, A, sc=0.5), rn(Ts, B, Hk), rn(A, sc=0.3)
+    qps = rn(Td, B, A, sc=0.5)
+    sl = torch.randint(1, Ts + 1, (B,), device="cuda", generator=g).to(torch.int32)
+    dctxs = torch.randn(Td, B, Hk, device="cuda", generator=g)
+    for mode in (abi.STASH, abi.RECOMPUTE):
+        desc = abi.AttnDesc(B, Ts, A, Hk, dt, mode, A, B * A, Hk, B * Hk)
+        st = mode == abi.STASH
+        E = torch.empty(Td, B, Ts, A, device="cuda", dtype=sd) if st else None
+        al = torch.empty(Td, B, Ts, device="cuda") if st else None
+        ctx = torch.empty(B, Hk, device="cuda", dtype=sd)
+        for t in range(Td):
+            abi.echo_attn_fwd(desc, qps[t], Kp, v, Hs, sl, ctx, E[t] if st else None, al[t] if st else None)
+        res = {}
+        for deferred in (False, True):
+            dqp = torch.empty(Td, B, A, device="cuda")
+            dvp = torch.zeros(B, A, device="cuda")
+            creg = None if st else torch.empty(Td, B, Hk, device="cuda", dtype=sd)
+            if deferred:
+                dKp = torch.full((Ts, B, A), float("nan"), device="cuda")
+                dHs = torch.full((Ts, B, Hk), float("nan"), device="cuda")
+                ds_all = torch.empty(Td, B, Ts, device="cuda")
+                al_all = al if st else torch.empty(Td, B, Ts, device="cuda")
+            else:
+                dKp = torch.zeros(Ts, B, A, device="cuda")
+                dHs = torch.zeros(Ts, B, Hk, device="cuda")
+            for t in reversed(range(Td)):
+                args = (None, None) if st else (qps[t], Kp)
+                e_a = (E[t], al[t]) if st else (None, None)
+                if deferred:
+                    abi.echo_attn_bwd_deferred(desc, *args, v, Hs, sl, *e_a, dctxs[t], dqp[t], dvp,
+                                               None if st else creg[t], ds_all[t], None if st else al_all[t])
+                else:
+                    abi.echo_attn_bwd(desc, *args, v, Hs, sl, *e_a, dctxs[t], dqp[t], dKp, dHs, dvp,
+                                      None if st else creg[t])
+            if deferred:
+                abi.echo_attn_bwd_finish(desc, Td, None if st else qps, None if st else Kp, E if st else None, v, sl,
+                                         ds_all, al_all, dctxs, dKp, dHs)
+            torch.cuda.synchronize()
+            res[deferred] = (dKp, dHs, dqp, dvp, creg)
+        for k, (x, y) in enumerate(zip(res[False], res[True])):
+            if x is not None:
+                assert bits_equal(x, y), (mode, k)

@@ -144,3 +144,21 @@ def test_stash_bytes_equal_estimator(cfg, storage, cuda_dev):
                                                        {k: v.numel() * v.element_size() for k, v in m.stash.items()})
         m._backward(acts)
         del acts
+
+
+@pytest.mark.parametrize("cfg,storage", [(SMALL_NMT, "fp32"), (RAGGED, "bf16"), (C2, "bf16")],
+                         ids=["small-fp32", "ragged-bf16", "C2-bf16"])
+def test_nmt_deferred_a6_bitwise(cfg, storage, cuda_dev, monkeypatch):
+    """The deferred dKp / dH_s accumulation gives bit-identical gradients to the per-step one."""
+    from paper_1805_08899_b200 import abi
+    params = nmt_params(21, cfg, storage)
+    batch = nmt_batch(22, cfg, lengths="random")
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("ECHO_A6_DEFERRED", flag)
+        for mode in (abi.STASH, abi.RECOMPUTE):
+            m, _ = _run(cfg, params, batch, dt, mode)
+            out[(flag, mode)] = m.gflat.clone()
+    for mode in (abi.STASH, abi.RECOMPUTE):
+        assert bits_equal(out[("0", mode)], out[("1", mode)]), mode
