@@ -160,8 +160,10 @@ template <> __device__ __forceinline__ float from_f<float>(float x) { return x; 
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
 // ------------------------------------------------------------------ math (IEEE, no fast-math)
+// 1 / (1 + e^-x): __frcp_rn is the correctly rounded reciprocal, i.e. exactly __fdiv_rn(1, .)
+// (same IEEE result) without the general-division sequence
 __device__ __forceinline__ float sigmoidf_(float x) {
-  return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+  return __frcp_rn(__fadd_rn(1.0f, expf(-x)));
 }
 
 // warp-wide sum with a fixed xor tree (deterministic, identical in every kernel)

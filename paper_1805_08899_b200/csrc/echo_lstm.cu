@@ -30,6 +30,18 @@ __device__ __forceinline__ float tanh_c(float c) { return St<T>::round(tanhf(c))
 template <typename T>
 __device__ __forceinline__ float hidden(float o, float tc) { return St<T>::round(__fmul_rn(o, tc)); }
 
+// per-step kernels (a1 / a3) at small B*H are latency-bound: spread the threads over more SMs
+// with smaller blocks (64 threads when there are fewer than 148 x 128 threads); ECHO_LSTM_BLOCK
+// overrides (A/B measurements)
+static int step_block(long threads) {
+  static const int forced = [] {
+    const char* e = getenv("ECHO_LSTM_BLOCK");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 32 || forced == 64 || forced == 128) return forced;
+  return threads >= 148L * 128 ? 128 : 64;
+}
+
 static int grid_for(long threads, int block) {
   long g = (threads + block - 1) / block;
   const long cap = 148L * 16;
@@ -433,13 +445,14 @@ extern "C" echo_status echo_lstm_fwd(const echo_lstm_desc* d, const void* gx_t, 
   if (c_out == c_prev) return fail(ECHO_ERR_INVALID, "%s: c_out must not alias c_prev", fn);
   cudaStream_t st = (cudaStream_t)stream;
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
-  const int grid = grid_for((long)d->B * d->H / V, 128);
+  const int blk = step_block((long)d->B * d->H / V);
+  const int grid = grid_for((long)d->B * d->H / V, blk);
   cudaError_t e_;
   if (d->dtype == ECHO_FP32)
-    e_ = launch(lstm_fwd_kernel<float>, dim3(grid), dim3(128), 0, st, 1, d->B, d->H, (const float*)gx_t,
+    e_ = launch(lstm_fwd_kernel<float>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H, (const float*)gx_t,
                 (const float*)gh_t, bias, c_prev, (float*)gates_t, c_out, (float*)tc_t, (float*)h_out);
   else
-    e_ = launch(lstm_fwd_kernel<__nv_bfloat16>, dim3(grid), dim3(128), 0, st, 1, d->B, d->H,
+    e_ = launch(lstm_fwd_kernel<__nv_bfloat16>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H,
                 (const __nv_bfloat16*)gx_t, (const __nv_bfloat16*)gh_t, bias, c_prev, (__nv_bfloat16*)gates_t, c_out,
                 (__nv_bfloat16*)tc_t, (__nv_bfloat16*)h_out);
   if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
@@ -492,13 +505,14 @@ extern "C" echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int V = d->dtype == ECHO_FP32 ? 4 : 8;
-  const int grid = grid_for((long)d->B * d->H / V, 128);
+  const int blk = step_block((long)d->B * d->H / V);
+  const int grid = grid_for((long)d->B * d->H / V, blk);
   cudaError_t e_;
   if (d->dtype == ECHO_FP32)
-    e_ = launch(lstm_bwd_kernel<float>, dim3(grid), dim3(128), 0, st, 1, d->B, d->H, (const float*)gates_t, c_prev,
+    e_ = launch(lstm_bwd_kernel<float>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H, (const float*)gates_t, c_prev,
                 c_t, (const float*)tc_t, dh_t, dc, (float*)dA_t, (float*)h_regen);
   else
-    e_ = launch(lstm_bwd_kernel<__nv_bfloat16>, dim3(grid), dim3(128), 0, st, 1, d->B, d->H,
+    e_ = launch(lstm_bwd_kernel<__nv_bfloat16>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H,
                 (const __nv_bfloat16*)gates_t, c_prev, c_t, (const __nv_bfloat16*)tc_t, dh_t, dc, (__nv_bfloat16*)dA_t,
                 (__nv_bfloat16*)h_regen);
   if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
