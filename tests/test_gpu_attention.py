@@ -53,7 +53,9 @@ def _run_attn(abi, d, storage, mode, layout):
 
 @pytest.mark.parametrize("storage", ["fp32", "bf16"])
 @pytest.mark.parametrize("B,Ts,A,Hk,layout", [(2, 4, 16, 16, "bsk"), (5, 37, 64, 48, "bsk"), (7, 29, 40, 88, "sbk"),
-                                               (128, 50, 512, 512, "sbk"), (3, 700, 256, 64, "bsk")])
+                                               (128, 50, 512, 512, "sbk"), (3, 700, 256, 64, "bsk"),
+                                               (1, 1, 8, 8, "bsk"), (2, 256, 64, 32, "sbk"), (2, 257, 64, 32, "sbk"),
+                                               (3, 13, 1024, 1024, "sbk"), (4, 9, 24, 1000, "bsk")])
 def test_attention_parity_and_bit_identity(storage, B, Ts, A, Hk, layout, cuda_dev):
     abi = _abi()
     d = mlp_attn_inputs(31, B, Ts, A, Hk, storage, lengths="random")
@@ -167,3 +169,57 @@ def test_attention_deferred_bitwise(storage, B, Ts, A, Hk, Td, cuda_dev):
         for k, (x, y) in enumerate(zip(res[False], res[True])):
             if x is not None:
                 assert bits_equal(x, y), (mode, k)
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+def test_attention_c5_launch_sampled_rows(storage, cuda_dev):
+    """C5's launch configuration (B = 24576 rows, Ts = 50, A = Hk = 512: the shape bench.py's C5
+    leg times) on sampled rows the oracle computes one by one; every row's softmax sums to one."""
+    abi = _abi()
+    B, Ts, A, Hk = 24576, 50, 512, 512
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    sd = torch.float32 if storage == "fp32" else torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Kp = (torch.randn(Ts, B, A, device="cuda", generator=g) * 0.5).to(sd)
+    Hs = torch.randn(Ts, B, Hk, device="cuda", generator=g).to(sd)
+    qp = (torch.randn(B, A, device="cuda", generator=g) * 0.5).to(sd)
+    v = (torch.randn(A, device="cuda", generator=g) * 0.2).to(sd)
+    sl = torch.randint(1, Ts + 1, (B,), device="cuda", generator=g).to(torch.int32)
+    dctx = torch.randn(B, Hk, device="cuda", generator=g)
+    desc = abi.AttnDesc(B, Ts, A, Hk, dt, abi.STASH, A, B * A, Hk, B * Hk)
+    ctx = torch.empty(B, Hk, device="cuda", dtype=sd)
+    Z = torch.empty(B, Ts, A, device="cuda", dtype=sd)
+    al = torch.empty(B, Ts, device="cuda")
+    abi.echo_attn_fwd(desc, qp, Kp, v, Hs, sl, ctx, Z, al)
+    dqp = torch.empty(B, A, device="cuda")
+    dKp = torch.zeros(Ts, B, A, device="cuda")
+    dHs = torch.zeros(Ts, B, Hk, device="cuda")
+    dvp = torch.zeros(B, A, device="cuda")
+    abi.echo_attn_bwd(desc, None, None, v, Hs, sl, Z, al, dctx, dqp, dKp, dHs, dvp, None)
+    torch.cuda.synchronize()
+    rows = al.sum(1)
+    assert torch.allclose(rows, torch.ones_like(rows), atol=1e-5)
+    for b in (0, 1, 4097, 12345, B - 1):
+        n = int(sl[b])
+        f64 = lambda x: x.double().cpu().numpy()
+        ref = OA.backward(f64(qp[b:b + 1]), f64(Kp[:, b:b + 1].transpose(0, 1)), f64(v),
+                          f64(Hs[:, b:b + 1].transpose(0, 1)), f64(dctx[b:b + 1]), src_len=np.array([n], np.int32))
+        assert_close(host(ctx[b:b + 1]), ref["ctx"], storage, f"ctx[{b}]")
+        assert_close(host(dqp[b:b + 1]), ref["dqp"], storage, f"dqp[{b}]")
+        assert_close(host(dKp[:, b:b + 1].transpose(0, 1)), ref["dKp"], storage, f"dKp[{b}]")
+        assert_close(host(dHs[:, b:b + 1].transpose(0, 1)), ref["dHs"], storage, f"dHs[{b}]")
+        assert_close(host(dvp[b]), ref["dv"], storage, f"dv[{b}]")
+
+
+def test_attention_rejects_bad_arguments(cuda_dev):
+    """Empty / misaligned / mode-inconsistent calls fail with ECHO_ERR_INVALID before any launch."""
+    abi = _abi()
+    x = torch.zeros(64, device="cuda")
+    for desc in (abi.AttnDesc(0, 4, 16, 16, abi.FP32, abi.RECOMPUTE, 16, 0, 16, 0),
+                 abi.AttnDesc(2, 4, 12, 16, abi.FP32, abi.RECOMPUTE, 12, 48, 16, 64)):
+        with pytest.raises(abi.EchoError) as ei:
+            abi.echo_attn_fwd(desc, x, x, x, x, None, x, None, None)
+        assert ei.value.status == 1
+    desc = abi.AttnDesc(2, 4, 16, 16, abi.FP32, abi.RECOMPUTE, 16, 64, 16, 64)
+    with pytest.raises(abi.EchoError):                        # RECOMPUTE must not get a stash buffer
+        abi.echo_attn_fwd(desc, x, x, x, x, None, x, x, x)

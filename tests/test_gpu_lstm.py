@@ -27,9 +27,10 @@ def _abi():
 
 @pytest.mark.parametrize("storage", STORAGES)
 @pytest.mark.parametrize("mode", ["stash", "recompute"])
-@pytest.mark.parametrize("B,H", [(3, 16), (5, 40), (128, 512)])
+@pytest.mark.parametrize("B,H", [(3, 16), (5, 40), (128, 512), (24576, 512)])
 def test_cell_fwd_bwd_step(storage, mode, B, H, cuda_dev):
-    """a1 + a3 on one step vs oracle cell_forward / cell_backward (A given)."""
+    """a1 + a3 on one step vs oracle cell_forward / cell_backward (A given); B = 24576 is C5's
+    per-step launch configuration (every row compared)."""
     abi = _abi()
     d = lstm_cell_inputs(11, B, H, storage)
     m = abi.STASH if mode == "stash" else abi.RECOMPUTE
