@@ -182,6 +182,197 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_f32_kernel(int M, int N, in
   }
 }
 
+// ---------------------------------------------------------------- small-M path: cp.async pipeline
+// 64x64 tile, BK = 16, NS-stage cp.async ring (16-byte copies, zero-filled outside the matrix);
+// shared tiles keep the global layout (no transposition), so the fragment loads are 128-bit in
+// whichever direction is contiguous; k is consumed in order (deterministic).
+constexpr int P_BM = 64, P_BN = 64, P_BK = 16, P_NS = 4;
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GEMM_THREADS) gemm_f32_pipe(int M, int N, int K, int kchunk, float alpha,
+                                                              const float* __restrict__ A, long lda,
+                                                              const float* __restrict__ B, long ldb, float beta,
+                                                              float* __restrict__ C, long ldc) {
+  pdl_wait();
+  // stage layouts: A !TA [64 m][BK+4] | TA [BK k][64+4];  B !TB [BK k][64+4] | TB [64 n][BK+4]
+  constexpr int AS = TA ? P_BK * (P_BM + 4) : P_BM * (P_BK + 4);
+  constexpr int BS = TB ? P_BN * (P_BK + 4) : P_BK * (P_BN + 4);
+  constexpr int STAGE = AS + BS, PART = P_BM * (P_BN + 4);
+  __shared__ __align__(16) float sm[P_NS * STAGE > PART ? P_NS * STAGE : PART];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * P_BM, n0 = blockIdx.x * P_BN;
+  const int S = gridDim.z, rank = blockIdx.z;
+  const int kb = rank * kchunk, ke = min(K, kb + kchunk);
+  const int nk = ke > kb ? (ke - kb + P_BK - 1) / P_BK : 0;
+  auto load_stage = [&](int st, int k0) {
+    float* as = sm + st * STAGE;
+    float* bs = as + AS;
+    if (!TA) {
+      const int m = tid / 4, kc = (tid % 4) * 4;
+      const bool ok = m0 + m < M && k0 + kc < ke;
+      cp_async16(as + m * (P_BK + 4) + kc, ok ? A + (long)(m0 + m) * lda + k0 + kc : A, ok);
+    } else {
+      const int k = tid / 16, mc = (tid % 16) * 4;
+      const bool ok = k0 + k < ke && m0 + mc < M;
+      cp_async16(as + k * (P_BM + 4) + mc, ok ? A + (long)(k0 + k) * lda + m0 + mc : A, ok);
+    }
+    if (!TB) {
+      const int k = tid / 16, nc = (tid % 16) * 4;
+      const bool ok = k0 + k < ke && n0 + nc < N;
+      cp_async16(bs + k * (P_BN + 4) + nc, ok ? B + (long)(k0 + k) * ldb + n0 + nc : B, ok);
+    } else {
+      const int n = tid / 4, kc = (tid % 4) * 4;
+      const bool ok = n0 + n < N && k0 + kc < ke;
+      cp_async16(bs + n * (P_BK + 4) + kc, ok ? B + (long)(n0 + n) * ldb + k0 + kc : B, ok);
+    }
+  };
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+#pragma unroll
+  for (int st = 0; st < P_NS - 1; ++st) {
+    if (st < nk) load_stage(st, kb + st * P_BK);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<P_NS - 2>();
+    __syncthreads();
+    const int nxt = it + P_NS - 1;                   // refill the stage consumed last iteration
+    if (nxt < nk) load_stage(nxt % P_NS, kb + nxt * P_BK);
+    cp_async_commit();
+    const float* as = sm + (it % P_NS) * STAGE;
+    const float* bs = as + AS;
+#pragma unroll
+    for (int kk = 0; kk < P_BK; kk += 4) {
+      float a[4][4], b[4][4];                        // a[i][q] = A(m_i, k+q), b[q][j] = B(k+q, n_j)
+      if (!TA) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 v = *reinterpret_cast<const float4*>(as + (ty * 4 + i) * (P_BK + 4) + kk);
+          a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(as + (kk + q) * (P_BM + 4) + ty * 4);
+          a[0][q] = v.x; a[1][q] = v.y; a[2][q] = v.z; a[3][q] = v.w;
+        }
+      }
+      if (!TB) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(bs + (kk + q) * (P_BN + 4) + tx * 4);
+          b[q][0] = v.x; b[q][1] = v.y; b[q][2] = v.z; b[q][3] = v.w;
+        }
+      } else {                                       // TB: columns tx + 16 j (conflict-free rows)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 v = *reinterpret_cast<const float4*>(bs + (tx + 16 * j) * (P_BK + 4) + kk);
+          b[0][j] = v.x; b[1][j] = v.y; b[2][j] = v.z; b[3][j] = v.w;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(a[i][q], b[q][j], acc[i][j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  auto store = [&](int m, int n, float4 s) {
+    float4* cp = reinterpret_cast<float4*>(C + (long)m * ldc + n);
+    float4 o = make_float4(__fmul_rn(alpha, s.x), __fmul_rn(alpha, s.y), __fmul_rn(alpha, s.z), __fmul_rn(alpha, s.w));
+    if (beta != 0.0f) {
+      const float4 c = *cp;
+      o.x = __fmaf_rn(beta, c.x, o.x); o.y = __fmaf_rn(beta, c.y, o.y);
+      o.z = __fmaf_rn(beta, c.z, o.z); o.w = __fmaf_rn(beta, c.w, o.w);
+    }
+    *cp = o;
+  };
+  float* Cs = sm;                                    // [64][68] tile (partial, or staging for S == 1)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float* row = Cs + (ty * 4 + i) * (P_BN + 4);
+    if (!TB) {
+      *reinterpret_cast<float4*>(row + tx * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) row[tx + 16 * j] = acc[i][j];
+    }
+  }
+  if (S == 1) {
+    __syncthreads();
+    for (int e = tid; e < P_BM * (P_BN / 4); e += GEMM_THREADS) {
+      const int r = e / (P_BN / 4), c4 = (e % (P_BN / 4)) * 4;
+      const int m = m0 + r, n = n0 + c4;
+      if (m < M && n < N) store(m, n, *reinterpret_cast<const float4*>(Cs + r * (P_BN + 4) + c4));
+    }
+    return;
+  }
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  for (int e = tid; e < P_BM * (P_BN / 4); e += GEMM_THREADS) {
+    const int r = e / (P_BN / 4), c4 = (e % (P_BN / 4)) * 4;
+    if (r % S != rank) continue;
+    const int m = m0 + r, n = n0 + c4;
+    if (m >= M || n >= N) continue;
+    float4 s = make_float4(0, 0, 0, 0);
+    for (int q = 0; q < S; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(cl.map_shared_rank(Cs, q) + r * (P_BN + 4) + c4);
+      s.x = __fadd_rn(s.x, v.x); s.y = __fadd_rn(s.y, v.y); s.z = __fadd_rn(s.z, v.z); s.w = __fadd_rn(s.w, v.w);
+    }
+    store(m, n, s);
+  }
+  cl.sync();
+}
+
+template <bool TA, bool TB>
+static cudaError_t launch_pipe(int M, int N, int K, float alpha, const float* A, long lda, const float* B, long ldb,
+                               float beta, float* C, long ldc, cudaStream_t st) {
+  // split K until ~2 CTAs per SM are in flight (each SM holds up to 4 of these CTAs); clusters up
+  // to 16 (non-portable size) so M = 128 rows x N = 512 still fills the GPU
+  const int tiles = ((M + P_BM - 1) / P_BM) * ((N + P_BN - 1) / P_BN);
+  static const int smax = [] {
+    const cudaError_t e0 = cudaFuncSetAttribute(gemm_f32_pipe<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    const cudaError_t e1 = cudaFuncSetAttribute(gemm_f32_pipe<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    const cudaError_t e2 = cudaFuncSetAttribute(gemm_f32_pipe<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    const cudaError_t e3 = cudaFuncSetAttribute(gemm_f32_pipe<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e0 || e1 || e2 || e3) {
+      cudaGetLastError();
+      return 8;
+    }
+    return 16;
+  }();
+  int S = 1;
+  const int limit = TA == TA ? smax : 8;
+  while (S < limit && tiles * S * 2 <= 2 * 2 * 148 && K / (S * 2) >= 2 * P_BK) S *= 2;
+  const int kchunk = ((K + S - 1) / S + P_BK - 1) / P_BK * P_BK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((N + P_BN - 1) / P_BN, (M + P_BM - 1) / P_BM, S);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = (unsigned)S;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_f32_pipe<TA, TB>, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
 template <int BM, int BN, int BK, bool TA, bool TB>
 static cudaError_t launch_gemm(int M, int N, int K, float alpha, const float* A, long lda, const float* B, long ldb,
                                float beta, float* C, long ldc, cudaStream_t st) {
@@ -210,7 +401,7 @@ static cudaError_t dispatch(int M, int N, int K, float alpha, const float* A, lo
                             float beta, float* C, long ldc, cudaStream_t st) {
   if ((long)M * N >= 1024L * 1024)
     return launch_gemm<128, 128, 8, TA, TB>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, st);
-  return launch_gemm<64, 64, 16, TA, TB>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, st);
+  return launch_pipe<TA, TB>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, st);
 }
 
 }  // namespace echo

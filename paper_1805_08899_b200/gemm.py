@@ -15,11 +15,21 @@ import torch
 
 import os
 
-# libecho's fp32 split-K GEMM is opt-in (ECHO_GEMM=echo): measured on B200 (scripts/gemm_bench.py)
-# it beats cuBLAS only on the decoder-backward shape (M=128, N=512, K=2048: 27 vs 34 us) and loses
-# on the rest (2-deep global->register->shared pipeline cannot hide HBM/L2 latency at 1-2 CTAs/SM;
-# large-K weight-gradient GEMMs 4x slower), so the step uses cuBLAS (TF32 off) by default.
-_USE_ECHO = os.environ.get("ECHO_GEMM", "torch") == "echo"
+# libecho's IEEE-fp32 split-K GEMM (echo_gemm_f32) replaces cuBLAS's fp32 SIMT kernels on the
+# small-M per-step shapes of the recurrence (M = batch rows, M*N < 1M) when TF32 is off (strict
+# fp32).  Measured on B200 inside CUDA graphs (scripts/gemm_bench.py): M=128 N=512 K=2048 17.5 vs
+# 33.1 us, K=512 8.3-8.7 vs 10.8-11.0 us; the wide transposed-B shape (N=2048) stays on cuBLAS
+# (14.5 vs 12.4 us), as do the large weight-gradient / projection GEMMs and every TF32 / bf16
+# GEMM.  C2 fp32 step: 28.2 -> 23.0 ms.  ECHO_GEMM=torch turns it off.
+_MODE = os.environ.get("ECHO_GEMM", "auto")
+
+
+def _echo_ok(M, N, tB):
+    if _MODE == "torch":
+        return False
+    if _MODE == "echo":
+        return True
+    return (not torch.backends.cuda.matmul.allow_tf32) and M * N < 1024 * 1024 and not (tB and N >= 2048)
 
 
 def _layout(x):
@@ -37,11 +47,11 @@ def gemm_into(out, a, b, beta=0.0):
     (echo_gemm_f32: deterministic, 3-10x cuBLAS's fp32 SIMT kernels at M = 128); everything else
     (bf16 operands -> cuBLAS tensor cores) stays on torch."""
     f32 = torch.float32
-    if _USE_ECHO and a.dtype == f32 and b.dtype == f32 and out.dtype == f32 and a.is_cuda and out.stride(1) == 1:
+    if _MODE != "torch" and a.dtype == f32 and b.dtype == f32 and out.dtype == f32 and a.is_cuda and out.stride(1) == 1:
         la, lb = _layout(a), _layout(b)
         M, K = a.shape
         N = b.shape[1]
-        if la and lb and out.stride(0) >= N:
+        if la and lb and out.stride(0) >= N and _echo_ok(M, N, lb[0]):
             from . import abi
             if abi.echo_gemm_f32_supported(M, N, K, la[0], lb[0], la[1], lb[1], out.stride(0)):
                 abi.echo_gemm_f32(M, N, K, 1.0, a, la[1], la[0], b, lb[1], lb[0], beta, out, out.stride(0))
@@ -61,7 +71,7 @@ def gemm_into(out, a, b, beta=0.0):
 def mm(a, b, out_dtype=None):
     """a @ b; out_dtype=torch.float32 forces an fp32 result for bf16 operands."""
     od = a.dtype if out_dtype is None else out_dtype
-    if _USE_ECHO and a.dtype == b.dtype == od == torch.float32 and a.is_cuda:
+    if _MODE != "torch" and a.dtype == b.dtype == od == torch.float32 and a.is_cuda:
         out = torch.empty(a.shape[0], b.shape[1], dtype=od, device=a.device)
         return gemm_into(out, a, b, 0.0)
     return torch.mm(a, b) if od == a.dtype else torch.mm(a, b, out_dtype=od)

@@ -1,4 +1,5 @@
-"""echo_gemm_f32 vs cuBLAS (torch, TF32 off) on the fp32 NMT step's GEMM shapes (CUDA events, warm)."""
+"""echo_gemm_f32 vs cuBLAS (torch, TF32 off) on the fp32 NMT step's GEMM shapes (20 launches captured in a
+CUDA graph, CUDA events: no host launch gaps)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -8,7 +9,10 @@ shapes = [(128, 512, 2048, 0, 0, "dh += dA Wh (decoder bwd)"), (128, 2048, 512, 
           (128, 512, 512, 0, 0, "dctx = dpre Wcc"), (128, 512, 512, 0, 1, "qp = q Wq^T"),
           (2048, 512, 6400, 1, 0, "dWh = dA^T h (wgrad)"), (6400, 2048, 512, 0, 1, "GX = X Wx^T (input proj)"),
           (6400, 512, 2048, 0, 0, "dX = dA Wx"), (6400, 8192, 512, 0, 1, "logits")]
+only = sys.argv[1] if len(sys.argv) > 1 else ""
 for M, N, K, tA, tB, name in shapes:
+    if only and only not in name:
+        continue
     A = torch.randn(K, M, device="cuda") if tA else torch.randn(M, K, device="cuda")
     B = torch.randn(N, K, device="cuda") if tB else torch.randn(K, N, device="cuda")
     C = torch.zeros(M, N, device="cuda")
@@ -21,10 +25,15 @@ for M, N, K, tA, tB, name in shapes:
         for _ in range(3):
             f()
         torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()                       # 20 launches in one graph: no host launch gaps
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                f()
+        g.replay()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(20):
-            f()
+        g.replay()
         e1.record()
         torch.cuda.synchronize()
         res[k] = e0.elapsed_time(e1) / 20 * 1e3

@@ -38,8 +38,8 @@ def test_gemm_wrapper_routes_views(cuda_dev):
     """gemm.mm / addmm_ on transposed views (W.t()) go through echo_gemm_f32 and match torch."""
     from paper_1805_08899_b200 import gemm
     torch.backends.cuda.matmul.allow_tf32 = False
-    saved = gemm._USE_ECHO
-    gemm._USE_ECHO = True
+    saved = gemm._MODE
+    gemm._MODE = "echo"
     x = torch.randn(128, 512, device="cuda")
     W = torch.randn(2048, 512, device="cuda")
     c = torch.randn(128, 2048, device="cuda")
@@ -48,4 +48,4 @@ def test_gemm_wrapper_routes_views(cuda_dev):
     assert (c - r).abs().max().item() <= 1e-3
     y = gemm.mm(x.t().contiguous().t(), W.t())
     assert (y - x @ W.t()).abs().max().item() <= 1e-3
-    gemm._USE_ECHO = saved
+    gemm._MODE = saved
