@@ -202,7 +202,7 @@ def time_attn_bwd(cfg, dtype, reps=20):
     return {"ms": ms, "bytes": nbytes, "bytes_per_row": nbytes / rows, "rows": rows}
 
 
-def extra_leg(name, dtype_s, steps=5, warmup=3):
+def extra_leg(name, dtype_s, steps=10, warmup=3):
     """Secondary configs (BASELINE.json configs[2..4]): device-timed steps of both modes (CUDA graph),
     exact stash bytes and allocator peak per mode.  C5 = C2 shapes at a per-GPU batch where STASH
     runs out of HBM and RECOMPUTE fits (the OOM is caught and reported)."""
