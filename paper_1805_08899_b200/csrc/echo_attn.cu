@@ -18,6 +18,7 @@
 // the forward and backward kernels, which makes the regenerated alpha / ctx
 // bit-identical to the stashed ones.
 #include <cmath>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 #include <cuda.h>
@@ -490,6 +491,8 @@ static __host__ __device__ __forceinline__ int tma_width(int X, int C) { return 
 // launch geometry computed once on the host (no integer divisions per CTA)
 struct TmaGeo {
   int C, Wb, WHb, R, Tr, P;   // cluster size, box widths, chunk rows, tile rows, phase-4 phases
+  int pf;                     // a6 dKp / dH_s L2 prefetch: 0 off, 1 after the stage-in landed, 2 at issue
+  int l2last;                 // 1: Kp / H_s / dKp / dH_s traffic carries an L2 evict_last policy
 };
 __device__ __forceinline__ Slice make_slice_g(const TmaGeo& q, int A, int Hk, int r) {
   Slice g;
@@ -620,6 +623,34 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 eviction policies: the attention tensors every decoder step re-reads (Kp, H_s) and
+// read-modify-writes (dKp, dH_s) can be marked evict_last so they stay resident across steps
+__device__ __forceinline__ uint64_t l2_policy(bool last) {
+  uint64_t p;
+  if (last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg4_hint(float* p, const float (&v)[4], uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(p), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map), "r"(c0),
                "r"(c1), "r"(c2), "r"(smem_u32(src))
@@ -635,9 +666,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(map), "r"(c0), "r"(c1),
-               "r"(c2)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile.L2::cache_hint [%0, {%1, %2, %3}], %4;\n" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "l"(pol)
                : "memory");
 }
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
@@ -672,18 +703,24 @@ struct SmallCopy {     // contiguous vectors staged with chunk 0 (qp / v / dctx 
 };
 __device__ __forceinline__ void issue_chunks(uint64_t* bar, int n, int R, void* kz, const CUtensorMap* mK, int a0,
                                              void* hs, const CUtensorMap* mH, int h0, int b, uint32_t rowK,
-                                             uint32_t rowH, const SmallCopy& sm) {
-  const int nch = (n + R - 1) / R;
-  // one arrive.expect_tx per barrier (count 1): chunk 0's also covers the small vectors
+                                             uint32_t rowH, const SmallCopy& sm, uint64_t pol) {
+  // one arrive.expect_tx per barrier (count 1): chunk 0's also covers the small vectors.  Chunk 0
+  // (always needed: n >= 1) goes out before n is used, so the src_len load overlaps its issue.
   mbar_expect_tx(&bar[0], sm.bytes[0] + sm.bytes[1] + sm.bytes[2] + (uint32_t)R * (rowK + rowH));
+  tma_load_3d_hint(kz, mK, a0, b, 0, &bar[0], pol);
+  tma_load_3d_hint(hs, mH, h0, b, 0, &bar[0], pol);
 #pragma unroll
   for (int i = 0; i < 3; ++i)
     if (sm.bytes[i]) bulk_load(sm.dst[i], sm.src[i], sm.bytes[i], &bar[0]);
-  for (int k = 0; k < nch; ++k) {
-    if (k > 0) mbar_expect_tx(&bar[k], (uint32_t)R * (rowK + rowH));
-    tma_load_3d(static_cast<unsigned char*>(kz) + (size_t)k * R * rowK, mK, a0, b, k * R, &bar[k]);
-    tma_load_3d(static_cast<unsigned char*>(hs) + (size_t)k * R * rowH, mH, h0, b, k * R, &bar[k]);
+  const int nch = (n + R - 1) / R;
+  for (int k = 1; k < nch; ++k) {
+    mbar_expect_tx(&bar[k], (uint32_t)R * (rowK + rowH));
+    tma_load_3d_hint(static_cast<unsigned char*>(kz) + (size_t)k * R * rowK, mK, a0, b, k * R, &bar[k], pol);
+    tma_load_3d_hint(static_cast<unsigned char*>(hs) + (size_t)k * R * rowH, mH, h0, b, k * R, &bar[k], pol);
   }
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(m) : "memory");
 }
 
 // Shared-memory tiles: [Tr][box width] per tensor for this CTA's column slice.
@@ -714,12 +751,15 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
   float* al = sc + Tp;
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
+  const uint64_t pol = l2_policy(q.l2last);
   if (tid == 0) {
+    prefetch_tmap(&mK);
+    prefetch_tmap(&mH);
     for (int k = 0; k < TMA_CHUNKS; ++k) mbar_init(&bar[k], 1);
     fence_mbar_init();
     SmallCopy sm{{qps, vs, nullptr}, {qp + (long)b * A + g.a0, v + g.a0, nullptr},
                  {(uint32_t)(W * sizeof(T)), (uint32_t)(W * sizeof(T)), 0u}};
-    issue_chunks(bar, n, R, kz, &mK, g.a0, hs, &mH, g.h0, b, Wb * sizeof(T), WHb * sizeof(T), sm);
+    issue_chunks(bar, n, R, kz, &mK, g.a0, hs, &mH, g.h0, b, Wb * sizeof(T), WHb * sizeof(T), sm, pol);
   }
   __syncthreads();                                            // barrier init visible before anyone waits
   mbar_wait(&bar[0], 0);                                      // chunk 0 + the qp / v slices
@@ -804,13 +844,23 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   float* red = Tr >= 2 * P ? E : dsv + Tp;
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
+  const uint64_t pol = l2_policy(q.l2last);
   ECHO_PHASE(0);
   if (tid == 0) {
+    prefetch_tmap(&mK);
+    prefetch_tmap(&mH);
     for (int k = 0; k < TMA_CHUNKS; ++k) mbar_init(&bar[k], 1);
     fence_mbar_init();
+    ECHO_PHASE(11);
     SmallCopy sm{{qps, vs, dcs}, {qp + (long)b * A + g.a0, v + g.a0, dctx + (long)b * Hk + g.h0},
                  {recompute ? (uint32_t)(W * sizeof(T)) : 0u, (uint32_t)(W * sizeof(T)), (uint32_t)WH * 4u}};
-    issue_chunks(bar, n, R, kz, &mK, g.a0, hs, &mH, g.h0, b, Wb * sizeof(T), WHb * sizeof(T), sm);
+    issue_chunks(bar, n, R, kz, &mK, g.a0, hs, &mH, g.h0, b, Wb * sizeof(T), WHb * sizeof(T), sm, pol);
+    if (dKp && q.pf == 2)                                      // dKp / dH_s into L2 behind the stage-in
+      for (int k = 0; k * R < n; ++k) {
+        if (W > 0) tma_prefetch_3d(&mdK, g.a0, b, k * R, pol);
+        if (WH > 0) tma_prefetch_3d(&mdH, g.h0, b, k * R, pol);
+      }
+    ECHO_PHASE(12);
   }
   // values only the epilogue / softmax need are fetched now so their latency hides under the
   // staging wait (W <= 128 < ATT_THREADS: one column per thread, see tma_cluster)
@@ -845,15 +895,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   }
   // L2 prefetch of the dKp / dH_s tiles phase 4 streams, issued by thread 0 once this CTA's loads
   // have landed so the reads overlap the exchange / softmax phases instead of phase 4
-#ifndef ECHO_A6_NO_PREFETCH
-  if (tid == 0 && dKp) {
+  if (tid == 0 && dKp && q.pf == 1) {
     for (int k = 0; k * R < n; ++k) mbar_wait(&bar[k], 0);
     for (int k = 0; k * R < n; ++k) {
-      if (W > 0) tma_prefetch_3d(&mdK, g.a0, b, k * R);
-      if (WH > 0) tma_prefetch_3d(&mdH, g.h0, b, k * R);
+      if (W > 0) tma_prefetch_3d(&mdK, g.a0, b, k * R, pol);
+      if (WH > 0) tma_prefetch_3d(&mdH, g.h0, b, k * R, pol);
     }
   }
-#endif
   ECHO_PHASE(3);
   cl.sync();
   ECHO_PHASE(4);
@@ -897,7 +945,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int s = s0 + u * P;
-        if (s < n && dKp) x[u] = *reinterpret_cast<const float4*>(base + (long)s * d.kp_stride_s);
+        if (s < n && dKp) x[u] = ldg4_hint(base + (long)s * d.kp_stride_s, pol);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -913,7 +961,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
             dq[k] = __fadd_rn(dq[k], dE);
             dvv[k] = __fmaf_rn(ds, e[k], dvv[k]);
           }
-          if (dKp) stg4(base + (long)s * d.kp_stride_s, xv);
+          if (dKp) stg4_hint(base + (long)s * d.kp_stride_s, xv, pol);
         }
       }
     }
@@ -927,7 +975,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int s = s0 + u * P;
-        if (s < n) x[u] = *reinterpret_cast<const float4*>(base + (long)s * d.hs_stride_s);
+        if (s < n) x[u] = ldg4_hint(base + (long)s * d.hs_stride_s, pol);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -936,7 +984,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
           const float a = al[s];
           float xv[4] = {__fmaf_rn(a, dc[0], x[u].x), __fmaf_rn(a, dc[1], x[u].y), __fmaf_rn(a, dc[2], x[u].z),
                          __fmaf_rn(a, dc[3], x[u].w)};
-          stg4(base + (long)s * d.hs_stride_s, xv);
+          stg4_hint(base + (long)s * d.hs_stride_s, xv, pol);
         }
       }
     }
@@ -1069,6 +1117,24 @@ static size_t bwd_smem(const echo_attn_desc* d) {
                           2 * (size_t)ATT_WARPS * d->A + 2 * (size_t)d->A + (size_t)G * d->Hk + d->Hk);
 }
 
+// a6 L2 prefetch of the dKp / dH_s tiles (ECHO_A6_PREFETCH=0|1|2, read once; see TmaGeo::pf)
+static int a6_prefetch_mode() {
+  static const int m = [] {
+    const char* e = getenv("ECHO_A6_PREFETCH");
+    return e && *e >= '0' && *e <= '2' ? *e - '0' : 1;
+  }();
+  return m;
+}
+
+// ECHO_ATTN_L2LAST=1: evict_last policy on the per-step attention tensors (see l2_policy)
+static int attn_l2_last() {
+  static const int m = [] {
+    const char* e = getenv("ECHO_ATTN_L2LAST");
+    return e && *e == '1' ? 1 : 0;
+  }();
+  return m;
+}
+
 // TMA path: cluster size and shared-memory footprint; returns false if the generic path must run
 static size_t al128h(size_t b) { return (b + 127) & ~(size_t)127; }
 static bool tma_params(const echo_attn_desc* d, int* C, int* rows, size_t* smem_fwd, size_t* smem_bwd,
@@ -1093,6 +1159,8 @@ static bool tma_params(const echo_attn_desc* d, int* C, int* rows, size_t* smem_
   geo->R = R;
   geo->Tr = (int)Ts;
   geo->P = (int)P;
+  geo->pf = a6_prefetch_mode();
+  geo->l2last = attn_l2_last();
   *smem_fwd = fwd;
   *smem_bwd = bwd;
   return true;

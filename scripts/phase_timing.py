@@ -31,6 +31,7 @@ names = ["start->issued", "issued->tma_done", "tma_done->phase1_end", "phase1->c
 for k in range(10):
     dd = t[k + 1] - t[k]
     print(f"{names[k]:24s} mean {dd.mean():8.0f} cyc  p50 {np.median(dd):8.0f}  max {dd.max():8.0f}")
+print("start->barriers_init    mean", (t[11]-t[0]).mean(), " start->all_issued mean", (t[12]-t[0]).mean())
 tot = t[10] - t[0]
 print("CTA lifetime cycles mean", tot.mean(), "max", tot.max())
 gt = buf[15, :ncta].astype(np.int64); gt -= gt.min()
