@@ -42,21 +42,121 @@ static int step_block(long threads) {
   return threads >= 148L * 128 ? 128 : 64;
 }
 
+// per-step a1 / a3 vector width (elements per thread): the widest 16/8/4-byte vector that still
+// yields >= 148 x 256 threads (ECHO_LSTM_VEC=N forces N); bf16 stays >= 2 elements (4 bytes)
+static int step_vec(long elems, bool bf) {
+  static const int forced = [] {
+    const char* e = getenv("ECHO_LSTM_VEC");
+    return e ? atoi(e) : 0;
+  }();
+  const int vmax = bf ? 8 : 4, vmin = bf ? 2 : 1;
+  if (forced >= vmin && forced <= vmax && (forced & (forced - 1)) == 0) return forced;
+  int v = vmax;
+  while (v > vmin && elems / v < 148L * 256) v >>= 1;
+  return v;
+}
+
 static int grid_for(long threads, int block) {
   long g = (threads + block - 1) / block;
   const long cap = 148L * 16;
   return (int)(g < cap ? (g > 0 ? g : 1) : cap);
 }
 
+// ---------------------------------------------------------------- vectors of N elements
+// Per-step a1 / a3 launches at C2 sizes (B*H = 65536) are latency-bound: with 16-byte vectors
+// only 8192 (bf16) / 16384 (fp32) threads exist, one warp per SM sub-partition and a long
+// serial chain of transcendentals per thread.  The vector width N is therefore a template
+// parameter and the host picks the widest N that still gives >= 148 x 256 threads (down to 4
+// bytes per access); every element's arithmetic is unchanged (bit-identical results).
+template <int N> struct FV;
+template <> struct FV<1> { typedef float t; };
+template <> struct FV<2> { typedef float2 t; };
+template <> struct FV<4> { typedef float4 t; };
+template <int N>
+__device__ __forceinline__ void ldv(const float* p, float (&o)[N]) {
+  if constexpr (N == 8) {
+    ldf<8>(p, o);
+  } else {
+    const typename FV<N>::t v = *reinterpret_cast<const typename FV<N>::t*>(p);
+    const float* f = reinterpret_cast<const float*>(&v);
+#pragma unroll
+    for (int k = 0; k < N; ++k) o[k] = f[k];
+  }
+}
+template <int N>
+__device__ __forceinline__ void stv(float* p, const float (&v)[N]) {
+  if constexpr (N == 8) {
+    stf<8>(p, v);
+  } else {
+    typename FV<N>::t u;
+    float* f = reinterpret_cast<float*>(&u);
+#pragma unroll
+    for (int k = 0; k < N; ++k) f[k] = v[k];
+    *reinterpret_cast<typename FV<N>::t*>(p) = u;
+  }
+}
+template <int N> struct BV;   // N bf16 = N/2 bf16x2 words
+template <> struct BV<2> { typedef uint32_t t; };
+template <> struct BV<4> { typedef uint2 t; };
+template <> struct BV<8> { typedef uint4 t; };
+template <int N>
+__device__ __forceinline__ void ldv(const __nv_bfloat16* p, float (&o)[N]) {
+  const typename BV<N>::t v = *reinterpret_cast<const typename BV<N>::t*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x;
+    o[2 * i + 1] = f.y;
+  }
+}
+template <int N>
+__device__ __forceinline__ void stv(__nv_bfloat16* p, const float (&v)[N]) {
+  typename BV<N>::t u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<typename BV<N>::t*>(p) = u;
+}
+
+// streaming (evict-first) variants for the scan's read-once gate loads
+template <int N>
+__device__ __forceinline__ void ldv_stream(const float* p, float (&o)[N]) {
+  if constexpr (N == 8) {
+    float a[4], b[4];
+    ld16_stream(p, a);
+    ld16_stream(p + 4, b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { o[k] = a[k]; o[4 + k] = b[k]; }
+  } else {
+    const typename FV<N>::t v = __ldcs(reinterpret_cast<const typename FV<N>::t*>(p));
+    const float* f = reinterpret_cast<const float*>(&v);
+#pragma unroll
+    for (int k = 0; k < N; ++k) o[k] = f[k];
+  }
+}
+template <int N>
+__device__ __forceinline__ void ldv_stream(const __nv_bfloat16* p, float (&o)[N]) {
+  typename BV<N>::t v;
+  if constexpr (N == 2) v = __ldcs(reinterpret_cast<const unsigned int*>(p));
+  else v = __ldcs(reinterpret_cast<const typename BV<N>::t*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x;
+    o[2 * i + 1] = f.y;
+  }
+}
+
 // ---------------------------------------------------------------- a1 forward
-template <typename T>
+template <typename T, int V>
 __global__ void __launch_bounds__(128) lstm_fwd_kernel(int B, int H, const T* gx,
                                                        const T* __restrict__ gh, const float* __restrict__ bias,
                                                        const float* __restrict__ c_prev, T* gates,
                                                        float* __restrict__ c_out, T* __restrict__ tc_out,
                                                        T* __restrict__ h_out) {
   pdl_wait();
-  constexpr int V = St<T>::VEC;
   const int nvec = H / V;
   const long total = (long)B * nvec;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
@@ -65,12 +165,12 @@ __global__ void __launch_bounds__(128) lstm_fwd_kernel(int B, int H, const T* gx
     const long row4 = (long)b * 4 * H;
     float a[4][V];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) ld16(gx + row4 + g * H + j, a[g]);
+    for (int g = 0; g < 4; ++g) ldv<V>(gx + row4 + g * H + j, a[g]);
     if (gh) {
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         float t[V];
-        ld16(gh + row4 + g * H + j, t);
+        ldv<V>(gh + row4 + g * H + j, t);
 #pragma unroll
         for (int k = 0; k < V; ++k) a[g][k] = __fadd_rn(a[g][k], t[k]);
       }
@@ -79,13 +179,13 @@ __global__ void __launch_bounds__(128) lstm_fwd_kernel(int B, int H, const T* gx
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         float t[V];
-        ldf<V>(bias + g * H + j, t);
+        ldv<V>(bias + g * H + j, t);
 #pragma unroll
         for (int k = 0; k < V; ++k) a[g][k] = __fadd_rn(a[g][k], t[k]);
       }
     }
     float cp[V];
-    ldf<V>(c_prev + (long)b * H + j, cp);
+    ldv<V>(c_prev + (long)b * H + j, cp);
     float gi[V], gf[V], gg[V], go[V], c[V], tc[V], h[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) {
@@ -97,23 +197,24 @@ __global__ void __launch_bounds__(128) lstm_fwd_kernel(int B, int H, const T* gx
       tc[k] = tanh_c<T>(c[k]);
       h[k] = hidden<T>(go[k], tc[k]);
     }
-    st16(gates + row4 + 0 * H + j, gi);
-    st16(gates + row4 + 1 * H + j, gf);
-    st16(gates + row4 + 2 * H + j, gg);
-    st16(gates + row4 + 3 * H + j, go);
-    stf<V>(c_out + (long)b * H + j, c);
-    if (tc_out) st16(tc_out + (long)b * H + j, tc);
-    st16(h_out + (long)b * H + j, h);
+    stv<V>(gates + row4 + 0 * H + j, gi);
+    stv<V>(gates + row4 + 1 * H + j, gf);
+    stv<V>(gates + row4 + 2 * H + j, gg);
+    stv<V>(gates + row4 + 3 * H + j, go);
+    stv<V>(c_out + (long)b * H + j, c);
+    if (tc_out) stv<V>(tc_out + (long)b * H + j, tc);
+    stv<V>(h_out + (long)b * H + j, h);
   }
 }
 
 // ---------------------------------------------------------------- a2 c-regeneration scan
-template <typename T, int U>
+// V elements per thread, U time steps of loads in flight: the bytes in flight over the whole grid
+// are B*H*U*3s, independent of V, so small B*H launches use narrow vectors and deep U (U = 8; bf16 16-/8-byte vectors keep U = 4)
+template <typename T, int V, int U>
 __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, const T* __restrict__ gates,
                                                          const float* __restrict__ c0, float* __restrict__ cws,
                                                          T* __restrict__ hws) {
   pdl_wait();
-  constexpr int V = St<T>::VEC;
   const int nvec = H / V;
   const long total = (long)B * nvec;
   const long gstep = (long)B * 4 * H;
@@ -125,16 +226,16 @@ __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, c
     float* cp = cws + (long)b * H + j;
     T* hp = hws ? hws + (long)b * H + j : nullptr;
     float c[V];
-    ldf<V>(c0 + (long)b * H + j, c);
+    ldv<V>(c0 + (long)b * H + j, c);
     for (int t0 = 0; t0 < T_; t0 += U) {
       float gi[U][V], gf[U][V], gg[U][V];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (t0 + u < T_) {
           const T* q = gp + (long)(t0 + u) * gstep;
-          ld16_stream(q, gi[u]);
-          ld16_stream(q + H, gf[u]);
-          ld16_stream(q + 2 * H, gg[u]);
+          ldv_stream<V>(q, gi[u]);
+          ldv_stream<V>(q + H, gf[u]);
+          ldv_stream<V>(q + 2 * H, gg[u]);
         }
       }
 #pragma unroll
@@ -142,13 +243,13 @@ __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, c
         if (t0 + u < T_) {
 #pragma unroll
           for (int k = 0; k < V; ++k) c[k] = cell_update(gf[u][k], c[k], gi[u][k], gg[u][k]);
-          stf<V>(cp + (long)(t0 + u) * cstep, c);
+          stv<V>(cp + (long)(t0 + u) * cstep, c);
           if (hp) {                                         // mirrored outputs: h_t = o * tanh(c_t)
             float go[V], h[V];
-            ld16_stream(gp + (long)(t0 + u) * gstep + 3 * H, go);
+            ldv_stream<V>(gp + (long)(t0 + u) * gstep + 3 * H, go);
 #pragma unroll
             for (int k = 0; k < V; ++k) h[k] = hidden<T>(go[k], tanh_c<T>(c[k]));
-            st16(hp + (long)(t0 + u) * cstep, h);
+            stv<V>(hp + (long)(t0 + u) * cstep, h);
           }
         }
       }
@@ -156,15 +257,17 @@ __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, c
   }
 }
 
-// ---------------------------------------------------------------- a3 backward (fused recompute)
 template <typename T>
+constexpr int scan_u(int v) { return sizeof(T) == 4 || v == 2 ? 8 : 4; }   // deeper U spills at 255 registers
+
+// ---------------------------------------------------------------- a3 backward (fused recompute)
+template <typename T, int V>
 __global__ void __launch_bounds__(128) lstm_bwd_kernel(int B, int H, const T* gates,
                                                        const float* __restrict__ c_prev,
                                                        const float* __restrict__ c_t, const T* __restrict__ tc_st,
                                                        const float* __restrict__ dh, float* dc, T* dA,
                                                        T* __restrict__ h_regen) {
   pdl_wait();
-  constexpr int V = St<T>::VEC;
   const int nvec = H / V;
   const long total = (long)B * nvec;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
@@ -173,19 +276,19 @@ __global__ void __launch_bounds__(128) lstm_bwd_kernel(int B, int H, const T* ga
     const long row4 = (long)b * 4 * H;
     const long row = (long)b * H + j;
     float gi[V], gf[V], gg[V], go[V];
-    ld16(gates + row4 + 0 * H + j, gi);
-    ld16(gates + row4 + 1 * H + j, gf);
-    ld16(gates + row4 + 2 * H + j, gg);
-    ld16(gates + row4 + 3 * H + j, go);
+    ldv<V>(gates + row4 + 0 * H + j, gi);
+    ldv<V>(gates + row4 + 1 * H + j, gf);
+    ldv<V>(gates + row4 + 2 * H + j, gg);
+    ldv<V>(gates + row4 + 3 * H + j, go);
     float cp[V], tc[V], h[V], dhv[V], dcv[V];
-    ldf<V>(c_prev + row, cp);
-    ldf<V>(dh + row, dhv);
-    ldf<V>(dc + row, dcv);
+    ldv<V>(c_prev + row, cp);
+    ldv<V>(dh + row, dhv);
+    ldv<V>(dc + row, dcv);
     if (tc_st) {                       // STASH: tanh(c_t) was stashed by a1
-      ld16(tc_st + row, tc);
+      ldv<V>(tc_st + row, tc);
     } else {                           // RECOMPUTE: regenerate tanh(c_t) and h_t
       float ct[V];
-      ldf<V>(c_t + row, ct);
+      ldv<V>(c_t + row, ct);
 #pragma unroll
       for (int k = 0; k < V; ++k) { tc[k] = tanh_c<T>(ct[k]); h[k] = hidden<T>(go[k], tc[k]); }
     }
@@ -204,12 +307,12 @@ __global__ void __launch_bounds__(128) lstm_bwd_kernel(int B, int H, const T* ga
       dg[k] = St<T>::round(__fmul_rn(d_g, __fsub_rn(1.0f, __fmul_rn(gg[k], gg[k]))));
       dout[k] = St<T>::round(__fmul_rn(d_o, __fmul_rn(go[k], __fsub_rn(1.0f, go[k]))));
     }
-    st16(dA + row4 + 0 * H + j, di);
-    st16(dA + row4 + 1 * H + j, df);
-    st16(dA + row4 + 2 * H + j, dg);
-    st16(dA + row4 + 3 * H + j, dout);
-    stf<V>(dc + row, dcn);
-    if (h_regen) st16(h_regen + row, h);
+    stv<V>(dA + row4 + 0 * H + j, di);
+    stv<V>(dA + row4 + 1 * H + j, df);
+    stv<V>(dA + row4 + 2 * H + j, dg);
+    stv<V>(dA + row4 + 3 * H + j, dout);
+    stv<V>(dc + row, dcn);
+    if (h_regen) stv<V>(h_regen + row, h);
   }
 }
 
@@ -444,17 +547,20 @@ extern "C" echo_status echo_lstm_fwd(const echo_lstm_desc* d, const void* gx_t, 
   else if (tc_t) return fail(ECHO_ERR_INVALID, "%s: tc_t must be NULL in RECOMPUTE mode", fn);
   if (c_out == c_prev) return fail(ECHO_ERR_INVALID, "%s: c_out must not alias c_prev", fn);
   cudaStream_t st = (cudaStream_t)stream;
-  const int V = d->dtype == ECHO_FP32 ? 4 : 8;
+  const bool bf = d->dtype != ECHO_FP32;
+  const int V = step_vec((long)d->B * d->H, bf);
   const int blk = step_block((long)d->B * d->H / V);
   const int grid = grid_for((long)d->B * d->H / V, blk);
   cudaError_t e_;
-  if (d->dtype == ECHO_FP32)
-    e_ = launch(lstm_fwd_kernel<float>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H, (const float*)gx_t,
-                (const float*)gh_t, bias, c_prev, (float*)gates_t, c_out, (float*)tc_t, (float*)h_out);
+#define ECHO_FWD_LAUNCH(TT, VV)                                                                                     \
+  launch(lstm_fwd_kernel<TT, VV>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H, (const TT*)gx_t, (const TT*)gh_t, bias, \
+         c_prev, (TT*)gates_t, c_out, (TT*)tc_t, (TT*)h_out)
+  typedef __nv_bfloat16 bft;
+  if (!bf)
+    e_ = V == 4 ? ECHO_FWD_LAUNCH(float, 4) : V == 2 ? ECHO_FWD_LAUNCH(float, 2) : ECHO_FWD_LAUNCH(float, 1);
   else
-    e_ = launch(lstm_fwd_kernel<__nv_bfloat16>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H,
-                (const __nv_bfloat16*)gx_t, (const __nv_bfloat16*)gh_t, bias, c_prev, (__nv_bfloat16*)gates_t, c_out,
-                (__nv_bfloat16*)tc_t, (__nv_bfloat16*)h_out);
+    e_ = V == 8 ? ECHO_FWD_LAUNCH(bft, 8) : V == 4 ? ECHO_FWD_LAUNCH(bft, 4) : ECHO_FWD_LAUNCH(bft, 2);
+#undef ECHO_FWD_LAUNCH
   if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
   return check_launch(fn);
 }
@@ -470,15 +576,21 @@ extern "C" echo_status echo_lstm_cscan(const echo_lstm_desc* d, int32_t T, const
   ECHO_REQ(c_ws, "c_ws");
   ECHO_OPT(h_ws, "h_ws");
   cudaStream_t st = (cudaStream_t)stream;
-  const int V = d->dtype == ECHO_FP32 ? 4 : 8;
+  const bool bf = d->dtype != ECHO_FP32;
+  // measured at C2 (CUPTI, in-graph): bf16 16-byte vectors / U = 4 38.3 us -> 4-byte / U = 8 15.9 us;
+  // fp32 stays at 16-byte vectors (4-byte loads: 18.3 -> 29.8 us)
+  const int V = bf || getenv("ECHO_LSTM_VEC") ? step_vec((long)d->B * d->H, bf) : 4;
   const int grid = grid_for((long)d->B * d->H / V, 128);
   cudaError_t e_;
-  if (d->dtype == ECHO_FP32)
-    e_ = launch(lstm_cscan_kernel<float, 8>, dim3(grid), dim3(128), 0, st, 1, T, d->B, d->H, (const float*)gates, c0,
-                c_ws, (float*)h_ws);
+#define ECHO_SCAN_LAUNCH(TT, VV)                                                                                      \
+  launch(lstm_cscan_kernel<TT, VV, scan_u<TT>(VV)>, dim3(grid), dim3(128), 0, st, 1, T, d->B, d->H, (const TT*)gates, c0, c_ws, \
+         (TT*)h_ws)
+  typedef __nv_bfloat16 bft;
+  if (!bf)
+    e_ = V == 4 ? ECHO_SCAN_LAUNCH(float, 4) : V == 2 ? ECHO_SCAN_LAUNCH(float, 2) : ECHO_SCAN_LAUNCH(float, 1);
   else
-    e_ = launch(lstm_cscan_kernel<__nv_bfloat16, 4>, dim3(grid), dim3(128), 0, st, 1, T, d->B, d->H,
-                (const __nv_bfloat16*)gates, c0, c_ws, (__nv_bfloat16*)h_ws);
+    e_ = V == 8 ? ECHO_SCAN_LAUNCH(bft, 8) : V == 4 ? ECHO_SCAN_LAUNCH(bft, 4) : ECHO_SCAN_LAUNCH(bft, 2);
+#undef ECHO_SCAN_LAUNCH
   if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
   return check_launch(fn);
 }
@@ -504,17 +616,20 @@ extern "C" echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_
     if (tc_t) return fail(ECHO_ERR_INVALID, "%s: tc_t must be NULL in RECOMPUTE mode", fn);
   }
   cudaStream_t st = (cudaStream_t)stream;
-  const int V = d->dtype == ECHO_FP32 ? 4 : 8;
+  const bool bf = d->dtype != ECHO_FP32;
+  const int V = step_vec((long)d->B * d->H, bf);
   const int blk = step_block((long)d->B * d->H / V);
   const int grid = grid_for((long)d->B * d->H / V, blk);
   cudaError_t e_;
-  if (d->dtype == ECHO_FP32)
-    e_ = launch(lstm_bwd_kernel<float>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H, (const float*)gates_t, c_prev,
-                c_t, (const float*)tc_t, dh_t, dc, (float*)dA_t, (float*)h_regen);
+#define ECHO_BWD_LAUNCH(TT, VV)                                                                                      \
+  launch(lstm_bwd_kernel<TT, VV>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H, (const TT*)gates_t, c_prev, c_t,       \
+         (const TT*)tc_t, dh_t, dc, (TT*)dA_t, (TT*)h_regen)
+  typedef __nv_bfloat16 bft;
+  if (!bf)
+    e_ = V == 4 ? ECHO_BWD_LAUNCH(float, 4) : V == 2 ? ECHO_BWD_LAUNCH(float, 2) : ECHO_BWD_LAUNCH(float, 1);
   else
-    e_ = launch(lstm_bwd_kernel<__nv_bfloat16>, dim3(grid), dim3(blk), 0, st, 1, d->B, d->H,
-                (const __nv_bfloat16*)gates_t, c_prev, c_t, (const __nv_bfloat16*)tc_t, dh_t, dc, (__nv_bfloat16*)dA_t,
-                (__nv_bfloat16*)h_regen);
+    e_ = V == 8 ? ECHO_BWD_LAUNCH(bft, 8) : V == 4 ? ECHO_BWD_LAUNCH(bft, 4) : ECHO_BWD_LAUNCH(bft, 2);
+#undef ECHO_BWD_LAUNCH
   if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
   return check_launch(fn);
 }
