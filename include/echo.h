@@ -287,6 +287,14 @@ echo_status echo_xent_fwd_bwd(int32_t N, int32_t V, float* logits, const float* 
 echo_status echo_colsum(int32_t rows, int32_t cols, int64_t ld, int32_t dtype, const void* x, float* out,
                         int32_t accumulate, void* stream);
 
+/* Backward of the attention hidden a_t = tanh(pre_t) (reading R7, §2;
+ * tanh keeps its output): dpre[i] = da[i] * (1 - a[i]^2), fp32 arithmetic in that
+ * order (a read in its storage dtype).  Outside the Echo decision (a_t is kept in both modes).
+ *  n       elements;  dtype  storage dtype of a (ECHO_FP32 / ECHO_BF16)
+ *  a       [n] device, storage dtype;  da  [n] fp32 device;  dpre  [n] fp32 device OUT (may alias da)
+ * Errors: ECHO_ERR_INVALID.                                                                      */
+echo_status echo_tanh_bwd(int64_t n, int32_t dtype, const void* a, const float* da, float* dpre, void* stream);
+
 /* ===================================================================== footprint estimator
  * Host-only, integer, deterministic.  Runs the adjusted pass pipeline of
  * Fig. 14: Gradient -> InferShape&Type -> EdgeUseRef ->

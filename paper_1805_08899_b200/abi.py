@@ -22,7 +22,7 @@ EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_c
             "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
             "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum", "echo_lstm_seq_fwd",
             "echo_lstm_seq_supported", "echo_gemm_f32", "echo_gemm_f32_supported",
-            "echo_attn_bwd_deferred", "echo_attn_bwd_finish",
+            "echo_attn_bwd_deferred", "echo_attn_bwd_finish", "echo_tanh_bwd",
             "echo_footprint_estimate")
 
 
@@ -83,6 +83,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                           ctypes.c_float, vp, ctypes.c_int64, vp],
         "echo_lstm_seq_fwd": [ctypes.POINTER(LstmDesc), i32, i32, i32, i32] + [vp] * 7 + [i32, vp, vp, vp],
         "echo_colsum": [i32, i32, ctypes.c_int64, i32, vp, vp, i32, vp],
+        "echo_tanh_bwd": [ctypes.c_int64, i32, vp, vp, vp, vp],
         "echo_footprint_estimate": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)],
     }
     for name, args in sigs.items():
@@ -212,6 +213,16 @@ def echo_xent_fwd_bwd(N, V, logits, bias, labels, row_loss, dlogits_bf16=None, s
     LAUNCHES["count"] += 1
     _check(load().echo_xent_fwd_bwd(N, V, _p(logits), _p(bias), _p(labels), _p(row_loss), _p(dlogits_bf16),
                                     _stream(stream)))
+
+
+def echo_tanh_bwd(a, da, dpre, stream=None):
+    """dpre (fp32) = da * (1 - a^2) for a = tanh(pre) in storage dtype (same shapes, contiguous)."""
+    import torch
+    assert a.is_contiguous() and da.is_contiguous() and dpre.is_contiguous()
+    assert a.numel() == da.numel() == dpre.numel() and da.dtype == dpre.dtype == torch.float32
+    LAUNCHES["count"] += 1
+    dt = FP32 if a.dtype == torch.float32 else BF16
+    _check(load().echo_tanh_bwd(a.numel(), dt, _p(a), _p(da), _p(dpre), _stream(stream)))
 
 
 def echo_colsum(x, out, accumulate=0, stream=None):

@@ -348,8 +348,7 @@ class NMTModel(probe.GraphStep):
         Wcc32, Wch32, Wq32 = self.P["att.Wcc"], self.P["att.Wch"], self.P["att.Wq"]
         lowp = sd != torch.float32                               # bf16 storage: TF32 for the fp32 GEMMs
         for t in reversed(range(Td)):
-            at = Aall[t].float()
-            torch.mul(dAout[t], 1.0 - at * at, out=dPRE[t])      # tanh' = 1 - a^2
+            abi.echo_tanh_bwd(Aall[t], dAout[t], dPRE[t])        # tanh' = 1 - a^2
             top = dHdec[-1][t]
             dctx = dctx_all[t] if deferred else dctx1
             with tf32(lowp):

@@ -68,3 +68,20 @@ def test_colsum_fp64_accumulation(rows, cols, dtype, cuda_dev):
     out2 = torch.ones(cols, device="cuda")
     abi.echo_colsum(t, out2, accumulate=1)
     assert torch.allclose(out2, out + 1.0)
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("n", [1, 777, 128 * 512])
+def test_tanh_bwd(storage, n, cuda_dev):
+    """echo_tanh_bwd == the fp32 expression da * (1 - a*a) bitwise, and == fp64 within fp32 rounding."""
+    from paper_1805_08899_b200 import abi
+    g = torch.Generator(device="cuda").manual_seed(n)
+    sd = torch.float32 if storage == "fp32" else torch.bfloat16
+    a = torch.tanh(torch.randn(n, device="cuda", generator=g) * 2).to(sd)
+    da = torch.randn(n, device="cuda", generator=g)
+    out = torch.empty(n, device="cuda")
+    abi.echo_tanh_bwd(a, da, out)
+    af = a.float()
+    assert torch.equal(out, da * (1.0 - af * af))
+    ref = da.double() * (1.0 - af.double() ** 2)
+    assert float((out.double() - ref).abs().max() / ref.abs().max()) < 1e-6
