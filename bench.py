@@ -231,10 +231,14 @@ def extra_leg(name, dtype_s, steps=10, warmup=3):
         params, batch = D.nmt_params(0, cfg, dtype_s), D.nmt_batch(1, cfg)
         res["workload"] = f"C5 NMT (C2 shapes) at B={Bc5} per GPU: STASH exceeds HBM, RECOMPUTE fits"
         samples = cfg.B
-    for mode, mname in ((abi.STASH, "stash"), (abi.RECOMPUTE, "recompute")):
+    plans = [(abi.STASH, "stash", False), (abi.RECOMPUTE, "recompute", False)]
+    if name in ("C3", "C4"):                         # the prior-work Mirror plan on the same kernels
+        plans.append((abi.RECOMPUTE, "mirror", True))
+    for mode, mname, mirror in plans:
         r = {}
+        m = None
         try:
-            m = M(cfg, dt, mode)
+            m = M(cfg, dt, mode, mirror=True) if mirror else M(cfg, dt, mode)
             m.load_params(params)
             m.upload_batch(batch)
             torch.cuda.synchronize()
@@ -269,6 +273,11 @@ def extra_leg(name, dtype_s, steps=10, warmup=3):
         res["recompute_overhead"] = rc["ms_per_step"] / st["ms_per_step"] - 1.0
     if st.get("stash_bytes") and rc.get("stash_bytes"):
         res["stash_ratio"] = st["stash_bytes"] / rc["stash_bytes"]
+    mi = res.get("mirror")
+    if mi and "ms_per_step" in mi and "ms_per_step" in st:
+        res["mirror_overhead"] = mi["ms_per_step"] / st["ms_per_step"] - 1.0
+    if mi and mi.get("stash_bytes") and st.get("stash_bytes"):
+        res["mirror_stash_ratio"] = st["stash_bytes"] / mi["stash_bytes"]     # < 1: Mirror keeps MORE
     return res
 
 

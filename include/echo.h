@@ -123,6 +123,32 @@ echo_status echo_lstm_seq_fwd(const echo_lstm_desc* d, int32_t T, int32_t k0, in
                               const void* gx, const void* Wh, const float* bias, const void* h0,
                               const float* c0, void* gates, float* c, int32_t c_ring, void* tc, void* h,
                               void* stream);
+/* ---- Mirror plan (the prior-work baseline, Chen et al.; Table 1, 749, 951;
+ * estimator strategy "mirror", R25).  Mirror recomputes every cheap op of the cell,
+ * so per step it keeps the INPUTS of the pre-activation adds -- the n_parts separate FC outputs
+ * (input projection(s) and h_{t-1} W_h^T) -- and h_t (an FC input), instead of the gates.  The
+ * kernels regenerate A = ((P_0 + P_1) + P_2) + b in fp32 in that order (a1's order for gx, gh,
+ * bias) and run the same gate / cell / gradient functions as a1 / a2 / a3.
+ *  n_parts      1..3;  part q of a step is at parts + q * part_stride (elements, >= 4*B*H)
+ *  parts_t      [n_parts][B,4H] s of this step;  bias [4H] fp32 or NULL
+ * echo_lstm_fwd_parts: c_prev [B,H] fp32 IN, c_out [B,H] fp32 OUT (must not alias c_prev),
+ *   h_out [B,H] s OUT (kept by the Mirror plan).
+ * echo_lstm_cscan_parts: c_1..c_T of the layer into c_ws [T,B,H] fp32 (processing order) from
+ *   c0; step k's parts at parts + k * step_stride (|step_stride| >= 4*B*H; negative walks a
+ *   time-ordered buffer backwards for a reverse-direction layer).
+ * echo_lstm_bwd_parts: as echo_lstm_bwd in RECOMPUTE mode with the gates regenerated from the
+ *   parts and no h output (h_t is kept); dA_t [B,4H] s OUT may alias part 0 of the step.
+ * Device pointers, 16-byte aligned; desc->mode is not used.  Errors: ECHO_ERR_INVALID.           */
+echo_status echo_lstm_fwd_parts(const echo_lstm_desc* d, int32_t n_parts, const void* parts_t,
+                                int64_t part_stride, const float* bias, const float* c_prev,
+                                float* c_out, void* h_out, void* stream);
+echo_status echo_lstm_cscan_parts(const echo_lstm_desc* d, int32_t T, int32_t n_parts, const void* parts,
+                                  int64_t part_stride, int64_t step_stride, const float* bias,
+                                  const float* c0, float* c_ws, void* stream);
+echo_status echo_lstm_bwd_parts(const echo_lstm_desc* d, int32_t n_parts, const void* parts_t,
+                                int64_t part_stride, const float* bias, const float* c_prev,
+                                const float* c_t, const float* dh_t, float* dc, void* dA_t, void* stream);
+
 /* 1 if echo_lstm_seq_fwd has a co-resident tile for this (B, H, dtype) on the current device. */
 int32_t echo_lstm_seq_supported(int32_t B, int32_t H, int32_t dtype);
 

@@ -23,6 +23,7 @@ EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_c
             "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum", "echo_lstm_seq_fwd",
             "echo_lstm_seq_supported", "echo_gemm_f32", "echo_gemm_f32_supported",
             "echo_attn_bwd_deferred", "echo_attn_bwd_finish", "echo_tanh_bwd",
+            "echo_lstm_fwd_parts", "echo_lstm_cscan_parts", "echo_lstm_bwd_parts",
             "echo_footprint_estimate")
 
 
@@ -84,6 +85,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_lstm_seq_fwd": [ctypes.POINTER(LstmDesc), i32, i32, i32, i32] + [vp] * 7 + [i32, vp, vp, vp],
         "echo_colsum": [i32, i32, ctypes.c_int64, i32, vp, vp, i32, vp],
         "echo_tanh_bwd": [ctypes.c_int64, i32, vp, vp, vp, vp],
+        "echo_lstm_fwd_parts": [ctypes.POINTER(LstmDesc), i32, vp, ctypes.c_int64] + [vp] * 5,
+        "echo_lstm_cscan_parts": [ctypes.POINTER(LstmDesc), i32, i32, vp, ctypes.c_int64, ctypes.c_int64] + [vp] * 4,
+        "echo_lstm_bwd_parts": [ctypes.POINTER(LstmDesc), i32, vp, ctypes.c_int64] + [vp] * 7,
         "echo_footprint_estimate": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)],
     }
     for name, args in sigs.items():
@@ -213,6 +217,25 @@ def echo_xent_fwd_bwd(N, V, logits, bias, labels, row_loss, dlogits_bf16=None, s
     LAUNCHES["count"] += 1
     _check(load().echo_xent_fwd_bwd(N, V, _p(logits), _p(bias), _p(labels), _p(row_loss), _p(dlogits_bf16),
                                     _stream(stream)))
+
+
+def echo_lstm_fwd_parts(d, n_parts, parts_t, part_stride, bias, c_prev, c_out, h_out, stream=None):
+    """Mirror plan a1: parts_t = pointer (tensor) to part 0 of the step; part q at + q*part_stride."""
+    LAUNCHES["count"] += 1
+    _check(load().echo_lstm_fwd_parts(ctypes.byref(d), int(n_parts), _p(parts_t), int(part_stride), _p(bias),
+                                      _p(c_prev), _p(c_out), _p(h_out), _stream(stream)))
+
+
+def echo_lstm_cscan_parts(d, T, n_parts, parts, part_stride, step_stride, bias, c0, c_ws, stream=None):
+    LAUNCHES["count"] += 1
+    _check(load().echo_lstm_cscan_parts(ctypes.byref(d), int(T), int(n_parts), _p(parts), int(part_stride),
+                                        int(step_stride), _p(bias), _p(c0), _p(c_ws), _stream(stream)))
+
+
+def echo_lstm_bwd_parts(d, n_parts, parts_t, part_stride, bias, c_prev, c_t, dh_t, dc, dA_t, stream=None):
+    LAUNCHES["count"] += 1
+    _check(load().echo_lstm_bwd_parts(ctypes.byref(d), int(n_parts), _p(parts_t), int(part_stride), _p(bias),
+                                      _p(c_prev), _p(c_t), _p(dh_t), _p(dc), _p(dA_t), _stream(stream)))
 
 
 def echo_tanh_bwd(a, da, dpre, stream=None):

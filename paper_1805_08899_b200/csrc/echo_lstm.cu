@@ -12,6 +12,7 @@
 #include "echo_common.cuh"
 
 #include <cooperative_groups.h>
+#include <type_traits>
 
 namespace echo {
 
@@ -29,6 +30,36 @@ __device__ __forceinline__ float tanh_c(float c) { return St<T>::round(tanhf(c))
 
 template <typename T>
 __device__ __forceinline__ float hidden(float o, float tc) { return St<T>::round(__fmul_rn(o, tc)); }
+
+// The ONE definition of the activated gates from the pre-activation A (a1, and the Mirror-plan
+// kernels that regenerate A from its parts)
+template <typename T>
+__device__ __forceinline__ void gates_of(float ai, float af, float ag, float ao, float& gi, float& gf, float& gg,
+                                         float& go) {
+  gi = St<T>::round(sigmoidf_(ai));
+  gf = St<T>::round(sigmoidf_(af));
+  gg = St<T>::round(tanhf(ag));
+  go = St<T>::round(sigmoidf_(ao));
+}
+
+// The ONE definition of the cell's backward (a3 and the Mirror-plan backward): from the gates,
+// c_{t-1}, tanh(c_t), dh_t and the carried dc, the pre-activation gradients and the new carry
+//   do = dh tc ; dc = carry + dh o (1 - tc^2) ; di = dc g ; dg = dc i ; df = dc c_{t-1} ; carry' = dc f
+template <typename T>
+__device__ __forceinline__ void cell_grad(float gi, float gf, float gg, float go, float cp, float tc, float dhv,
+                                          float dcv, float& di, float& df, float& dg, float& dout, float& dcn) {
+  const float d_o = __fmul_rn(dhv, tc);
+  const float one_m_tc2 = __fsub_rn(1.0f, __fmul_rn(tc, tc));
+  const float dcc = __fadd_rn(dcv, __fmul_rn(__fmul_rn(dhv, go), one_m_tc2));
+  const float d_i = __fmul_rn(dcc, gg);
+  const float d_g = __fmul_rn(dcc, gi);
+  const float d_f = __fmul_rn(dcc, cp);
+  dcn = __fmul_rn(dcc, gf);
+  di = St<T>::round(__fmul_rn(d_i, __fmul_rn(gi, __fsub_rn(1.0f, gi))));
+  df = St<T>::round(__fmul_rn(d_f, __fmul_rn(gf, __fsub_rn(1.0f, gf))));
+  dg = St<T>::round(__fmul_rn(d_g, __fsub_rn(1.0f, __fmul_rn(gg, gg))));
+  dout = St<T>::round(__fmul_rn(d_o, __fmul_rn(go, __fsub_rn(1.0f, go))));
+}
 
 // per-step kernels (a1 / a3) at small B*H are latency-bound: spread the threads over more SMs
 // with smaller blocks (64 threads when there are fewer than 148 x 128 threads); ECHO_LSTM_BLOCK
@@ -189,10 +220,7 @@ __global__ void __launch_bounds__(128) lstm_fwd_kernel(int B, int H, const T* gx
     float gi[V], gf[V], gg[V], go[V], c[V], tc[V], h[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-      gi[k] = St<T>::round(sigmoidf_(a[0][k]));
-      gf[k] = St<T>::round(sigmoidf_(a[1][k]));
-      gg[k] = St<T>::round(tanhf(a[2][k]));
-      go[k] = St<T>::round(sigmoidf_(a[3][k]));
+      gates_of<T>(a[0][k], a[1][k], a[2][k], a[3][k], gi[k], gf[k], gg[k], go[k]);
       c[k] = cell_update(gf[k], cp[k], gi[k], gg[k]);
       tc[k] = tanh_c<T>(c[k]);
       h[k] = hidden<T>(go[k], tc[k]);
@@ -294,25 +322,148 @@ __global__ void __launch_bounds__(128) lstm_bwd_kernel(int B, int H, const T* ga
     }
     float di[V], df[V], dg[V], dout[V], dcn[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const float d_o = __fmul_rn(dhv[k], tc[k]);
-      const float one_m_tc2 = __fsub_rn(1.0f, __fmul_rn(tc[k], tc[k]));
-      const float dcc = __fadd_rn(dcv[k], __fmul_rn(__fmul_rn(dhv[k], go[k]), one_m_tc2));
-      const float d_i = __fmul_rn(dcc, gg[k]);
-      const float d_g = __fmul_rn(dcc, gi[k]);
-      const float d_f = __fmul_rn(dcc, cp[k]);
-      dcn[k] = __fmul_rn(dcc, gf[k]);
-      di[k] = St<T>::round(__fmul_rn(d_i, __fmul_rn(gi[k], __fsub_rn(1.0f, gi[k]))));
-      df[k] = St<T>::round(__fmul_rn(d_f, __fmul_rn(gf[k], __fsub_rn(1.0f, gf[k]))));
-      dg[k] = St<T>::round(__fmul_rn(d_g, __fsub_rn(1.0f, __fmul_rn(gg[k], gg[k]))));
-      dout[k] = St<T>::round(__fmul_rn(d_o, __fmul_rn(go[k], __fsub_rn(1.0f, go[k]))));
-    }
+    for (int k = 0; k < V; ++k)
+      cell_grad<T>(gi[k], gf[k], gg[k], go[k], cp[k], tc[k], dhv[k], dcv[k], di[k], df[k], dg[k], dout[k], dcn[k]);
     stv<V>(dA + row4 + 0 * H + j, di);
     stv<V>(dA + row4 + 1 * H + j, df);
     stv<V>(dA + row4 + 2 * H + j, dg);
     stv<V>(dA + row4 + 3 * H + j, dout);
     stv<V>(dc + row, dcn);
     if (h_regen) stv<V>(h_regen + row, h);
+  }
+}
+
+// ---------------------------------------------------------------- Mirror plan (prior work)
+// The Mirror baseline (Chen et al.; estimator strategy "mirror", reading
+// R25) mirrors every cheap op of the cell, so what it keeps per step are the INPUTS of the
+// pre-activation adds: the NP separate FC outputs (input projection(s) and h_{t-1} W_h^T, part q
+// at parts + q * pstride) and h_t (an FC input).  Its kernels regenerate
+//   A = ((P_0 + P_1) + P_2) + b      (fp32, this order; a1's order for gx, gh, bias)
+// and then run the same gate / cell / gradient device functions as a1 / a2 / a3.
+template <typename T, int V, int NP>
+__device__ __forceinline__ void parts_A(const T* p, long pstride, const float* __restrict__ bias, int H, int j,
+                                        int ngates, float (&a)[4][V]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+    if (g < ngates) ldv<V>(p + g * H + j, a[g]);
+#pragma unroll
+  for (int q = 1; q < NP; ++q)
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if (g < ngates) {
+        float t[V];
+        ldv<V>(p + q * pstride + g * H + j, t);
+#pragma unroll
+        for (int k = 0; k < V; ++k) a[g][k] = __fadd_rn(a[g][k], t[k]);
+      }
+  if (bias)
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if (g < ngates) {
+        float t[V];
+        ldv<V>(bias + g * H + j, t);
+#pragma unroll
+        for (int k = 0; k < V; ++k) a[g][k] = __fadd_rn(a[g][k], t[k]);
+      }
+}
+
+template <typename T, int V, int NP>
+__global__ void __launch_bounds__(128) lstm_fwd_parts_kernel(int B, int H, const T* __restrict__ parts, long pstride,
+                                                             const float* __restrict__ bias,
+                                                             const float* __restrict__ c_prev, float* __restrict__ c_out,
+                                                             T* __restrict__ h_out) {
+  pdl_wait();
+  const int nvec = H / V;
+  const long total = (long)B * nvec;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(idx / nvec);
+    const int j = (int)(idx - (long)b * nvec) * V;
+    float a[4][V], cp[V], c[V], h[V];
+    parts_A<T, V, NP>(parts + (long)b * 4 * H, pstride, bias, H, j, 4, a);
+    ldv<V>(c_prev + (long)b * H + j, cp);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float gi, gf, gg, go;
+      gates_of<T>(a[0][k], a[1][k], a[2][k], a[3][k], gi, gf, gg, go);
+      c[k] = cell_update(gf, cp[k], gi, gg);
+      h[k] = hidden<T>(go, tanh_c<T>(c[k]));
+    }
+    stv<V>(c_out + (long)b * H + j, c);
+    stv<V>(h_out + (long)b * H + j, h);
+  }
+}
+
+// c-chain regeneration from the parts: step k's parts at parts + k * sstride (sstride < 0 walks
+// a time-ordered buffer backwards for a reverse-direction layer); c_k to cws[k] (processing order)
+template <typename T, int V, int NP>
+__global__ void __launch_bounds__(128) lstm_cscan_parts_kernel(int T_, int B, int H, const T* __restrict__ parts,
+                                                               long pstride, long sstride, const float* __restrict__ bias,
+                                                               const float* __restrict__ c0, float* __restrict__ cws) {
+  pdl_wait();
+  constexpr int U = 4;
+  const int nvec = H / V;
+  const long total = (long)B * nvec;
+  const long cstep = (long)B * H;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(idx / nvec);
+    const int j = (int)(idx - (long)b * nvec) * V;
+    const T* gp = parts + (long)b * 4 * H;
+    float c[V];
+    ldv<V>(c0 + (long)b * H + j, c);
+    for (int t0 = 0; t0 < T_; t0 += U) {
+      float a[U][4][V];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t0 + u < T_) parts_A<T, V, NP>(gp + (long)(t0 + u) * sstride, pstride, bias, H, j, 3, a[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t0 + u < T_) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            float gi, gf, gg, go;
+            gates_of<T>(a[u][0][k], a[u][1][k], a[u][2][k], 0.0f, gi, gf, gg, go);
+            c[k] = cell_update(gf, c[k], gi, gg);
+          }
+          stv<V>(cws + (long)(t0 + u) * cstep + (long)b * H + j, c);
+        }
+    }
+  }
+}
+
+// backward step from the parts (h_t is kept by the Mirror plan, so it is not regenerated); dA may
+// alias part 0 of this step
+template <typename T, int V, int NP>
+__global__ void __launch_bounds__(128) lstm_bwd_parts_kernel(int B, int H, const T* parts, long pstride,
+                                                             const float* __restrict__ bias,
+                                                             const float* __restrict__ c_prev,
+                                                             const float* __restrict__ c_t,
+                                                             const float* __restrict__ dh, float* dc, T* dA) {
+  pdl_wait();
+  const int nvec = H / V;
+  const long total = (long)B * nvec;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(idx / nvec);
+    const int j = (int)(idx - (long)b * nvec) * V;
+    const long row4 = (long)b * 4 * H;
+    const long row = (long)b * H + j;
+    float a[4][V], cp[V], ct[V], dhv[V], dcv[V];
+    parts_A<T, V, NP>(parts + row4, pstride, bias, H, j, 4, a);
+    ldv<V>(c_prev + row, cp);
+    ldv<V>(c_t + row, ct);
+    ldv<V>(dh + row, dhv);
+    ldv<V>(dc + row, dcv);
+    float di[V], df[V], dg[V], dout[V], dcn[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float gi, gf, gg, go;
+      gates_of<T>(a[0][k], a[1][k], a[2][k], a[3][k], gi, gf, gg, go);
+      cell_grad<T>(gi, gf, gg, go, cp[k], tanh_c<T>(ct[k]), dhv[k], dcv[k], di[k], df[k], dg[k], dout[k], dcn[k]);
+    }
+    stv<V>(dA + row4 + 0 * H + j, di);
+    stv<V>(dA + row4 + 1 * H + j, df);
+    stv<V>(dA + row4 + 2 * H + j, dg);
+    stv<V>(dA + row4 + 3 * H + j, dout);
+    stv<V>(dc + row, dcn);
   }
 }
 
@@ -705,3 +856,90 @@ extern "C" int echo_debug_seq_phase(unsigned long long* host, int reset) {
   return e;
 }
 #endif
+
+// ---------------------------------------------------------------- Mirror-plan entry points
+#define ECHO_PARTS_CHECK()                                                                          \
+  echo_status s = check_desc(d);                                                                    \
+  if (s) return s;                                                                                  \
+  if (n_parts < 1 || n_parts > 3) return fail(ECHO_ERR_INVALID, "%s: n_parts=%d not in [1, 3]", fn, n_parts); \
+  if (n_parts > 1 && (part_stride % 8 || part_stride < 4L * d->B * d->H))                          \
+    return fail(ECHO_ERR_INVALID, "%s: part_stride=%lld must be a multiple of 8 and >= 4*B*H", fn,   \
+                (long long)part_stride)
+
+// (storage type, vector width) dispatch for the Mirror-plan launches: f(T{}, integral_constant<V>)
+template <typename F>
+static cudaError_t dispatch_tv(bool bf, int V, F&& f) {
+  typedef __nv_bfloat16 bft;
+  if (!bf) {
+    if (V == 4) return f(float{}, std::integral_constant<int, 4>{});
+    if (V == 2) return f(float{}, std::integral_constant<int, 2>{});
+    return f(float{}, std::integral_constant<int, 1>{});
+  }
+  if (V == 8) return f(bft{}, std::integral_constant<int, 8>{});
+  if (V == 4) return f(bft{}, std::integral_constant<int, 4>{});
+  return f(bft{}, std::integral_constant<int, 2>{});
+}
+#define ECHO_PARTS_LAUNCH(KERN, ...)                                                                \
+  do {                                                                                              \
+    const bool bf_ = d->dtype != ECHO_FP32;                                                         \
+    const int V_ = step_vec((long)d->B * d->H, bf_);                                                \
+    const int g_ = grid_for((long)d->B * d->H / V_, 128);                                           \
+    cudaStream_t st_ = (cudaStream_t)stream;                                                        \
+    const cudaError_t e_ = dispatch_tv(bf_, V_, [&](auto tt_, auto vv_) {                           \
+      typedef decltype(tt_) TT;                                                                     \
+      constexpr int VV = decltype(vv_)::value;                                                      \
+      if (n_parts == 1) return launch(KERN<TT, VV, 1>, dim3(g_), dim3(128), 0, st_, 1, __VA_ARGS__); \
+      if (n_parts == 2) return launch(KERN<TT, VV, 2>, dim3(g_), dim3(128), 0, st_, 1, __VA_ARGS__); \
+      return launch(KERN<TT, VV, 3>, dim3(g_), dim3(128), 0, st_, 1, __VA_ARGS__);                  \
+    });                                                                                             \
+    if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_)); \
+    return check_launch(fn);                                                                        \
+  } while (0)
+
+extern "C" echo_status echo_lstm_fwd_parts(const echo_lstm_desc* d, int32_t n_parts, const void* parts_t,
+                                           int64_t part_stride, const float* bias, const float* c_prev,
+                                           float* c_out, void* h_out, void* stream) {
+  const char* fn = "echo_lstm_fwd_parts";
+  ECHO_PARTS_CHECK();
+  ECHO_REQ(parts_t, "parts_t");
+  ECHO_OPT(bias, "bias");
+  ECHO_REQ(c_prev, "c_prev");
+  ECHO_REQ(c_out, "c_out");
+  ECHO_REQ(h_out, "h_out");
+  if (c_out == c_prev) return fail(ECHO_ERR_INVALID, "%s: c_out must not alias c_prev", fn);
+  ECHO_PARTS_LAUNCH(lstm_fwd_parts_kernel, d->B, d->H, (const TT*)parts_t, (long)part_stride, bias, c_prev, c_out,
+                    (TT*)h_out);
+}
+
+extern "C" echo_status echo_lstm_cscan_parts(const echo_lstm_desc* d, int32_t T, int32_t n_parts, const void* parts,
+                                             int64_t part_stride, int64_t step_stride, const float* bias,
+                                             const float* c0, float* c_ws, void* stream) {
+  const char* fn = "echo_lstm_cscan_parts";
+  ECHO_PARTS_CHECK();
+  if (T <= 0) return fail(ECHO_ERR_INVALID, "%s: T=%d must be > 0", fn, T);
+  if (step_stride % 8 || (step_stride < 0 ? -step_stride : step_stride) < 4L * d->B * d->H)
+    return fail(ECHO_ERR_INVALID, "%s: |step_stride|=%lld must be a multiple of 8 and >= 4*B*H", fn,
+                (long long)step_stride);
+  ECHO_REQ(parts, "parts");
+  ECHO_OPT(bias, "bias");
+  ECHO_REQ(c0, "c0");
+  ECHO_REQ(c_ws, "c_ws");
+  ECHO_PARTS_LAUNCH(lstm_cscan_parts_kernel, T, d->B, d->H, (const TT*)parts, (long)part_stride, (long)step_stride,
+                    bias, c0, c_ws);
+}
+
+extern "C" echo_status echo_lstm_bwd_parts(const echo_lstm_desc* d, int32_t n_parts, const void* parts_t,
+                                           int64_t part_stride, const float* bias, const float* c_prev,
+                                           const float* c_t, const float* dh_t, float* dc, void* dA_t, void* stream) {
+  const char* fn = "echo_lstm_bwd_parts";
+  ECHO_PARTS_CHECK();
+  ECHO_REQ(parts_t, "parts_t");
+  ECHO_OPT(bias, "bias");
+  ECHO_REQ(c_prev, "c_prev");
+  ECHO_REQ(c_t, "c_t");
+  ECHO_REQ(dh_t, "dh_t");
+  ECHO_REQ(dc, "dc");
+  ECHO_REQ(dA_t, "dA_t");
+  ECHO_PARTS_LAUNCH(lstm_bwd_parts_kernel, d->B, d->H, (const TT*)parts_t, (long)part_stride, bias, c_prev, c_t,
+                    dh_t, dc, (TT*)dA_t);
+}

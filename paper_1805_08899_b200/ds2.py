@@ -9,6 +9,12 @@ STASH keeps every LSTM feature map (gates, c, tanh c, h); RECOMPUTE (Echo's plan
 and regenerates the c-chain, tanh(c) and h — including the layer outputs the layer above and the
 output FC read, whose weight gradients are therefore deferred until the regenerating backward
 (the dead-node FC of PAPER.md:672).
+
+mirror=True runs the prior-work Mirror plan (estimator strategy "mirror"):
+every cell keeps its separate FC outputs (input projection(s) and h_{t-1} W_h^T) and h_t, the
+output layer keeps its two FC outputs and the labels instead of the CE probabilities (the CE is
+mirrored and re-run in the backward).  PAPER.md:951 reports that on DS2 this plan needs MORE
+memory than the Baseline; the GPU stash bytes equal the estimator's for all three plans.
 """
 from __future__ import annotations
 
@@ -22,9 +28,11 @@ from synth.data import ds2_param_shapes
 
 
 class DS2Model(probe.GraphStep):
-    def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda"):
+    def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda", mirror=False):
         abi.load()
-        self.cfg, self.dtype, self.mode = cfg, dtype, mode
+        if mirror and mode != abi.RECOMPUTE:
+            raise ValueError("the Mirror plan runs the kernels in RECOMPUTE mode")
+        self.cfg, self.dtype, self.mode, self.mirror = cfg, dtype, mode, bool(mirror)
         self.sd = TORCH_DTYPE[dtype]
         self.device = torch.device(device)
         self.shapes = ds2_param_shapes(cfg)
@@ -119,7 +127,7 @@ class DS2Model(probe.GraphStep):
         layers = []
         low = None
         for l in range(c.layers):
-            pair = [LSTMLayer(T, B, H, self.dtype, md, dev, reverse=rev) for rev in (False, True)]
+            pair = [LSTMLayer(T, B, H, self.dtype, md, dev, reverse=rev, mirror=self.mirror) for rev in (False, True)]
 
             def run(d, L, l=l, low=low):
                 Wx = self.S[f"l{l}.{d}.Wx"]
@@ -127,25 +135,36 @@ class DS2Model(probe.GraphStep):
                 L.forward_multi(ins, self.S[f"l{l}.{d}.Wh"], self.P[f"l{l}.{d}.b"], self.zero_h, self.zero_c)
 
             self._both(lambda: run("fw", pair[0]), lambda: run("bw", pair[1]))
-            if md == abi.RECOMPUTE and low is not None:
+            if md == abi.RECOMPUTE and not self.mirror and low is not None:
                 low[0].h = low[1].h = None                    # lower outputs only fed the input FCs
             layers.append(pair)
             low = pair
         N = T * B
         Wo = self.S["out.W"]
         logits = mm(low[0].h.reshape(N, H), Wo[:, :H].t(), torch.float32)
-        logits.add_(mm(low[1].h.reshape(N, H), Wo[:, H:].t(), torch.float32))
-        if md == abi.RECOMPUTE:
+        if self.mirror:                                       # the two FC outputs are kept; the add + CE mirrored
+            lg_b = mm(low[1].h.reshape(N, H), Wo[:, H:].t(), torch.float32)
+            lg_a, logits = logits, logits + lg_b
+        else:
+            logits.add_(mm(low[1].h.reshape(N, H), Wo[:, H:].t(), torch.float32))
+        if md == abi.RECOMPUTE and not self.mirror:
             low[0].h = low[1].h = None
         row_loss = torch.empty(N, dtype=torch.float32, device=dev)
         abi.echo_xent_fwd_bwd(N, V, logits, self.P["out.b"], self.labels, row_loss, None)   # in place -> dlogits
         torch.div(row_loss.sum(), N, out=self.loss)
-        reg = {"x": self.x, "h0": self.zero_h, "c0": self.zero_c, "ce_probs": logits}
+        if self.mirror:
+            del logits
+            reg = {"x": self.x, "h0": self.zero_h, "c0": self.zero_c, "labels": self.labels, "logits_a": lg_a,
+                   "logits_b": lg_b}
+        else:
+            reg = {"x": self.x, "h0": self.zero_h, "c0": self.zero_c, "ce_probs": logits}
         for l, pair in enumerate(layers):
             for d, L in zip(("fw", "bw"), pair):
                 for k, t in L.stash_views().items():
                     reg[f"l{l}.{d}.{k}"] = t
         self.stash = reg
+        if self.mirror:
+            return {"layers": layers, "logits_ab": (lg_a, lg_b)}
         return {"layers": layers, "dlogits": logits}
 
     def _backward(self, a):
@@ -154,7 +173,15 @@ class DS2Model(probe.GraphStep):
         N = T * B
         G = self.G
         self.gflat.zero_()
-        dlog = a["dlogits"]
+        if self.mirror:                                       # re-run the mirrored add + CE (same kernels)
+            lg_a, lg_b = a.pop("logits_ab")
+            dlog = lg_a + lg_b
+            del lg_a, lg_b
+            row_loss = torch.empty(N, dtype=torch.float32, device=self.device)
+            abi.echo_xent_fwd_bwd(N, c.classes, dlog, self.P["out.b"], self.labels, row_loss, None)
+            del row_loss
+        else:
+            dlog = a["dlogits"]
         dlog_s = dlog if sd == torch.float32 else dlog.to(sd)
         G["out.b"].copy_(_colsum(dlog))
         Wo = self.S["out.W"]
@@ -190,7 +217,7 @@ class DS2Model(probe.GraphStep):
                     G[f"l{lu}.{d}.Wx"][:, :H].copy_(dW[0])
                     G[f"l{lu}.{d}.Wx"][:, H:].copy_(dW[1])
                     U.release_backward()
-                    U.gates = None
+                    U.gates = U.parts = None
             del outs
             above = pair
             dH = dX

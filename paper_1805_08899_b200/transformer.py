@@ -12,6 +12,11 @@ STASH (Baseline) keeps P, the byte mask and P_d per block; RECOMPUTE (Echo's pla
 estimator derives it on synth/graphs.py transformer) keeps the raw scores S and a 1-bit mask and
 regenerates P and P_d inside a7's backward (P_d feeds the dV GEMM).  Both keep x, the head-
 layout q/k/v and O of every block (the FC / batched-dot inputs, Eq. 2).
+
+mirror=True runs the prior-work Mirror plan (Chen et al.; the estimator's
+"mirror" strategy, reading R25) on the same kernels: the cheap softmax is mirrored, so its input S
+is kept, but the batched-dot gradient reads its ORIGINAL input P_d, which is kept too (S + P_d +
+1-bit mask per block); a7's backward regenerates P only.
 """
 from __future__ import annotations
 
@@ -27,9 +32,11 @@ from synth.data import tx_param_shapes
 
 
 class TXModel(probe.GraphStep):
-    def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda"):
+    def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda", mirror=False):
         abi.load()
-        self.cfg, self.dtype, self.mode = cfg, dtype, mode
+        if mirror and mode != abi.RECOMPUTE:
+            raise ValueError("the Mirror plan runs the kernels in RECOMPUTE mode")
+        self.cfg, self.dtype, self.mode, self.mirror = cfg, dtype, mode, bool(mirror)
         self.sd = TORCH_DTYPE[dtype]
         self.device = torch.device(device)
         self.shapes = tx_param_shapes(cfg)
@@ -136,6 +143,8 @@ class TXModel(probe.GraphStep):
             if md == abi.STASH:
                 blk["P"], blk["Pd"] = P, Pd
                 del S
+            elif self.mirror:
+                blk["S"], blk["Pd"] = S, Pd
             else:
                 blk["S"] = S
                 del Pd
@@ -170,6 +179,10 @@ class TXModel(probe.GraphStep):
                 with probe.timed("dot_bwd"):
                     abi.echo_dot_softmax_bwd(self.desc(k), None, blk["P"], blk["mask"], dPd, dPd, None)
                 Pd = blk["Pd"]
+            elif self.mirror:
+                Pd = blk["Pd"]
+                with probe.timed("dot_bwd"):
+                    abi.echo_dot_softmax_bwd(self.desc(k), blk["S"], None, blk["mask"], dPd, dPd, None)
             else:
                 Pd = torch.empty_like(dPd)
                 with probe.timed("dot_bwd"):

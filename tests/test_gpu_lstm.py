@@ -140,3 +140,71 @@ def test_validation_errors(cuda_dev):
     with pytest.raises(abi.EchoError):   # misaligned pointer
         abi.echo_lstm_fwd(abi.LstmDesc(B, H, abi.FP32, abi.RECOMPUTE), t.view(-1)[1:].data_ptr(), None, None, c, t,
                           c.clone(), None, c.clone())
+
+
+@pytest.mark.parametrize("storage", STORAGES)
+@pytest.mark.parametrize("n_parts", [1, 2, 3])
+@pytest.mark.parametrize("B,H", [(3, 16), (128, 512)])
+def test_mirror_parts_kernels(storage, n_parts, B, H, cuda_dev):
+    """Mirror-plan kernels (echo_lstm_*_parts): A = ((P0 + P1) + P2) + b in fp32; forward, scan and
+    backward vs the oracle cell on that A; fwd_parts with two parts == a1 with (gx, gh, bias)
+    bitwise; the scan's c == the forward's c bitwise; bwd_parts == a3 (RECOMPUTE) on a1's gates."""
+    abi = _abi()
+    rng = np.random.default_rng(B * 10 + n_parts)
+    sd = torch.float32 if storage == "fp32" else torch.bfloat16
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    desc = abi.LstmDesc(B, H, dt, abi.RECOMPUTE)
+    T = 3
+    parts = torch.from_numpy(rng.standard_normal((n_parts, T, B, 4 * H)).astype(np.float32) * 0.7).cuda().to(sd)
+    bias = torch.from_numpy(rng.standard_normal(4 * H).astype(np.float32) * 0.3).cuda()
+    c0 = torch.from_numpy(rng.standard_normal((B, H)).astype(np.float32)).cuda()
+    ps = T * B * 4 * H
+    A = parts[0].float()
+    for q in range(1, n_parts):
+        A = A + parts[q].float()
+    A = A + bias
+    # forward over T steps
+    c = [c0]
+    h = torch.empty(T, B, H, dtype=sd, device="cuda")
+    for t in range(T):
+        c.append(torch.empty(B, H, device="cuda"))
+        abi.echo_lstm_fwd_parts(desc, n_parts, parts[0][t], ps, bias, c[t], c[t + 1], h[t])
+    for t in range(T):
+        ref = O.cell_forward(host(A[t]), host(c[t]))
+        assert_close(host(c[t + 1]), ref["c"], storage, "c")
+        assert_close(host(h[t]), ref["h"], storage, "h")
+    if n_parts == 2:                                   # same arithmetic as a1 with gx, gh, bias
+        g1 = torch.empty(B, 4 * H, dtype=sd, device="cuda")
+        c1 = torch.empty(B, H, device="cuda")
+        h1 = torch.empty(B, H, dtype=sd, device="cuda")
+        abi.echo_lstm_fwd(desc, parts[0][0], parts[1][0], bias, c0, g1, c1, None, h1)
+        assert bits_equal(c1, c[1]) and bits_equal(h1, h[0])
+    cws = torch.empty(T, B, H, device="cuda")
+    abi.echo_lstm_cscan_parts(desc, T, n_parts, parts[0][0], ps, B * 4 * H, bias, c0, cws)
+    for t in range(T):
+        assert bits_equal(cws[t], c[t + 1])
+    cws_r = torch.empty(T, B, H, device="cuda")            # reverse walk (negative step stride)
+    abi.echo_lstm_cscan_parts(desc, T, n_parts, parts[0][T - 1], ps, -B * 4 * H, bias, c0, cws_r)
+    cr = c0
+    for k in range(T):
+        ref = O.cell_forward(host(A[T - 1 - k]), host(cr))
+        assert_close(host(cws_r[k]), ref["c"], storage, "c reverse")
+        cr = cws_r[k]
+    # backward of the last step vs the oracle, and (fp32) vs a3 on a1's gates bitwise
+    dh = torch.from_numpy(rng.standard_normal((B, H)).astype(np.float32)).cuda()
+    dc_in = torch.from_numpy(rng.standard_normal((B, H)).astype(np.float32)).cuda()
+    dc = dc_in.clone()
+    dA = torch.empty(B, 4 * H, dtype=sd, device="cuda")
+    abi.echo_lstm_bwd_parts(desc, n_parts, parts[0][T - 1], ps, bias, c[T - 1], c[T], dh, dc, dA)
+    rdA, rdc = O.cell_backward(host(A[T - 1]), host(c[T - 1]), host(dh), host(dc_in))
+    assert_close(host(dA), rdA, storage, "dA")
+    assert_close(host(dc), rdc, storage, "dc")
+    if storage == "fp32":                                 # a1 on the fp32 A itself: the same gates
+        gates = torch.empty(B, 4 * H, device="cuda")
+        cc = torch.empty(B, H, device="cuda")
+        hh = torch.empty(B, H, device="cuda")
+        abi.echo_lstm_fwd(desc, A[T - 1].contiguous(), None, None, c[T - 1], gates, cc, None, hh)
+        dc2 = dc_in.clone()
+        dA2 = torch.empty_like(dA)
+        abi.echo_lstm_bwd(desc, gates, c[T - 1], c[T], None, dh, dc2, dA2, None)
+        assert bits_equal(dA, dA2) and bits_equal(dc, dc2)
