@@ -303,8 +303,8 @@ def run_ours(args):
         pinned.append({k: torch.from_numpy(b[k]).pin_memory() for k in ("src", "tgt_in", "tgt_out", "src_len")})
     lr = 0.05
 
-    def build(mode):
-        m = NMTModel(cfg, dtype=dtype, mode=mode, device=dev)
+    def build(mode, mirror=False):
+        m = NMTModel(cfg, dtype=dtype, mode=mode, device=dev, mirror=mirror)
         m.load_params(params)
         m.upload_batch(pinned[0])
         return m
@@ -365,8 +365,8 @@ def run_ours(args):
         dt = dp.max_over_ranks(dt, dev)
         return dt
 
-    def peak_activation(mode):
-        m = NMTModel(cfg, dtype=dtype, mode=mode, device=dev)
+    def peak_activation(mode, mirror=False):
+        m = NMTModel(cfg, dtype=dtype, mode=mode, device=dev, mirror=mirror)
         m.load_params(params)
         m.upload_batch(pinned[0])
         m.step(0.0)                                              # warm the allocator / cuBLAS handles
@@ -453,6 +453,14 @@ def run_ours(args):
                 mem[md] = peak_activation(md)
             except torch.OutOfMemoryError:
                 mem[md] = (None, None)
+        try:                                                     # prior-work Mirror plan (Table 1 analogue)
+            m3 = build(abi.RECOMPUTE, mirror=True)
+            ms_mirror, _ = timed(m3, use_graph, args.steps, args.warmup)
+            del m3
+            torch.cuda.empty_cache()
+            out["mirror"] = {"ms_per_step": ms_mirror, "mem": peak_activation(abi.RECOMPUTE, mirror=True)}
+        except Exception as ex:
+            print(f"[bench] mirror plan failed: {ex}", file=sys.stderr)
         out["ms_other"] = ms_other
         out["mem"] = mem
         out["kern"] = time_attn_bwd(cfg, dtype)
@@ -518,6 +526,14 @@ def run_ours(args):
             "stash_ratio": (st[1] / rc[1]) if st[1] and rc[1] else None,
             "how": "torch max_memory_allocated - memory_allocated at step start (eager), fp32 allocator bytes",
         }
+        mi = out.get("mirror")
+        if mi:
+            line["mirror_mode"] = {
+                "plan": "Mirror (Chen et al.; PAPER.md:286-305 Table 1): cheap ops mirrored, FC inputs and "
+                        "the FC outputs feeding mirrored adds kept",
+                "value": samples / (mi["ms_per_step"] / 1e3), "ms_per_step": mi["ms_per_step"],
+                "peak_activation_bytes": mi["mem"][0], "stash_bytes": mi["mem"][1],
+                "stash_reduction_vs_stash": (st[1] / mi["mem"][1]) if st[1] and mi["mem"][1] else None}
         if out["ms_other"]:
             other_name = "stash" if mode == abi.RECOMPUTE else "recompute"
             line[f"{other_name}_mode"] = {"value": samples / (out["ms_other"] / 1e3), "ms_per_step": out["ms_other"]}

@@ -128,16 +128,17 @@ def test_stash_bytes_ratio_c2(cuda_dev):
 @pytest.mark.parametrize("storage", ["fp32", "bf16"])
 def test_stash_bytes_equal_estimator(cfg, storage, cuda_dev):
     """Exact integer bytes: the tensors the GPU step keeps across the forward -> backward boundary
-    sum to the estimator's stash bytes — Baseline plan for STASH, Echo's plan for RECOMPUTE."""
+    sum to the estimator's stash bytes — Baseline plan for STASH, Echo's plan for RECOMPUTE, and the
+    prior-work Mirror plan for the Mirror mode."""
     import json
     from paper_1805_08899_b200 import abi
     from paper_1805_08899_b200.nmt import NMTModel
     from synth import graphs as Gr
     doc = json.dumps(Gr.nmt(cfg, "f32" if storage == "fp32" else "bf16"))
     dt = abi.FP32 if storage == "fp32" else abi.BF16
-    for mode, strat in ((abi.STASH, "baseline"), (abi.RECOMPUTE, "echo")):
+    for mode, strat in ((abi.STASH, "baseline"), (abi.RECOMPUTE, "echo"), (abi.RECOMPUTE, "mirror")):
         rep = json.loads(abi.echo_footprint_estimate(doc, json.dumps({"strategy": strat})))
-        m = NMTModel(cfg, dt, mode)
+        m = NMTModel(cfg, dt, mode, mirror=strat == "mirror")
         m.upload_batch(nmt_batch(0, cfg))
         acts = m._forward()
         assert m.stash_bytes() == rep["stash_bytes"], (strat, m.stash_bytes(), rep["stash_bytes"],
@@ -162,3 +163,32 @@ def test_nmt_deferred_a6_bitwise(cfg, storage, cuda_dev, monkeypatch):
             out[(flag, mode)] = m.gflat.clone()
     for mode in (abi.STASH, abi.RECOMPUTE):
         assert bits_equal(out[("0", mode)], out[("1", mode)]), mode
+
+
+@pytest.mark.parametrize("cfg,storage", [(C1, "fp32"), (SMALL_NMT, "fp32"), (RAGGED, "fp32"), (RAGGED, "bf16")],
+                         ids=lambda x: getattr(x, "name", x))
+def test_nmt_mirror_plan_parity_and_graph(cfg, storage, cuda_dev):
+    """The Mirror plan trains the same model: loss and every gradient vs the fp64 oracle within the
+    tolerance, and its CUDA-graph replay == its eager step bitwise."""
+    from paper_1805_08899_b200 import abi
+    from paper_1805_08899_b200.nmt import NMTModel
+    params = nmt_params(11, cfg, storage)
+    batch = nmt_batch(12, cfg, lengths="random")
+    ref = O.step(params, batch, cfg)
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    tol = 1e-4 if storage == "fp32" else 2e-2
+    metric = relerr if storage == "fp32" else relerr_fro
+    m = NMTModel(cfg, dt, abi.RECOMPUTE, mirror=True)
+    m.load_params(params)
+    m.upload_batch(batch)
+    loss = m.train_step(lr=0.0)
+    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"]), (loss, ref["loss"])
+    g = m.grads_numpy()
+    for k, v in ref["grads"].items():
+        assert metric(g[k], v) <= tol, (k, metric(g[k], v))
+    eager = m.gflat.clone()
+    m.capture(0.0)
+    m.gflat.zero_()
+    m.replay()
+    torch.cuda.synchronize()
+    assert bits_equal(m.gflat, eager)
