@@ -1,7 +1,7 @@
 // Stage-in microbenchmark for a5/a6: 512 CTAs (clusterless, 4 per SM by smem) pull their
 // [Ts = 50 rows x 512 B] Kp and H_s slices (s-major [Ts][B][A] fp32, A = 512, B = 128; 26.2 MB per
-// launch) into shared memory and exit.  NREP launches back to back, each on its own copy of the
-// tensors (NREP x 26 MB > L2), timed together with one event pair; an empty kernel with the same
+// launch) into shared memory and exit.  NREP launches captured in one CUDA graph, each on its own copy of
+// the tensors (NREP x 26 MB > L2), timed together with one event pair; an empty kernel with the same
 // grid gives the launch / drain floor.  Variants: TMA boxes of R rows, cp.async 16 B, ld.128+st.shared.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 stagein.cu -lcuda -o stagein
 #include <cuda.h>
@@ -114,13 +114,21 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float base_us = 0;
-  auto run = [&](const char* name, auto launch) {
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  auto run = [&](const char* name, auto launch) {   // NREP launches captured in one CUDA graph
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+    for (int r = 0; r < NREP; ++r) launch(r);
+    cudaStreamEndCapture(st, &g);
+    cudaGraphInstantiate(&ge, g, 0);
     std::vector<float> ts;
     for (int it = 0; it < 7; ++it) {
-      launch(0);
-      cudaEventRecord(e0);
-      for (int r = 0; r < NREP; ++r) launch(r);
-      cudaEventRecord(e1);
+      cudaGraphLaunch(ge, st);
+      cudaEventRecord(e0, st);
+      cudaGraphLaunch(ge, st);
+      cudaEventRecord(e1, st);
       cudaEventSynchronize(e1);
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
@@ -133,7 +141,7 @@ int main() {
            us, us - base_us, 2.0 * n * 4 / (us * 1e3), 2.0 * n * 4 / ((us - base_us) * 1e3),
            cudaGetErrorString(cudaGetLastError()));
   };
-  run("empty (same grid)", [&](int) { k_empty<<<dim3(C, B), THREADS, smem>>>(sink); });
+  run("empty (same grid)", [&](int) { k_empty<<<dim3(C, B), THREADS, smem, st>>>(sink); });
   for (int R : {13, 25, 50}) {
     CUtensorMap mK, mH;
     cuuint64_t dims[3] = {A, B, (cuuint64_t)TS * NREP}, str[2] = {A * 4, (cuuint64_t)B * A * 4};
@@ -144,9 +152,9 @@ int main() {
         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     char nm[64];
     snprintf(nm, 64, "tma R=%d", R);
-    run(nm, [&](int rep) { k_tma<<<dim3(C, B), THREADS, smem>>>(mK, mH, R, rep, sink); });
+    run(nm, [&](int rep) { k_tma<<<dim3(C, B), THREADS, smem, st>>>(mK, mH, R, rep, sink); });
   }
-  run("cp.async 16B", [&](int rep) { k_ldg<<<dim3(C, B), THREADS, smem>>>(K, H, rep, sink, 1); });
-  run("ldg.128 + sts", [&](int rep) { k_ldg<<<dim3(C, B), THREADS, smem>>>(K, H, rep, sink, 0); });
+  run("cp.async 16B", [&](int rep) { k_ldg<<<dim3(C, B), THREADS, smem, st>>>(K, H, rep, sink, 1); });
+  run("ldg.128 + sts", [&](int rep) { k_ldg<<<dim3(C, B), THREADS, smem, st>>>(K, H, rep, sink, 0); });
   return 0;
 }
