@@ -234,11 +234,14 @@ def extra_leg(name, dtype_s, steps=10, warmup=3):
     plans = [(abi.STASH, "stash", False), (abi.RECOMPUTE, "recompute", False)]
     if name in ("C3", "C4"):                         # the prior-work Mirror plan on the same kernels
         plans.append((abi.RECOMPUTE, "mirror", True))
+    if name == "C4":                                 # Echo's plan with Philox-regenerated masks (R30)
+        plans.append((abi.RECOMPUTE, "recompute_regen_masks", "regen"))
     for mode, mname, mirror in plans:
         r = {}
         m = None
         try:
-            m = M(cfg, dt, mode, mirror=True) if mirror else M(cfg, dt, mode)
+            m = M(cfg, dt, mode, regen_masks=True) if mirror == "regen" else \
+                M(cfg, dt, mode, mirror=True) if mirror else M(cfg, dt, mode)
             m.load_params(params)
             m.upload_batch(batch)
             torch.cuda.synchronize()

@@ -261,12 +261,14 @@ typedef struct {
 
 /* a7 forward.  S [R,L] s (caller's Q K^T), Pd [R,L] s OUT (feeds the caller's PV GEMM),
  *  P_st [R,L] s OUT (STASH) / NULL, mask: STASH byte mask [R,L] uint8 OUT;
- *  RECOMPUTE bit mask [R, L/8] uint8 OUT (bit j%8 of byte j/8).                        */
+ *  RECOMPUTE bit mask [R, L/8] uint8 OUT (bit j%8 of byte j/8), or NULL: nothing is kept and
+ *  the backward regenerates the mask from (seed, offset) (Philox is counter-based; R30).       */
 echo_status echo_dot_softmax_fwd(const echo_dot_desc* d, const void* S, void* Pd, void* P_st,
                                  uint8_t* mask, void* stream);
 
 /* a7 backward.  dPd [R,L] s = dLoss/dP_d.  STASH: reads P_st + byte mask (S may be NULL);
- *  RECOMPUTE: reads S + bit mask and regenerates P.  dS [R,L] s OUT = dLoss/dS (may alias dPd);
+ *  RECOMPUTE: reads S + bit mask (or regenerates the mask from (seed, offset) when mask is
+ *  NULL) and regenerates P.  dS [R,L] s OUT = dLoss/dS (may alias dPd);
  *  Pd_regen [R,L] s OUT (RECOMPUTE; for the caller's dV GEMM) or NULL.                */
 echo_status echo_dot_softmax_bwd(const echo_dot_desc* d, const void* S, const void* P_st,
                                  const uint8_t* mask, const void* dPd, void* dS, void* Pd_regen,
@@ -331,7 +333,10 @@ echo_status echo_tanh_bwd(int64_t n, int32_t dtype, const void* a, const float* 
  *               document": {version:1, placeholders:[...], nodes:[...], outputs:[...]})
  *  config_json  NUL-terminated strategy config {strategy: "baseline"|"mirror"|"echo",
  *               compute_heavy_ops, binarizable_ops, enable_dead_node,
- *               enable_binarization, flop_threshold, weight_multiplier}; NULL = echo defaults
+ *               enable_binarization, regenerate_masks, flop_threshold, weight_multiplier};
+ *               NULL = echo defaults.  regenerate_masks (default false, echo / mirror only;
+ *               DESIGN.md R30): dropout keep-masks come from a counter-based generator, so a
+ *               mirrored dropout regenerates its mask instead of keeping it (0 bytes)
  *  report_json  caller buffer for the NUL-terminated report; may be NULL to query
  *  report_len   IN capacity of report_json; OUT bytes needed (including the NUL).
  *               Returns ECHO_ERR_CAPACITY (with *report_len set) if too small.

@@ -149,7 +149,7 @@ class Graph:
         return math.ceil(self.numel(e) * WIDTH[self.dtype[e]])
 
     def is_random(self, e):
-        """dropout's keep-mask: random state, never recomputable."""
+        """dropout's keep-mask: random state, never recomputable (R26)."""
         return e[0] in self.nodes and self.nodes[e[0]]["op"] == "dropout" and e[1] == 1
 
     def n_out(self, i):
@@ -205,6 +205,7 @@ class Strategy:
         self.dead = bool(cfg.get("enable_dead_node", True))
         self.binarize = bool(cfg.get("enable_binarization", True))
         self.flop_threshold = cfg.get("flop_threshold")
+        self.regen = bool(cfg.get("regenerate_masks", False)) and self.kind != "baseline"
         if self.kind != "echo":
             self.dead = False
             self.binarize = False if self.kind == "baseline" else self.binarize
@@ -243,6 +244,8 @@ def stash_set(G, M, st):
             for e in G.outs(i):
                 if G.is_random(e):                          # a mirrored dropout re-applies its stored mask
                     S[e] = S.get(e, True) and st.binarize
+    if st.regen:                                            # R30: masks regenerated from (seed, counter)
+        S = {e: b for e, b in S.items() if not G.is_random(e)}
     return S
 
 

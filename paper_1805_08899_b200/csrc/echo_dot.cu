@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) dot_fwd_kernel(echo_dot_desc d, uint32_t 
         mb.x = ((bits >> 0) & 1u) | (((bits >> 1) & 1u) << 8) | (((bits >> 2) & 1u) << 16) | (((bits >> 3) & 1u) << 24);
         mb.y = ((bits >> 4) & 1u) | (((bits >> 5) & 1u) << 8) | (((bits >> 6) & 1u) << 16) | (((bits >> 7) & 1u) << 24);
         *reinterpret_cast<uint2*>(mask + n0) = mb;
-      } else {     // RECOMPUTE: 1-bit mask
+      } else if (mask) {     // RECOMPUTE: 1-bit mask (NULL: regenerated in the backward)
         mask[n0 >> 3] = (uint8_t)bits;
       }
     }
@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(256) dot_fwd_kernel(echo_dot_desc d, uint32_t 
 }
 
 template <typename T, int CH>
-__global__ void __launch_bounds__(256) dot_bwd_kernel(echo_dot_desc d, float inv_keep, const T* __restrict__ S,
+__global__ void __launch_bounds__(256) dot_bwd_kernel(echo_dot_desc d, uint32_t thr, float inv_keep,
+                                                      const T* __restrict__ S,
                                                       const T* __restrict__ P_st, const uint8_t* __restrict__ mask,
                                                       const T* dPd, T* dS, T* __restrict__ Pd_regen) {
   pdl_wait();
@@ -160,7 +161,9 @@ __global__ void __launch_bounds__(256) dot_bwd_kernel(echo_dot_desc d, float inv
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const int j0 = (c * 32 + lane) * 8;
-        bits[c] = j0 < L ? (uint32_t)mask[((uint64_t)r * L + j0) >> 3] : 0u;
+        if (j0 >= L) bits[c] = 0u;
+        else if (mask) bits[c] = (uint32_t)mask[((uint64_t)r * L + j0) >> 3];
+        else bits[c] = d.dropout_p > 0.0f ? keep_bits8(d.seed, d.offset, (uint64_t)r * L + j0, thr) : 0xFFu;
       }
     }
     float dP[CH][8];
@@ -233,18 +236,19 @@ static void launch_fwd(const echo_dot_desc* d, uint32_t thr, float ik, const voi
   if (ch <= 1) L_(1); else if (ch <= 2) L_(2); else if (ch <= 4) L_(4); else L_(8);
 #undef L_
 }
+
+static uint32_t keep_thr(float p) { return (uint32_t)floor((double)p * 16777216.0); }
+
 template <typename T>
-static void launch_bwd(const echo_dot_desc* d, float ik, const void* S, const void* P_st, const uint8_t* mask,
-                       const void* dPd, void* dS, void* Pdr, cudaStream_t st) {
+static void launch_bwd(const echo_dot_desc* d, uint32_t thr, float ik, const void* S, const void* P_st,
+                       const uint8_t* mask, const void* dPd, void* dS, void* Pdr, cudaStream_t st) {
   const int ch = (d->L + 255) / 256;
   const int grid = dot_grid(d->R);
-#define L_(CH) (void)launch(dot_bwd_kernel<T, CH>, dim3(grid), dim3(256), 0, st, 1, *d, ik, (const T*)S, \
+#define L_(CH) (void)launch(dot_bwd_kernel<T, CH>, dim3(grid), dim3(256), 0, st, 1, *d, thr, ik, (const T*)S, \
                          (const T*)P_st, mask, (const T*)dPd, (T*)dS, (T*)Pdr)
   if (ch <= 1) L_(1); else if (ch <= 2) L_(2); else if (ch <= 4) L_(4); else L_(8);
 #undef L_
 }
-
-static uint32_t keep_thr(float p) { return (uint32_t)floor((double)p * 16777216.0); }
 
 extern "C" echo_status echo_dot_softmax_fwd(const echo_dot_desc* d, const void* S, void* Pd, void* P_st, uint8_t* mask,
                                             void* stream) {
@@ -253,7 +257,7 @@ extern "C" echo_status echo_dot_softmax_fwd(const echo_dot_desc* d, const void* 
   if (s) return s;
   ECHO_REQ(S, "S");
   ECHO_REQ(Pd, "Pd");
-  if (!mask) return fail(ECHO_ERR_INVALID, "%s: mask is NULL", fn);
+  if (!mask && d->mode == ECHO_STASH) return fail(ECHO_ERR_INVALID, "%s: mask is NULL in STASH mode", fn);
   if (d->mode == ECHO_STASH) {
     ECHO_REQ(P_st, "P_st");
     if ((reinterpret_cast<uintptr_t>(mask) & 7u) != 0) return fail(ECHO_ERR_INVALID, "%s: byte mask must be 8-byte aligned", fn);
@@ -274,7 +278,7 @@ extern "C" echo_status echo_dot_softmax_bwd(const echo_dot_desc* d, const void* 
   if (s) return s;
   ECHO_REQ(dPd, "dPd");
   ECHO_REQ(dS, "dS");
-  if (!mask) return fail(ECHO_ERR_INVALID, "%s: mask is NULL", fn);
+  if (!mask && d->mode == ECHO_STASH) return fail(ECHO_ERR_INVALID, "%s: mask is NULL in STASH mode", fn);
   if (d->mode == ECHO_STASH) {
     ECHO_REQ(P_st, "P_st");
     if (Pd_regen) return fail(ECHO_ERR_INVALID, "%s: Pd_regen must be NULL in STASH mode", fn);
@@ -284,7 +288,8 @@ extern "C" echo_status echo_dot_softmax_bwd(const echo_dot_desc* d, const void* 
     if (Pd_regen && !aligned16(Pd_regen)) return fail(ECHO_ERR_INVALID, "%s: Pd_regen not 16-byte aligned", fn);
   }
   const float ik = (float)(1.0 / (1.0 - (double)d->dropout_p));
-  if (d->dtype == ECHO_FP32) launch_bwd<float>(d, ik, S, P_st, mask, dPd, dS, Pd_regen, (cudaStream_t)stream);
-  else launch_bwd<__nv_bfloat16>(d, ik, S, P_st, mask, dPd, dS, Pd_regen, (cudaStream_t)stream);
+  const uint32_t thr = keep_thr(d->dropout_p);
+  if (d->dtype == ECHO_FP32) launch_bwd<float>(d, thr, ik, S, P_st, mask, dPd, dS, Pd_regen, (cudaStream_t)stream);
+  else launch_bwd<__nv_bfloat16>(d, thr, ik, S, P_st, mask, dPd, dS, Pd_regen, (cudaStream_t)stream);
   return check_launch(fn);
 }

@@ -446,6 +446,7 @@ struct Config {
   std::set<std::string> heavy{"fully_connected", "matmul", "batched_dot", "conv2d"};
   std::set<std::string> binarizable{"relu", "dropout"};
   bool dead = true, binarize = true;
+  bool regen = false;          // counter-based dropout masks may be regenerated (reading R30)
   bool has_threshold = false;
   double threshold = 0;
   double weight_multiplier = 1;
@@ -468,13 +469,14 @@ Config parse_config(const char* s) {
   }
   if (auto* v = j.get("enable_dead_node")) c.dead = v->b;
   if (auto* v = j.get("enable_binarization")) c.binarize = v->b;
+  if (auto* v = j.get("regenerate_masks")) c.regen = v->b;
   if (auto* v = j.get("flop_threshold"))
     if (v->kind == Json::NUM) { c.has_threshold = true; c.threshold = v->num; }
   if (auto* v = j.get("weight_multiplier"))
     if (v->kind == Json::NUM) c.weight_multiplier = v->num;
   if (c.kind != "echo") {
     c.dead = false;
-    if (c.kind == "baseline") c.binarize = false;
+    if (c.kind == "baseline") c.binarize = c.regen = false;
   }
   return c;
 }
@@ -517,7 +519,7 @@ struct Analysis {
     const Node& p = g.nodes[g.edges[e].node];
     return p.placeholder && p.trainable;
   }
-  // dropout's keep-mask: random state, never recomputed (reading R26)
+  // dropout's keep-mask: random state, never recomputed from the dropout's input (reading R26)
   bool is_random(int e) const {
     const Node& p = g.nodes[g.edges[e].node];
     return !p.placeholder && p.op == DROPOUT && g.edges[e].out == 1;
@@ -528,6 +530,7 @@ struct Analysis {
     const int p = g.edges[e].node;
     const bool pm = mirrored[p];
     const bool rnd = is_random(e);
+    if (rnd && cfg.regen) return 0;                          // R30: regenerated from (seed, counter)
     int st = 0;
     for (int r : g.grad_readers[e]) {
       if (pm && !heavy_orig[r] && !rnd) continue;            // gradient reads the recomputed copy

@@ -17,6 +17,10 @@ mirror=True runs the prior-work Mirror plan (Chen et al.; the
 "mirror" strategy, reading R25) on the same kernels: the cheap softmax is mirrored, so its input S
 is kept, but the batched-dot gradient reads its ORIGINAL input P_d, which is kept too (S + P_d +
 1-bit mask per block); a7's backward regenerates P only.
+
+regen_masks=True (RECOMPUTE / Mirror; reading R30): the keep-mask is a pure
+function of (seed, offset, index) under the counter-based Philox generator, so nothing is kept for
+it -- a7's backward regenerates it (0 bytes instead of one bit per probability).
 """
 from __future__ import annotations
 
@@ -32,11 +36,12 @@ from synth.data import tx_param_shapes
 
 
 class TXModel(probe.GraphStep):
-    def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda", mirror=False):
+    def __init__(self, cfg, dtype=abi.FP32, mode=abi.RECOMPUTE, device="cuda", mirror=False, regen_masks=False):
         abi.load()
-        if mirror and mode != abi.RECOMPUTE:
-            raise ValueError("the Mirror plan runs the kernels in RECOMPUTE mode")
+        if (mirror or regen_masks) and mode != abi.RECOMPUTE:
+            raise ValueError("the Mirror plan and regenerated masks run the kernels in RECOMPUTE mode")
         self.cfg, self.dtype, self.mode, self.mirror = cfg, dtype, mode, bool(mirror)
+        self.regen = bool(regen_masks)
         self.sd = TORCH_DTYPE[dtype]
         self.device = torch.device(device)
         self.shapes = tx_param_shapes(cfg)
@@ -134,12 +139,14 @@ class TXModel(probe.GraphStep):
                 mask = torch.empty(R * L, dtype=torch.uint8, device=dev)
             else:
                 P = None
-                mask = torch.empty(R * L // 8, dtype=torch.uint8, device=dev)
+                mask = None if self.regen else torch.empty(R * L // 8, dtype=torch.uint8, device=dev)
             with probe.timed("dot_fwd"):
                 abi.echo_dot_softmax_fwd(self.desc(k), S, Pd, P, mask)
             O = self._merge(torch.matmul(Pd, vh))
             y = torch.addmm(x, O, self.S[f"b{k}.Wo"].t())               # residual
-            blk = {"x": x, "qh": qh, "kh": kh, "vh": vh, "mask": mask, "O": O}
+            blk = {"x": x, "qh": qh, "kh": kh, "vh": vh, "O": O}
+            if mask is not None:
+                blk["mask"] = mask
             if md == abi.STASH:
                 blk["P"], blk["Pd"] = P, Pd
                 del S
@@ -177,16 +184,16 @@ class TXModel(probe.GraphStep):
             dPd = torch.matmul(dOh, vh.transpose(-1, -2))
             if md == abi.STASH:
                 with probe.timed("dot_bwd"):
-                    abi.echo_dot_softmax_bwd(self.desc(k), None, blk["P"], blk["mask"], dPd, dPd, None)
+                    abi.echo_dot_softmax_bwd(self.desc(k), None, blk["P"], blk.get("mask"), dPd, dPd, None)
                 Pd = blk["Pd"]
             elif self.mirror:
                 Pd = blk["Pd"]
                 with probe.timed("dot_bwd"):
-                    abi.echo_dot_softmax_bwd(self.desc(k), blk["S"], None, blk["mask"], dPd, dPd, None)
+                    abi.echo_dot_softmax_bwd(self.desc(k), blk["S"], None, blk.get("mask"), dPd, dPd, None)
             else:
                 Pd = torch.empty_like(dPd)
                 with probe.timed("dot_bwd"):
-                    abi.echo_dot_softmax_bwd(self.desc(k), blk["S"], None, blk["mask"], dPd, dPd, Pd)
+                    abi.echo_dot_softmax_bwd(self.desc(k), blk["S"], None, blk.get("mask"), dPd, dPd, Pd)
             dS = dPd                                                   # dS written in place (scale included)
             dV = self._merge(torch.matmul(Pd.transpose(-1, -2), dOh))
             dQ = self._merge(torch.matmul(dS, kh))

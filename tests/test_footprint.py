@@ -184,3 +184,24 @@ def test_error_codes(est):
     buf = ctypes.create_string_buffer(4)
     st = lib.echo_footprint_estimate(json.dumps(Gr.add_tanh(8)).encode(), None, buf, ctypes.byref(n))
     assert st == abi.ECHO_ERR_CAPACITY and n.value > 4
+
+
+def test_regenerated_masks_reading_r30(est):
+    """regenerate_masks (R30): counter-based dropout masks are recomputed, never kept.  C++ == oracle on
+    the Transformer graph and on random graphs with dropout; on the Transformer graph Echo's plan then
+    keeps exactly the 1-bit masks fewer (one bit per probability element per block), and the
+    baseline ignores the option."""
+    from synth.configs import SMALL_TX
+    doc = Gr.transformer(SMALL_TX)
+    _compare(est, doc, ("baseline", "mirror", "echo"), {"regenerate_masks": True})
+    e = est(doc, {"strategy": "echo"})
+    r = est(doc, {"strategy": "echo", "regenerate_masks": True})
+    n = SMALL_TX.B * SMALL_TX.heads * SMALL_TX.L * SMALL_TX.L
+    assert e["stash_bytes"] - r["stash_bytes"] == SMALL_TX.blocks * ((n + 7) // 8)
+    assert est(doc, {"strategy": "baseline", "regenerate_masks": True})["stash_bytes"] == \
+        est(doc, {"strategy": "baseline"})["stash_bytes"]
+    for seed in range(60):
+        g = Gr.random_graph(seed)
+        _compare(est, g, ("mirror", "echo"), {"regenerate_masks": True})
+        assert est(g, {"strategy": "echo", "regenerate_masks": True})["stash_bytes"] <= \
+            est(g, {"strategy": "echo"})["stash_bytes"], seed

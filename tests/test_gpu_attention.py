@@ -115,6 +115,13 @@ def test_dot_softmax_dropout(storage, R, L, p, cuda_dev):
     assert bits_equal(out[abi.STASH][2], out[abi.RECOMPUTE][2])
     assert bits_equal(out[abi.RECOMPUTE][3], out[abi.RECOMPUTE][0])
     assert_close(host(out[abi.STASH][4]), ref["P"], storage, "P")
+    # regenerated masks (R30): no mask kept; the backward re-derives it from (seed, offset)
+    desc = abi.DotDesc(R, L, dt, abi.RECOMPUTE, scale, p, seed, off)
+    Pd = torch.empty_like(S)
+    abi.echo_dot_softmax_fwd(desc, S, Pd, None, None)
+    dS, Pdr = torch.empty_like(S), torch.empty_like(S)
+    abi.echo_dot_softmax_bwd(desc, S, None, None, dPd, dS, Pdr)
+    assert bits_equal(Pd, out[abi.STASH][0]) and bits_equal(dS, out[abi.STASH][2]) and bits_equal(Pdr, Pd)
 
 
 @pytest.mark.parametrize("storage", ["fp32", "bf16"])

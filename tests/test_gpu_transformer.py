@@ -20,9 +20,9 @@ def _strict_fp32():
     torch.backends.cuda.matmul.allow_tf32 = False
 
 
-def _run(cfg, params, batch, dtype, mode, mirror=False):
+def _run(cfg, params, batch, dtype, mode, mirror=False, regen=False):
     from paper_1805_08899_b200.transformer import TXModel
-    m = TXModel(cfg, dtype, mode, mirror=mirror)
+    m = TXModel(cfg, dtype, mode, mirror=mirror, regen_masks=regen)
     m.load_params(params)
     m.upload_batch(batch)
     return m, m.train_step(lr=0.0)
@@ -39,15 +39,17 @@ def test_tx_parity_and_bit_identity(cfg, storage, cuda_dev):
     tol = 1e-4 if storage == "fp32" else 2e-2
     metric = relerr if storage == "fp32" else relerr_fro
     res = {}
-    for mode, mirror in ((abi.STASH, False), (abi.RECOMPUTE, False), (abi.RECOMPUTE, True)):
-        m, loss = _run(cfg, params, batch, dt, mode, mirror)
+    plans = ((abi.STASH, False, False), (abi.RECOMPUTE, False, False), (abi.RECOMPUTE, True, False),
+             (abi.RECOMPUTE, False, True), (abi.RECOMPUTE, True, True))
+    for mode, mirror, regen in plans:
+        m, loss = _run(cfg, params, batch, dt, mode, mirror, regen)
         assert abs(loss - ref["loss"]) <= tol * max(abs(ref["loss"]), 1e-3), (loss, ref["loss"])
         g = m.grads_numpy()
         for k, v in ref["grads"].items():
             assert metric(g[k], v) <= tol, (k, metric(g[k], v))
-        res[(mode, mirror)] = m.gflat.clone()
-    assert bits_equal(res[(abi.STASH, False)], res[(abi.RECOMPUTE, False)])
-    assert bits_equal(res[(abi.STASH, False)], res[(abi.RECOMPUTE, True)])      # Mirror plan: same gradients
+        res[(mode, mirror, regen)] = m.gflat.clone()
+    for p in plans[1:]:               # Echo, Mirror, and both with regenerated masks: the same gradients
+        assert bits_equal(res[plans[0]], res[p]), p
 
 
 @pytest.mark.parametrize("cfg", [SMALL_TX, C4], ids=lambda c: c.name)
@@ -58,9 +60,11 @@ def test_tx_stash_bytes_equal_estimator(cfg, storage, cuda_dev):
     from synth import graphs as Gr
     doc = json.dumps(Gr.transformer(cfg, "f32" if storage == "fp32" else "bf16"))
     dt = abi.FP32 if storage == "fp32" else abi.BF16
-    for mode, strat in ((abi.STASH, "baseline"), (abi.RECOMPUTE, "echo"), (abi.RECOMPUTE, "mirror")):
-        rep = json.loads(abi.echo_footprint_estimate(doc, json.dumps({"strategy": strat})))
-        m = TXModel(cfg, dt, mode, mirror=strat == "mirror")
+    for mode, strat, regen in ((abi.STASH, "baseline", False), (abi.RECOMPUTE, "echo", False),
+                               (abi.RECOMPUTE, "mirror", False), (abi.RECOMPUTE, "echo", True),
+                               (abi.RECOMPUTE, "mirror", True)):
+        rep = json.loads(abi.echo_footprint_estimate(doc, json.dumps({"strategy": strat, "regenerate_masks": regen})))
+        m = TXModel(cfg, dt, mode, mirror=strat == "mirror", regen_masks=regen)
         m.upload_batch(tx_batch(0, cfg, storage))
         acts = m._forward()
         assert m.stash_bytes() == rep["stash_bytes"], (strat, m.stash_bytes(), rep["stash_bytes"])
