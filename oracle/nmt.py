@@ -8,7 +8,9 @@ a_t from [context; query] "sent to the next decoder time step" -> output
 layer -> training loss.  Readings: R3 MLP score with qp = W_q h + b_q,
 Kp = W_k H_s; R6 zero initial states; R7 a_t = tanh(W_cc ctx_t + W_ch h_t) and
 decoder input x_t = [emb(y_{t-1}); a_{t-1}] with a_0 = 0; R10 mean softmax
-cross-entropy over all B*Td target tokens; R8 source masking.
+cross-entropy over all B*Td target tokens; R8 source masking; R31 embedding dropout with rate
+cfg.dropout on the source and target embeddings (Philox keep-masks of reading R19, one site per
+embedding, keys batch["drop_seeds"], element n = (t*B + b)*E + j of the time-major [T,B,E] tensor).
 
 Echo changes no math, so this is the one oracle for both the
 STASH and RECOMPUTE GPU modes.  Pins: tests/test_oracle_nmt.py (central finite
@@ -19,6 +21,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import attention
+from .dot_softmax import dropout_keep_mask
 from .lstm import cell_forward, cell_backward, layer_forward, layer_backward
 
 
@@ -37,9 +40,16 @@ def step(params, batch, cfg, need_grads=True):
     src, tgt_in, tgt_out, src_len = batch["src"], batch["tgt_in"], batch["tgt_out"], batch["src_len"]
     B, Ts, Td, E, H = cfg.B, cfg.Ts, cfg.Td, cfg.E, cfg.H
     zeros = np.zeros((B, H))
+    p = getattr(cfg, "dropout", 0.0)
+    if p > 0.0:                                              # R31: keep / (1 - p) per embedding element
+        ks, kt = (int(x) for x in batch["drop_seeds"])
+        ms = dropout_keep_mask(ks, 0, Ts * B * E, p).reshape(Ts, B, E) / (1.0 - p)
+        mt = dropout_keep_mask(kt, 0, Td * B * E, p).reshape(Td, B, E) / (1.0 - p)
+    else:
+        ms, mt = np.ones((Ts, B, E)), np.ones((Td, B, E))
 
     # ---------------- encoder
-    X = P["emb_src"][src].transpose(1, 0, 2)                 # [Ts, B, E]
+    X = P["emb_src"][src].transpose(1, 0, 2) * ms            # [Ts, B, E]
     enc_in = []
     for l in range(cfg.enc_layers):
         enc_in.append(X)
@@ -58,7 +68,7 @@ def step(params, batch, cfg, need_grads=True):
           "q": [None] * Td, "qp": [None] * Td, "ctx": [None] * Td, "a": [None] * Td, "logp": [None] * Td}
     loss = 0.0
     for t in range(Td):
-        x = np.concatenate([P["emb_tgt"][tgt_in[:, t]], a_prev], axis=1)
+        x = np.concatenate([P["emb_tgt"][tgt_in[:, t]] * mt[t], a_prev], axis=1)
         for l in range(L):
             A = x @ P[f"dec{l}.Wx"].T + h[l] @ P[f"dec{l}.Wh"].T + P[f"dec{l}.b"]
             tr["A"][l][t], tr["c_prev"][l][t], tr["h_prev"][l][t], tr["x_in"][l][t] = A, c[l], h[l], x
@@ -115,7 +125,7 @@ def step(params, batch, cfg, need_grads=True):
             G[f"dec{l}.b"] += dA.sum(axis=0)
             dh_rec[l] = dA @ P[f"dec{l}.Wh"]
             dx = dA @ P[f"dec{l}.Wx"]
-        np.add.at(G["emb_tgt"], tgt_in[:, t], dx[:, :E])
+        np.add.at(G["emb_tgt"], tgt_in[:, t], dx[:, :E] * mt[t])
         da_carry = dx[:, E:]
     G["att.Wk"] += np.einsum("bsa,bsh->ah", dKp, Hs)
     dHs += dKp @ P["att.Wk"]
@@ -126,6 +136,6 @@ def step(params, batch, cfg, need_grads=True):
         G[f"enc{l}.Wh"] += bw["dWh"]
         G[f"enc{l}.b"] += bw["db"]
         dH = bw["dX"]
-    np.add.at(G["emb_src"], src.T.reshape(-1), dH.reshape(Ts * B, E))
+    np.add.at(G["emb_src"], src.T.reshape(-1), (dH * ms).reshape(Ts * B, E))
     out["grads"] = G
     return out

@@ -24,6 +24,7 @@ class NMTConfig:
     V: int          # vocabulary (src = tgt), reading R17
     enc_layers: int
     dec_layers: int
+    dropout: float = 0.0  # embedding dropout rate (reading R31; 0 = none, the C1/C2 configs)
 
     @property
     def Hk(self) -> int:  # key / value width = encoder hidden
@@ -65,6 +66,8 @@ class TXConfig:
 C1 = NMTConfig("C1-tiny", B=2, Ts=4, Td=4, E=16, H=16, A=16, V=32, enc_layers=1, dec_layers=1)
 C2 = NMTConfig("C2-nmt", B=128, Ts=50, Td=50, E=512, H=512, A=512, V=8192, enc_layers=2, dec_layers=2)
 SMALL_NMT = NMTConfig("small-nmt", B=4, Ts=8, Td=8, E=32, H=32, A=32, V=64, enc_layers=2, dec_layers=2)
+SMALL_NMT_DROP = NMTConfig("small-nmt-drop", B=4, Ts=8, Td=8, E=32, H=32, A=32, V=64, enc_layers=2, dec_layers=2,
+                           dropout=0.1)
 C3 = DS2Config("C3-ds2", B=32, T=400, F=1600, H=800, layers=5)
 C4 = TXConfig("C4-tx", B=64, L=256, d_model=512, heads=8, blocks=6)
 SMALL_TX = TXConfig("small-tx", B=2, L=24, d_model=32, heads=4, blocks=2, dropout_p=0.1)

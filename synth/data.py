@@ -153,7 +153,10 @@ def nmt_batch(seed, cfg: NMTConfig, lengths="full"):
     else:
         src_len = g.integers(1, cfg.Ts + 1, size=(cfg.B,)).astype(np.int32)
         src_len[0] = cfg.Ts
-    return {"src": src, "tgt_in": tgt[:, :-1].copy(), "tgt_out": tgt[:, 1:].copy(), "src_len": src_len}
+    # Philox keys of the two embedding-dropout sites (source, target), drawn per batch (R31)
+    seeds = g.integers(1, 2 ** 62, size=2).astype(np.uint64)
+    return {"src": src, "tgt_in": tgt[:, :-1].copy(), "tgt_out": tgt[:, 1:].copy(), "src_len": src_len,
+            "drop_seeds": seeds}
 
 
 # ----------------------------------------------------------------------------- DS2

@@ -48,11 +48,14 @@ def test_fd_sampled_gradients_c1():
             assert abs(num - ana) <= 1e-7 + 1e-6 * abs(num), (name, i, num, ana)
 
 
-def _torch_nmt_loss(P, b, cfg):
-    """Same model written with torch.nn.LSTM / LSTMCell + autograd (library routines)."""
+def _torch_nmt_loss(P, b, cfg, ms=None, mt=None):
+    """Same model written with torch.nn.LSTM / LSTMCell + autograd (library routines).  ms / mt:
+    optional embedding-dropout multipliers [Ts,B,E] / [Td,B,E] (keep / (1 - p))."""
     T = {k: torch.from_numpy(v).requires_grad_(True) for k, v in P.items()}
     B, H, E = cfg.B, cfg.H, cfg.E
     x = T["emb_src"][torch.from_numpy(b["src"])].transpose(0, 1)
+    if ms is not None:
+        x = x * torch.from_numpy(ms)
     for l in range(cfg.enc_layers):
         m = torch.nn.LSTM(x.shape[2], H).double()
         x, _ = torch.func.functional_call(m, {"weight_ih_l0": T[f"enc{l}.Wx"], "weight_hh_l0": T[f"enc{l}.Wh"],
@@ -66,7 +69,10 @@ def _torch_nmt_loss(P, b, cfg):
     a = torch.zeros(B, H, dtype=torch.float64)
     loss = 0
     for t in range(cfg.Td):
-        inp = torch.cat([T["emb_tgt"][torch.from_numpy(b["tgt_in"][:, t])], a], dim=1)
+        et = T["emb_tgt"][torch.from_numpy(b["tgt_in"][:, t])]
+        if mt is not None:
+            et = et * torch.from_numpy(mt[t])
+        inp = torch.cat([et, a], dim=1)
         for l, cell in enumerate(cells):
             h[l], c[l] = torch.func.functional_call(cell, {"weight_ih": T[f"dec{l}.Wx"], "weight_hh": T[f"dec{l}.Wh"],
                                                           "bias_ih": T[f"dec{l}.b"], "bias_hh": torch.zeros(4 * H, dtype=torch.float64)},
@@ -95,3 +101,42 @@ def test_torch_autograd_crosscheck_small_nmt():
     for k in P:
         scale = max(np.abs(tg[k]).max(), 1e-30)
         assert np.abs(r["grads"][k] - tg[k]).max() / scale < 1e-10, k
+
+
+def test_embedding_dropout_oracle_pins():
+    """R31 embedding dropout: (1) the same model in torch autograd with the masks applied explicitly
+    (the mask generator itself is pinned by the Random123 known-answer vectors in
+    test_oracle_dot_softmax.py); (2) central FD on C1 with p = 0.3; (3) p = 0 equals no dropout."""
+    from dataclasses import replace
+    from oracle.dot_softmax import dropout_keep_mask
+    cfg = replace(SMALL_NMT, dropout=0.25)
+    P = _f64(nmt_params(5, cfg))
+    b = nmt_batch(6, cfg, lengths="random")
+    r = O.step(P, b, cfg)
+    ks, kt = (int(x) for x in b["drop_seeds"])
+    ms = dropout_keep_mask(ks, 0, cfg.Ts * cfg.B * cfg.E, 0.25).reshape(cfg.Ts, cfg.B, cfg.E) / 0.75
+    mt = dropout_keep_mask(kt, 0, cfg.Td * cfg.B * cfg.E, 0.25).reshape(cfg.Td, cfg.B, cfg.E) / 0.75
+    assert 0.6 < (ms > 0).mean() < 0.9 and 0.6 < (mt > 0).mean() < 0.9
+    tl, tg = _torch_nmt_loss(P, b, cfg, ms, mt)
+    assert abs(r["loss"] - tl) < 1e-12
+    for k in P:
+        scale = max(np.abs(tg[k]).max(), 1e-30)
+        assert np.abs(r["grads"][k] - tg[k]).max() / scale < 1e-10, k
+    c1 = replace(C1, dropout=0.3)
+    P1 = _f64(nmt_params(3, c1))
+    b1 = nmt_batch(4, c1)
+    G = O.step(P1, b1, c1)["grads"]
+    eps = 1e-6
+    for name in ("emb_src", "emb_tgt", "enc0.Wx", "dec0.Wx"):
+        toks = b1["src"] if name == "emb_src" else b1["tgt_in"]
+        idxs = [int(toks.reshape(-1)[0]) * P1[name].shape[1] + j for j in range(4)] if name.startswith("emb") else [0, 7, 33]
+        for i in idxs:
+            Pp = {k: v.copy() for k, v in P1.items()}
+            Pm = {k: v.copy() for k, v in P1.items()}
+            Pp[name].reshape(-1)[i] += eps
+            Pm[name].reshape(-1)[i] -= eps
+            num = (O.step(Pp, b1, c1, False)["loss"] - O.step(Pm, b1, c1, False)["loss"]) / (2 * eps)
+            assert abs(num - G[name].reshape(-1)[i]) <= 1e-7 + 1e-6 * abs(num), (name, i)
+    r0 = O.step(P1, b1, replace(c1, dropout=0.0))
+    r00 = O.step(P1, b1, C1)
+    assert r0["loss"] == r00["loss"]
