@@ -224,6 +224,13 @@ def extra_leg(name, dtype_s, steps=10, warmup=3):
         params, batch = D.tx_params(0, cfg, dtype_s), D.tx_batch(1, cfg, dtype_s)
         res["workload"] = "C4 Transformer-base attention blocks: d=512, 8 heads, L=256, B=64, 6 blocks, dropout 0.1"
         samples = cfg.B
+    elif name == "C2d":
+        from dataclasses import replace
+        from paper_1805_08899_b200.nmt import NMTModel as M
+        cfg = replace(K.C2, dropout=0.1)
+        params, batch = D.nmt_params(0, cfg, dtype_s), D.nmt_batch(1, cfg)
+        res["workload"] = "C2d NMT (C2 shapes) with embedding dropout p=0.1 (R31): byte / 1-bit / regenerated masks"
+        samples = cfg.B
     else:
         from paper_1805_08899_b200.nmt import NMTModel as M
         Bc5 = 24576 if dtype_s == "bf16" else 16384
@@ -232,9 +239,9 @@ def extra_leg(name, dtype_s, steps=10, warmup=3):
         res["workload"] = f"C5 NMT (C2 shapes) at B={Bc5} per GPU: STASH exceeds HBM, RECOMPUTE fits"
         samples = cfg.B
     plans = [(abi.STASH, "stash", False), (abi.RECOMPUTE, "recompute", False)]
-    if name in ("C3", "C4"):                         # the prior-work Mirror plan on the same kernels
+    if name in ("C3", "C4", "C2d"):                  # the prior-work Mirror plan on the same kernels
         plans.append((abi.RECOMPUTE, "mirror", True))
-    if name == "C4":                                 # Echo's plan with Philox-regenerated masks (R30)
+    if name in ("C4", "C2d"):                        # Echo's plan with Philox-regenerated masks (R30)
         plans.append((abi.RECOMPUTE, "recompute_regen_masks", "regen"))
     for mode, mname, mirror in plans:
         r = {}
@@ -569,7 +576,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the stash comparison, memory and kernel legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--legs", default="C3,C4,C5", help="secondary configs to report (C3,C4,C5; '' for none)")
+    ap.add_argument("--legs", default="C3,C4,C2d,C5", help="secondary configs to report (C3,C4,C2d,C5; '' for none)")
     ap.add_argument("--leg-dtype", default="bf16", choices=["fp32", "bf16"])
     args = ap.parse_args()
     if args.warmup < 3:

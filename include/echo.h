@@ -315,6 +315,27 @@ echo_status echo_xent_fwd_bwd(int32_t N, int32_t V, float* logits, const float* 
 echo_status echo_colsum(int32_t rows, int32_t cols, int64_t ld, int32_t dtype, const void* x, float* out,
                         int32_t accumulate, void* stream);
 
+/* ===================================================================== dropout on the LSTM inputs
+ * Dropout of the NMT embeddings (reading R31, Sockeye's embedding dropout) with the paper's 1-bit
+ * encoding of its feature map (Alg. 1 line 18) or, reading R30, no kept mask:
+ * keep(n) from Philox4x32-10 exactly as a7 (counter offset + n/4, key seed, word n%4, keep iff
+ * (word >> 8) >= floor(p 2^24); R19), scale 1/(1-p) rounded to fp32.
+ *  n          elements, a multiple of 8;  p in [0, 1)
+ *  mask_kind  0: none (regenerated from (seed, offset)), 1: bits [n/8] uint8 (bit k of byte j =
+ *             element 8j + k), 2: bytes [n] uint8 (0/1; 8-byte aligned)
+ * echo_dropout_fwd: y [n] = round_s(x * keep / (1-p)) (x, y in dtype; 16-byte aligned), the keep-
+ *   mask written to mask in mask_kind (mask may be NULL for kind 0).
+ * echo_dropout_apply: y (+)= x * keep / (1-p) with keep DECODED from the kept mask (kinds 1, 2) or
+ *   regenerated (kind 0): re-applies a mirrored dropout (x, y storage dtype) and back-propagates
+ *   through it (x = dLoss/dy, y = dLoss/dx, fp32).  accumulate: 0 overwrite, 1 add (fp32 sum,
+ *   then rounded to y_dtype).  x and y may alias when accumulate is 0.
+ * Device pointers.  Errors: ECHO_ERR_INVALID.                                                     */
+echo_status echo_dropout_fwd(int64_t n, int32_t dtype, float p, uint64_t seed, uint64_t offset, const void* x,
+                             void* y, uint8_t* mask, int32_t mask_kind, void* stream);
+echo_status echo_dropout_apply(int64_t n, float p, uint64_t seed, uint64_t offset, const uint8_t* mask,
+                               int32_t mask_kind, int32_t x_dtype, const void* x, int32_t y_dtype, void* y,
+                               int32_t accumulate, void* stream);
+
 /* Backward of the attention hidden a_t = tanh(pre_t) (reading R7, §2;
  * tanh keeps its output): dpre[i] = da[i] * (1 - a[i]^2), fp32 arithmetic in that
  * order (a read in its storage dtype).  Outside the Echo decision (a_t is kept in both modes).

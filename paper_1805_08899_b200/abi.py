@@ -24,6 +24,7 @@ EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_c
             "echo_lstm_seq_supported", "echo_gemm_f32", "echo_gemm_f32_supported",
             "echo_attn_bwd_deferred", "echo_attn_bwd_finish", "echo_tanh_bwd",
             "echo_lstm_fwd_parts", "echo_lstm_cscan_parts", "echo_lstm_bwd_parts",
+            "echo_dropout_fwd", "echo_dropout_apply",
             "echo_footprint_estimate")
 
 
@@ -85,6 +86,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_lstm_seq_fwd": [ctypes.POINTER(LstmDesc), i32, i32, i32, i32] + [vp] * 7 + [i32, vp, vp, vp],
         "echo_colsum": [i32, i32, ctypes.c_int64, i32, vp, vp, i32, vp],
         "echo_tanh_bwd": [ctypes.c_int64, i32, vp, vp, vp, vp],
+        "echo_dropout_fwd": [ctypes.c_int64, i32, ctypes.c_float, u64, u64, vp, vp, vp, i32, vp],
+        "echo_dropout_apply": [ctypes.c_int64, ctypes.c_float, u64, u64, vp, i32, i32, vp, i32, vp, i32, vp],
         "echo_lstm_fwd_parts": [ctypes.POINTER(LstmDesc), i32, vp, ctypes.c_int64] + [vp] * 5,
         "echo_lstm_cscan_parts": [ctypes.POINTER(LstmDesc), i32, i32, vp, ctypes.c_int64, ctypes.c_int64] + [vp] * 4,
         "echo_lstm_bwd_parts": [ctypes.POINTER(LstmDesc), i32, vp, ctypes.c_int64] + [vp] * 7,
@@ -236,6 +239,29 @@ def echo_lstm_bwd_parts(d, n_parts, parts_t, part_stride, bias, c_prev, c_t, dh_
     LAUNCHES["count"] += 1
     _check(load().echo_lstm_bwd_parts(ctypes.byref(d), int(n_parts), _p(parts_t), int(part_stride), _p(bias),
                                       _p(c_prev), _p(c_t), _p(dh_t), _p(dc), _p(dA_t), _stream(stream)))
+
+
+MASK_NONE, MASK_BITS, MASK_BYTES = 0, 1, 2
+
+
+def _dt(t):
+    import torch
+    return FP32 if t.dtype == torch.float32 else BF16
+
+
+def echo_dropout_fwd(p, seed, offset, x, y, mask=None, mask_kind=MASK_NONE, stream=None):
+    """y = dropout(x) (same dtype, contiguous); the keep-mask optionally kept as bits / bytes."""
+    LAUNCHES["count"] += 1
+    _check(load().echo_dropout_fwd(x.numel(), _dt(x), float(p), int(seed), int(offset), _p(x), _p(y), _p(mask),
+                                   int(mask_kind), _stream(stream)))
+
+
+def echo_dropout_apply(p, seed, offset, mask, mask_kind, x, y, accumulate=0, stream=None):
+    """y (+)= x * keep / (1-p), keep decoded from the kept mask (or regenerated for MASK_NONE)."""
+    assert x.numel() == y.numel()
+    LAUNCHES["count"] += 1
+    _check(load().echo_dropout_apply(x.numel(), float(p), int(seed), int(offset), _p(mask), int(mask_kind), _dt(x),
+                                     _p(x), _dt(y), _p(y), int(accumulate), _stream(stream)))
 
 
 def echo_tanh_bwd(a, da, dpre, stream=None):

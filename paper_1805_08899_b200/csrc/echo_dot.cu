@@ -16,32 +16,7 @@
 
 namespace echo {
 
-struct U4 { uint32_t x, y, z, w; };
-
-__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
-    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
-  }
-  return c;
-}
-
-// keep-bits of the 8 elements n0..n0+7 (n0 % 8 == 0), bit k = element n0 + k
-__device__ __forceinline__ uint32_t keep_bits8(uint64_t seed, uint64_t offset, uint64_t n0, uint32_t thr) {
-  const uint64_t q = offset + (n0 >> 2);
-  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-  const U4 a = philox4x32_10(U4{(uint32_t)q, (uint32_t)(q >> 32), 0u, 0u}, k0, k1);
-  const uint64_t q1 = q + 1;
-  const U4 b = philox4x32_10(U4{(uint32_t)q1, (uint32_t)(q1 >> 32), 0u, 0u}, k0, k1);
-  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-  uint32_t bits = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) bits |= ((w[k] >> 8) >= thr ? 1u : 0u) << k;
-  return bits;
-}
+// Philox4x32-10 and keep_bits8 live in echo_common.cuh (shared with the embedding dropout)
 
 template <typename T> __device__ __forceinline__ void ld8(const T* p, float (&o)[8]);
 template <> __device__ __forceinline__ void ld8<float>(const float* p, float (&o)[8]) {

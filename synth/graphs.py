@@ -185,9 +185,14 @@ def nmt(cfg, s="f32"):
     Wch = g.placeholder("att.Wch", [H, H], s, trainable=True)
     Wo = g.placeholder("out.Wo", [V, H], s, trainable=True)
     bo = g.placeholder("out.bo", [V], "f32", trainable=True)
+    p = getattr(cfg, "dropout", 0.0)
+
+    def drop(x):                                         # R31: embedding dropout (keep-mask = output 1)
+        return g.op("dropout", [x], tag="embed", nout=2, p=p)[0] if p > 0 else x
+
     # encoder
-    xs = [g.op("embedding", [g.op("slice", [src], tag="embed", axis=0, begin=t, end=t + 1, squeeze=1), emb_s],
-               tag="embed") for t in range(Ts)]
+    xs = [drop(g.op("embedding", [g.op("slice", [src], tag="embed", axis=0, begin=t, end=t + 1, squeeze=1), emb_s],
+                    tag="embed")) for t in range(Ts)]
     for l in range(cfg.enc_layers):
         Wx, Wh, b = enc[l]
         h, c = h0, c0
@@ -205,8 +210,8 @@ def nmt(cfg, s="f32"):
     a_prev = None
     a_all = []
     for t in range(Td):
-        e_t = g.op("embedding", [g.op("slice", [tgt], tag="embed", axis=0, begin=t, end=t + 1, squeeze=1), emb_t],
-                   tag="embed")
+        e_t = drop(g.op("embedding", [g.op("slice", [tgt], tag="embed", axis=0, begin=t, end=t + 1, squeeze=1), emb_t],
+                        tag="embed"))
         x = None
         for l in range(cfg.dec_layers):
             if l == 0:

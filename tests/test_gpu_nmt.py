@@ -192,3 +192,84 @@ def test_nmt_mirror_plan_parity_and_graph(cfg, storage, cuda_dev):
     m.replay()
     torch.cuda.synchronize()
     assert bits_equal(m.gflat, eager)
+
+
+RAGGED_DROP = NMTConfig("ragged-drop", B=5, Ts=11, Td=7, E=24, H=40, A=32, V=50, enc_layers=2, dec_layers=2,
+                        dropout=0.2)
+
+
+C1_DROP = NMTConfig("C1-drop", B=2, Ts=4, Td=4, E=16, H=16, A=16, V=32, enc_layers=1, dec_layers=1, dropout=0.3)
+
+
+@pytest.mark.parametrize("cfg,storage", [(C1_DROP, "fp32"), (RAGGED_DROP, "fp32"), (RAGGED_DROP, "bf16")],
+                         ids=lambda x: getattr(x, "name", x))
+def test_nmt_embedding_dropout_plans(cfg, storage, cuda_dev):
+    """R31 embedding dropout on the GPU: every plan (STASH with byte masks, Echo with 1-bit masks,
+    Echo with regenerated masks, Mirror) matches the fp64 oracle; STASH == Echo == Echo-regen
+    bitwise; the kept bytes equal the estimator's for each plan."""
+    import json
+    from paper_1805_08899_b200 import abi
+    from paper_1805_08899_b200.nmt import NMTModel
+    from synth import graphs as Gr
+    params = nmt_params(11, cfg, storage)
+    batch = nmt_batch(12, cfg, lengths="random")
+    ref = O.step(params, batch, cfg)
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    tol = 1e-4 if storage == "fp32" else 2e-2
+    metric = relerr if storage == "fp32" else relerr_fro
+    doc = json.dumps(Gr.nmt(cfg, "f32" if storage == "fp32" else "bf16"))
+    plans = {"stash": (abi.STASH, False, False, "baseline"), "echo": (abi.RECOMPUTE, False, False, "echo"),
+             "echo-regen": (abi.RECOMPUTE, False, True, "echo"), "mirror": (abi.RECOMPUTE, True, False, "mirror")}
+    res = {}
+    for name, (mode, mirror, regen, strat) in plans.items():
+        m = NMTModel(cfg, dt, mode, mirror=mirror, regen_masks=regen)
+        m.load_params(params)
+        m.upload_batch(batch)
+        acts = m._forward()
+        rep = json.loads(abi.echo_footprint_estimate(doc, json.dumps({"strategy": strat, "regenerate_masks": regen})))
+        assert m.stash_bytes() == rep["stash_bytes"], (name, m.stash_bytes(), rep["stash_bytes"])
+        m._backward(acts)
+        del acts
+        loss = float(m.loss.item())
+        assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"]), (name, loss, ref["loss"])
+        g = m.grads_numpy()
+        for k, v in ref["grads"].items():
+            assert metric(g[k], v) <= tol, (name, k, metric(g[k], v))
+        res[name] = m.gflat.clone()
+    assert bits_equal(res["stash"], res["echo"]) and bits_equal(res["stash"], res["echo-regen"])
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("n,p", [(8, 0.1), (6400 * 24, 0.2), (128 * 50 * 512, 0.1), (64, 0.0)])
+def test_dropout_kernels(storage, n, p, cuda_dev):
+    """echo_dropout_fwd / _apply: keep-mask bit-exact vs the oracle's Philox (integer decision),
+    bytes / bits / regenerated decode the same mask, y = x * keep / (1 - p) exactly in fp32."""
+    from paper_1805_08899_b200 import abi
+    from oracle.dot_softmax import dropout_keep_mask
+    sd = torch.float32 if storage == "fp32" else torch.bfloat16
+    seed, off = 0x0DDB_A11C_AFE5, 6
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randn(n, device="cuda", generator=g).to(sd)
+    keep = dropout_keep_mask(seed, off, n, p)
+    ik = np.float32(1.0 / (1.0 - p))
+    ref = (x.float() * torch.from_numpy(np.where(keep, ik, np.float32(0.0))).cuda()).to(sd)
+    outs = {}
+    dy = torch.randn(n, device="cuda", generator=g)
+    for kind in (abi.MASK_NONE, abi.MASK_BITS, abi.MASK_BYTES):
+        mask = None if kind == abi.MASK_NONE else torch.empty(n if kind == abi.MASK_BYTES else n // 8,
+                                                             dtype=torch.uint8, device="cuda")
+        y = torch.empty_like(x)
+        abi.echo_dropout_fwd(p, seed, off, x, y, mask, kind)
+        assert bits_equal(y, ref)
+        if kind == abi.MASK_BITS:
+            assert np.array_equal(np.unpackbits(mask.cpu().numpy(), bitorder="little").astype(bool), keep)
+        if kind == abi.MASK_BYTES:
+            assert np.array_equal(mask.cpu().numpy().astype(bool), keep)
+        y2 = torch.empty_like(x)
+        abi.echo_dropout_apply(p, seed, off, mask, kind, x, y2, 0)       # re-applied mask == forward
+        assert bits_equal(y2, y)
+        dx = dy.clone()
+        abi.echo_dropout_apply(p, seed, off, mask, kind, dx, dx, 0)      # backward, in place
+        outs[kind] = dx
+        assert bits_equal(dx, dy * torch.from_numpy(np.where(keep, ik, np.float32(0.0))).cuda())
+    assert bits_equal(outs[abi.MASK_NONE], outs[abi.MASK_BITS]) and bits_equal(outs[abi.MASK_BITS], outs[abi.MASK_BYTES])
