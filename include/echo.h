@@ -239,6 +239,17 @@ echo_status echo_attn_bwd_finish(const echo_attn_desc* d, int32_t Td, const void
                                  const float* ds_all, const float* alpha_all, const float* dctx_all,
                                  float* dKp, float* dHs, void* stream);
 
+/* One decoder step of the deferred accumulation, added to the running sums: dKp[b,s,:] += dE_t and
+ * dH_s[b,s,:] += alpha_t[b,s] dctx_t[b,:] for s < len_b (rows s >= len_b untouched), with exactly
+ * the per-step expressions of echo_attn_bwd (same bits when called for t = Td-1 .. 0 in order).
+ * Lets the caller run the read-modify-write of step t OFF the critical path (e.g. on a second
+ * stream after echo_attn_bwd_deferred of step t) while the recurrence continues.
+ *  qp_t [B,A], E_st_t [B,Ts,A] (STASH), ds_t / alpha_t [B,Ts] fp32, dctx_t [B,Hk] fp32: step t's rows. */
+echo_status echo_attn_bwd_accumulate(const echo_attn_desc* d, const void* qp_t, const void* Kp, const void* E_st_t,
+                                     const void* v, const int32_t* src_len, const float* ds_t,
+                                     const float* alpha_t, const float* dctx_t, float* dKp, float* dHs,
+                                     void* stream);
+
 /* dv[a] (+)= sum_b dv_part[b,a] in ascending b (deterministic).  accumulate != 0 adds to dv. */
 echo_status echo_attn_dv_reduce(int32_t B, int32_t A, const float* dv_part, float* dv,
                                 int32_t accumulate, void* stream);

@@ -22,7 +22,7 @@ EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_c
             "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
             "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum", "echo_lstm_seq_fwd",
             "echo_lstm_seq_supported", "echo_gemm_f32", "echo_gemm_f32_supported",
-            "echo_attn_bwd_deferred", "echo_attn_bwd_finish", "echo_tanh_bwd",
+            "echo_attn_bwd_deferred", "echo_attn_bwd_finish", "echo_attn_bwd_accumulate", "echo_tanh_bwd",
             "echo_lstm_fwd_parts", "echo_lstm_cscan_parts", "echo_lstm_bwd_parts",
             "echo_dropout_fwd", "echo_dropout_apply",
             "echo_footprint_estimate")
@@ -78,6 +78,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_attn_dv_reduce": [i32, i32, vp, vp, i32, vp],
         "echo_attn_bwd_deferred": [ctypes.POINTER(AttnDesc)] + [vp] * 14,
         "echo_attn_bwd_finish": [ctypes.POINTER(AttnDesc), i32] + [vp] * 11,
+        "echo_attn_bwd_accumulate": [ctypes.POINTER(AttnDesc)] + [vp] * 11,
         "echo_dot_softmax_fwd": [ctypes.POINTER(DotDesc)] + [vp] * 5,
         "echo_dot_softmax_bwd": [ctypes.POINTER(DotDesc)] + [vp] * 7,
         "echo_xent_fwd_bwd": [i32, i32, vp, vp, vp, vp, vp, vp],
@@ -214,6 +215,12 @@ def echo_attn_bwd_finish(d, Td, qp_all, Kp, E_st_all, v, src_len, ds_all, alpha_
     LAUNCHES["count"] += 2
     _check(load().echo_attn_bwd_finish(ctypes.byref(d), Td, _p(qp_all), _p(Kp), _p(E_st_all), _p(v), _p(src_len),
                                        _p(ds_all), _p(alpha_all), _p(dctx_all), _p(dKp), _p(dHs), _stream(stream)))
+
+
+def echo_attn_bwd_accumulate(d, qp_t, Kp, E_st_t, v, src_len, ds_t, alpha_t, dctx_t, dKp, dHs, stream=None):
+    LAUNCHES["count"] += 2
+    _check(load().echo_attn_bwd_accumulate(ctypes.byref(d), _p(qp_t), _p(Kp), _p(E_st_t), _p(v), _p(src_len),
+                                           _p(ds_t), _p(alpha_t), _p(dctx_t), _p(dKp), _p(dHs), _stream(stream)))
 
 
 def echo_xent_fwd_bwd(N, V, logits, bias, labels, row_loss, dlogits_bf16=None, stream=None):

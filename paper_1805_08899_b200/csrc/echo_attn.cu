@@ -1023,7 +1023,8 @@ __global__ void __launch_bounds__(256) attn_dkp_finish_kernel(echo_attn_desc d, 
                                                               const T* __restrict__ Kp, const T* __restrict__ Z_all,
                                                               const T* __restrict__ v,
                                                               const int32_t* __restrict__ src_len,
-                                                              const float* __restrict__ ds_all, float* __restrict__ dKp) {
+                                                              const float* __restrict__ ds_all, float* __restrict__ dKp,
+                                                              int accumulate) {
   pdl_wait();
   extern __shared__ float fsm[];
   const int A = d.A, Ts = d.Ts, B = d.B;
@@ -1045,7 +1046,8 @@ __global__ void __launch_bounds__(256) attn_dkp_finish_kernel(echo_attn_desc d, 
   if (a >= A) return;
   const float vc = to_f(v[a]);
   for (int s = tid / FIN_COLS; s < Ts; s += 256 / FIN_COLS) {
-    float acc = 0.0f;
+    if (accumulate && s >= n) continue;                        // masked rows untouched (per-step RMW)
+    float acc = accumulate ? dKp[(long)b * d.kp_stride_b + (long)s * d.kp_stride_s + a] : 0.0f;
     if (s < n) {
       const float kz = rec ? to_f(Kp[(long)b * d.kp_stride_b + (long)s * d.kp_stride_s + a]) : 0.0f;
       for (int t = Td - 1; t >= 0; --t) {
@@ -1064,7 +1066,7 @@ __global__ void __launch_bounds__(256) attn_dhs_finish_kernel(echo_attn_desc d, 
                                                               const int32_t* __restrict__ src_len,
                                                               const float* __restrict__ al_all,
                                                               const float* __restrict__ dctx_all,
-                                                              float* __restrict__ dHs) {
+                                                              float* __restrict__ dHs, int accumulate) {
   pdl_wait();
   extern __shared__ float fsm[];
   const int Hk = d.Hk, Ts = d.Ts, B = d.B;
@@ -1084,7 +1086,8 @@ __global__ void __launch_bounds__(256) attn_dhs_finish_kernel(echo_attn_desc d, 
   const int c = tid % FIN_COLS, h = h0 + c;
   if (h >= Hk) return;
   for (int s = tid / FIN_COLS; s < Ts; s += 256 / FIN_COLS) {
-    float acc = 0.0f;
+    if (accumulate && s >= n) continue;
+    float acc = accumulate ? dHs[(long)b * d.hs_stride_b + (long)s * d.hs_stride_s + h] : 0.0f;
     if (s < n)
       for (int t = Td - 1; t >= 0; --t) acc = __fmaf_rn(als[t * Ts + s], cs[t * FIN_COLS + c], acc);
     dHs[(long)b * d.hs_stride_b + (long)s * d.hs_stride_s + h] = acc;
@@ -1390,11 +1393,10 @@ extern "C" echo_status echo_attn_bwd_deferred(const echo_attn_desc* d, const voi
                        ds_out, alpha_out, stream);
 }
 
-extern "C" echo_status echo_attn_bwd_finish(const echo_attn_desc* d, int32_t Td, const void* qp_all, const void* Kp,
-                                            const void* E_st_all, const void* v, const int32_t* src_len,
-                                            const float* ds_all, const float* alpha_all, const float* dctx_all,
-                                            float* dKp, float* dHs, void* stream) {
-  const char* fn = "echo_attn_bwd_finish";
+static echo_status finish_impl(const char* fn, const echo_attn_desc* d, int32_t Td, const void* qp_all,
+                               const void* Kp, const void* E_st_all, const void* v, const int32_t* src_len,
+                               const float* ds_all, const float* alpha_all, const float* dctx_all, float* dKp,
+                               float* dHs, int accumulate, void* stream) {
   echo_status s = check_attn(fn, d);
   if (s) return s;
   if (Td <= 0) return fail(ECHO_ERR_INVALID, "%s: Td=%d", fn, Td);
@@ -1413,20 +1415,36 @@ extern "C" echo_status echo_attn_bwd_finish(const echo_attn_desc* d, int32_t Td,
     if ((s = set_smem((const void*)attn_dkp_finish_kernel<float>, smem, fn))) return s;
     e = launch(attn_dkp_finish_kernel<float>, dim3((d->A + FIN_COLS - 1) / FIN_COLS, d->B), dim3(256), smem, st, 1, *d,
                (int)Td, (const float*)qp_all, (const float*)Kp, rec ? nullptr : (const float*)E_st_all,
-               (const float*)v, src_len, ds_all, dKp);
+               (const float*)v, src_len, ds_all, dKp, accumulate);
   } else {
     typedef __nv_bfloat16 bf;
     if ((s = set_smem((const void*)attn_dkp_finish_kernel<bf>, smem, fn))) return s;
     e = launch(attn_dkp_finish_kernel<bf>, dim3((d->A + FIN_COLS - 1) / FIN_COLS, d->B), dim3(256), smem, st, 1, *d,
                (int)Td, (const bf*)qp_all, (const bf*)Kp, rec ? nullptr : (const bf*)E_st_all, (const bf*)v, src_len,
-               ds_all, dKp);
+               ds_all, dKp, accumulate);
   }
   if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   if ((s = set_smem((const void*)attn_dhs_finish_kernel, smem, fn))) return s;
   e = launch(attn_dhs_finish_kernel, dim3((d->Hk + FIN_COLS - 1) / FIN_COLS, d->B), dim3(256), smem, st, 1, *d,
-             (int)Td, src_len, alpha_all, dctx_all, dHs);
+             (int)Td, src_len, alpha_all, dctx_all, dHs, accumulate);
   if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);
+}
+
+extern "C" echo_status echo_attn_bwd_finish(const echo_attn_desc* d, int32_t Td, const void* qp_all, const void* Kp,
+                                            const void* E_st_all, const void* v, const int32_t* src_len,
+                                            const float* ds_all, const float* alpha_all, const float* dctx_all,
+                                            float* dKp, float* dHs, void* stream) {
+  return finish_impl("echo_attn_bwd_finish", d, Td, qp_all, Kp, E_st_all, v, src_len, ds_all, alpha_all, dctx_all,
+                     dKp, dHs, 0, stream);
+}
+
+extern "C" echo_status echo_attn_bwd_accumulate(const echo_attn_desc* d, const void* qp_t, const void* Kp,
+                                                const void* E_st_t, const void* v, const int32_t* src_len,
+                                                const float* ds_t, const float* alpha_t, const float* dctx_t,
+                                                float* dKp, float* dHs, void* stream) {
+  return finish_impl("echo_attn_bwd_accumulate", d, 1, qp_t, Kp, E_st_t, v, src_len, ds_t, alpha_t, dctx_t, dKp, dHs,
+                     1, stream);
 }
 
 #ifdef ECHO_PHASE_TIMING

@@ -150,19 +150,28 @@ def test_stash_bytes_equal_estimator(cfg, storage, cuda_dev):
 @pytest.mark.parametrize("cfg,storage", [(SMALL_NMT, "fp32"), (RAGGED, "bf16"), (C2, "bf16")],
                          ids=["small-fp32", "ragged-bf16", "C2-bf16"])
 def test_nmt_deferred_a6_bitwise(cfg, storage, cuda_dev, monkeypatch):
-    """The deferred dKp / dH_s accumulation gives bit-identical gradients to the per-step one."""
+    """The deferred dKp / dH_s accumulation (after the loop, or per step on a side stream: split a6)
+    gives bit-identical gradients to the per-step read-modify-write."""
     from paper_1805_08899_b200 import abi
     params = nmt_params(21, cfg, storage)
     batch = nmt_batch(22, cfg, lengths="random")
     dt = abi.FP32 if storage == "fp32" else abi.BF16
     out = {}
-    for flag in ("0", "1"):
-        monkeypatch.setenv("ECHO_A6_DEFERRED", flag)
+    for flag in ("0", "1", "split"):
+        monkeypatch.setenv("ECHO_A6_DEFERRED", "1" if flag == "1" else "0")
+        monkeypatch.setenv("ECHO_A6_SPLIT", "1" if flag == "split" else "0")
         for mode in (abi.STASH, abi.RECOMPUTE):
             m, _ = _run(cfg, params, batch, dt, mode)
             out[(flag, mode)] = m.gflat.clone()
+            if flag == "split":                  # the side-stream branch inside the step graph
+                m.capture(0.0)
+                m.gflat.zero_()
+                m.replay()
+                torch.cuda.synchronize()
+                assert bits_equal(m.gflat, out[(flag, mode)]), mode
     for mode in (abi.STASH, abi.RECOMPUTE):
         assert bits_equal(out[("0", mode)], out[("1", mode)]), mode
+        assert bits_equal(out[("0", mode)], out[("split", mode)]), mode
 
 
 @pytest.mark.parametrize("cfg,storage", [(C1, "fp32"), (SMALL_NMT, "fp32"), (RAGGED, "fp32"), (RAGGED, "bf16")],
