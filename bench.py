@@ -202,6 +202,30 @@ def time_attn_bwd(cfg, dtype, reps=20):
     return {"ms": ms, "bytes": nbytes, "bytes_per_row": nbytes / rows, "rows": rows}
 
 
+def c5_a6_roofline(m, cfg, dt, reps=2):
+    """a6 launch duration inside the C5 step (probed re-capture: the timed graph is released first)."""
+    import gc
+    import torch
+    m.graph = None
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    m.capture(0.01, warmup=1, with_probe=True)
+    m.replay()
+    lt = []
+    for _ in range(reps):
+        m.replay()
+        lt.extend(m.kernel_times().get("attn_bwd", []))
+    nbytes, rows = attn_bwd_bytes(cfg, dt)
+    pk = _peaks()
+    l_ms = statistics.mean(lt)
+    ach = nbytes / (l_ms / 1e3) / 1e9
+    return {"kernel": "echo_attn_bwd (a6, RECOMPUTE)", "launch_us": 1e3 * l_ms, "bytes_per_launch": nbytes,
+            "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
+            "timing": "CUDA events on the launch stream around each of the 50 a6 launches per step, inside "
+                      "replays of the C5 step graph (event-record nodes)"}
+
+
 def extra_leg(name, dtype_s, steps=10, warmup=3):
     """Secondary configs (BASELINE.json configs[2..4]): device-timed steps of both modes (CUDA graph),
     exact stash bytes and allocator peak per mode.  C5 = C2 shapes at a per-GPU batch where STASH
@@ -272,6 +296,11 @@ def extra_leg(name, dtype_s, steps=10, warmup=3):
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / steps
             r.update({"ms_per_step": ms, "samples_per_s": samples / (ms / 1e3), "steps": steps, "cuda_graph": True})
+            if name == "C5" and mname == "recompute":       # a6 in-step roofline where the batch fills HBM
+                try:
+                    r["a6_roofline"] = c5_a6_roofline(m, cfg, dt)
+                except torch.OutOfMemoryError as ex:
+                    r["a6_roofline"] = {"error": str(ex).split("\n")[0][:120]}
         except torch.OutOfMemoryError as ex:
             r["oom"] = str(ex).split("\n")[0][:160]
         finally:
@@ -419,7 +448,7 @@ def run_ours(args):
     ms2 = dp.max_over_ranks(a.elapsed_time(b) / args.steps, dev)
     clocks = sampler.stop()
     ms = min(ms, ms2)
-    e2e_s = e2e(model, use_graph, max(4, args.steps // 2))
+    e2e_s = e2e(model, use_graph, max(10, args.steps))
     in_bytes = model.input_bytes()
     del model
     torch.cuda.empty_cache()
