@@ -565,6 +565,28 @@ __device__ __forceinline__ float score_partial(const T* kz_row, const T* qps, co
   return warp_sum(acc);
 }
 
+// score_partial for the TMA kernels, whose column slices are <= 128 wide (W / 4 <= 32: one 4-column
+// group per lane): the lane's qp / v values are loaded into registers once per CTA instead of once
+// per position.  Same operations in the same order as score_partial (bit-identical).
+template <typename T>
+__device__ __forceinline__ float score_partial_r(const T* kz_row, const float (&qr)[4], const float (&vr)[4], bool act,
+                                                 int c4, bool add_qp, T* z_out, float* e_out) {
+  float acc = 0.0f;
+  if (act) {
+    float kz[4], z[4], e[4];
+    lds4(kz_row + c4 * 4, kz);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      z[k] = z_of<T>(add_qp ? qr[k] : 0.0f, kz[k], add_qp);
+      e[k] = tanhf(z[k]);
+      acc = __fmaf_rn(e[k], vr[k], acc);
+    }
+    if (z_out) stg4(z_out + c4 * 4, z);
+    if (e_out) *reinterpret_cast<float4*>(e_out + c4 * 4) = make_float4(e[0], e[1], e[2], e[3]);
+  }
+  return warp_sum(acc);
+}
+
 // rank-ordered gather of the C partial vectors part_c[0..n) into out[0..n)
 __device__ __forceinline__ void gather_sum(cg::cluster_group& cl, float* part, float* out, int n, int C, int tid) {
   for (int s = tid; s < n; s += ATT_THREADS) {
@@ -763,13 +785,19 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
   }
   __syncthreads();                                            // barrier init visible before anyone waits
   mbar_wait(&bar[0], 0);                                      // chunk 0 + the qp / v slices
+  const bool act = lane < W / 4;                              // W <= 128: one column group per lane
+  float qr[4] = {0.0f, 0.0f, 0.0f, 0.0f}, vr[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  if (act) {
+    lds4(qps + lane * 4, qr);
+    lds4(vs + lane * 4, vr);
+  }
   for (int k = 0, s = w; k * R < n; ++k) {                   // chunk by chunk: one wait per chunk
     const int s1 = min(n, (k + 1) * R);
     if (s >= s1) continue;
     mbar_wait(&bar[k], 0);
     for (; s < s1; s += ATT_WARPS) {
       T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
-      const float p = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, true, z_out, nullptr);
+      const float p = score_partial_r<T>(kz + (size_t)s * Wb, qr, vr, act, lane, true, z_out, nullptr);
       if (lane == 0) sc_part[s] = p;
     }
   }
@@ -871,20 +899,29 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   ECHO_PHASE(1);
   if (n > 0) mbar_wait(&bar[0], 0);
   ECHO_PHASE(2);
-  // phase 1: E = tanh(z) into smem (fp32), partial scores (RECOMPUTE) and partial dalpha
+  // phase 1: E = tanh(z) into smem (fp32), partial scores (RECOMPUTE) and partial dalpha.  The
+  // slices are <= 128 columns wide, so each lane owns one 4-column group of A and of Hk: its qp, v
+  // and dctx values stay in registers across the positions
+  const bool actA = lane < W / 4, actH = lane < WH / 4;
+  float qr[4] = {0.0f, 0.0f, 0.0f, 0.0f}, vr[4] = {0.0f, 0.0f, 0.0f, 0.0f}, dr[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  if (actA) {
+    if (recompute) lds4(qps + lane * 4, qr);
+    lds4(vs + lane * 4, vr);
+  }
+  if (actH) lds4(dcs + lane * 4, dr);
   for (int k = 0, s = w; k * R < n; ++k) {                   // chunk by chunk: one wait per chunk
     const int s1 = min(n, (k + 1) * R);
     if (s >= s1) continue;
     mbar_wait(&bar[k], 0);
     for (; s < s1; s += ATT_WARPS) {
-      const float ps = score_partial<T>(kz + (size_t)s * Wb, qps, vs, W, lane, recompute, nullptr, E + (size_t)s * Wb);
+      const float ps = score_partial_r<T>(kz + (size_t)s * Wb, qr, vr, actA, lane, recompute, nullptr,
+                                          E + (size_t)s * Wb);
       float acc = 0.0f;
-      const T* hrow = hs + (size_t)s * WHb;
-      for (int c4 = lane; c4 < WH / 4; c4 += 32) {
+      if (actH) {
         float h4[4];
-        lds4(hrow + c4 * 4, h4);
+        lds4(hs + (size_t)s * WHb + lane * 4, h4);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc = __fmaf_rn(dcs[c4 * 4 + q], h4[q], acc);
+        for (int q = 0; q < 4; ++q) acc = __fmaf_rn(dr[q], h4[q], acc);
       }
       acc = warp_sum(acc);
       if (lane == 0) {
