@@ -587,6 +587,34 @@ __device__ __forceinline__ float score_partial_r(const T* kz_row, const float (&
   return warp_sum(acc);
 }
 
+// Per-lane partials of GR row slots -> full warp sums with log2(GR) halving exchanges (each lane
+// keeps the half of its slots picked by one lane bit) and 5 - log2(GR) butterflies: GR - 1 + 5 -
+// log2(GR) shuffles instead of 5 GR.  Every slot's sum is formed by the SAME pairwise tree as
+// warp_sum (partners at xor 16, 8, 4, 2, 1, IEEE addition commutes), so it is bitwise equal to
+// warp_sum of that slot.  Returns the sum of slot lane >> (5 - log2(GR)).
+template <int GR>
+__device__ __forceinline__ float reduce_scatter(float (&p)[GR], int lane) {
+  static_assert(GR == 2 || GR == 4 || GR == 8, "GR");
+  constexpr int LG = GR == 2 ? 1 : GR == 4 ? 2 : 3;
+#pragma unroll
+  for (int st = 0, n = GR; st < LG; ++st) {
+    const int o = 16 >> st;
+    const bool hi = (lane & o) != 0;
+    n >>= 1;
+#pragma unroll
+    for (int i = 0; i < GR / 2; ++i)
+      if (i < n) {
+        const float send = hi ? p[i] : p[i + n];
+        const float keep = hi ? p[i + n] : p[i];
+        p[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
+      }
+  }
+  float x = p[0];
+#pragma unroll
+  for (int o = 16 >> LG; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
 // rank-ordered gather of the C partial vectors part_c[0..n) into out[0..n)
 __device__ __forceinline__ void gather_sum(cg::cluster_group& cl, float* part, float* out, int n, int C, int tid) {
   for (int s = tid; s < n; s += ATT_THREADS) {
@@ -909,25 +937,44 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     lds4(vs + lane * 4, vr);
   }
   if (actH) lds4(dcs + lane * 4, dr);
-  for (int k = 0, s = w; k * R < n; ++k) {                   // chunk by chunk: one wait per chunk
-    const int s1 = min(n, (k + 1) * R);
-    if (s >= s1) continue;
-    mbar_wait(&bar[k], 0);
-    for (; s < s1; s += ATT_WARPS) {
-      const float ps = score_partial_r<T>(kz + (size_t)s * Wb, qr, vr, actA, lane, recompute, nullptr,
-                                          E + (size_t)s * Wb);
-      float acc = 0.0f;
-      if (actH) {
-        float h4[4];
-        lds4(hs + (size_t)s * WHb + lane * 4, h4);
+  // rows s = w, w + 8, ... of this warp in groups of GR: per-lane partials first, then one
+  // reduce_scatter per quantity (bitwise equal to a warp_sum per row)
+  constexpr int GR = 4;
+  for (int s0 = w; s0 < n; s0 += GR * ATT_WARPS) {
+    float psc[GR], pda[GR];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc = __fmaf_rn(dr[q], h4[q], acc);
+    for (int j = 0; j < GR; ++j) {
+      const int s = s0 + j * ATT_WARPS;
+      psc[j] = 0.0f;
+      pda[j] = 0.0f;
+      if (s < n) {
+        mbar_wait(&bar[s / R], 0);                            // the chunk holding row s has landed
+        if (actA) {
+          float kzv[4], z[4], e[4];
+          lds4(kz + (size_t)s * Wb + lane * 4, kzv);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            z[q] = z_of<T>(recompute ? qr[q] : 0.0f, kzv[q], recompute);
+            e[q] = tanhf(z[q]);
+            psc[j] = __fmaf_rn(e[q], vr[q], psc[j]);
+          }
+          *reinterpret_cast<float4*>(E + (size_t)s * Wb + lane * 4) = make_float4(e[0], e[1], e[2], e[3]);
+        }
+        if (actH) {
+          float h4[4];
+          lds4(hs + (size_t)s * WHb + lane * 4, h4);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pda[j] = __fmaf_rn(dr[q], h4[q], pda[j]);
+        }
       }
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        sc_part[s] = ps;
-        dal_part[s] = acc;
-      }
+    }
+    const float ps = reduce_scatter<GR>(psc, lane);
+    const float pd = reduce_scatter<GR>(pda, lane);
+    const int j = lane >> 3;                                  // slot whose sums this lane holds
+    const int s = s0 + j * ATT_WARPS;
+    if ((lane & 7) == 0 && s < n) {
+      sc_part[s] = ps;
+      dal_part[s] = pd;
     }
   }
   // L2 prefetch of the dKp / dH_s tiles phase 4 streams, issued by thread 0 once this CTA's loads
