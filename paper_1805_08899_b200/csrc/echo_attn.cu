@@ -939,7 +939,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   if (actH) lds4(dcs + lane * 4, dr);
   // rows s = w, w + 8, ... of this warp in groups of GR: per-lane partials first, then one
   // reduce_scatter per quantity (bitwise equal to a warp_sum per row)
-  constexpr int GR = 4;
+  constexpr int GR = 8;
   for (int s0 = w; s0 < n; s0 += GR * ATT_WARPS) {
     float psc[GR], pda[GR];
 #pragma unroll
@@ -970,9 +970,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     }
     const float ps = reduce_scatter<GR>(psc, lane);
     const float pd = reduce_scatter<GR>(pda, lane);
-    const int j = lane >> 3;                                  // slot whose sums this lane holds
+    constexpr int SH = GR == 8 ? 2 : GR == 4 ? 3 : 4;         // slot of lane: lane >> (5 - log2 GR)
+    const int j = lane >> SH;
     const int s = s0 + j * ATT_WARPS;
-    if ((lane & 7) == 0 && s < n) {
+    if ((lane & ((1 << SH) - 1)) == 0 && s < n) {
       sc_part[s] = ps;
       dal_part[s] = pd;
     }
