@@ -630,14 +630,25 @@ __device__ __forceinline__ void gather_sum(cg::cluster_group& cl, float* part, f
 }
 
 // softmax of sc[0..n) into al[0..n) by ONE warp (max-subtracted, fixed order)
+// (TMA kernels: n <= 256, so each lane keeps its <= 8 exponentials in registers between the sum and
+// the normalisation instead of evaluating expf twice; same values, same order)
 __device__ __forceinline__ void softmax_row_warp(const float* sc, float* al, int n, int lane) {
   float m = -INFINITY;
   for (int s = lane; s < n; s += 32) m = fmaxf(m, sc[s]);
   m = warp_max(m);
-  float l = 0.0f;
-  for (int s = lane; s < n; s += 32) l = __fadd_rn(l, expf(__fsub_rn(sc[s], m)));
+  float l = 0.0f, ev[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int s = lane + 32 * k;
+    ev[k] = s < n ? expf(__fsub_rn(sc[s], m)) : 0.0f;
+    if (s < n) l = __fadd_rn(l, ev[k]);
+  }
   l = warp_sum(l);
-  for (int s = lane; s < n; s += 32) al[s] = __fdiv_rn(expf(__fsub_rn(sc[s], m)), l);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int s = lane + 32 * k;
+    if (s < n) al[s] = __fdiv_rn(ev[k], l);
+  }
 }
 
 // ctx columns of this CTA: one thread per column; positions are split round-robin over four
