@@ -50,6 +50,24 @@ __device__ unsigned long long g_echo_phase[16][8192];
 #define ECHO_PHASE(k) do { } while (0)
 #endif
 
+// The ONE tanh of the attention feature map E = tanh(z) (a5, a6 and the deferred passes; readings
+// R9 / R9b).  fp32 storage: IEEE-accurate tanhf.  bf16 storage: z is a bf16 value and the 2e-2
+// storage tolerance applies, so E = sign(z) (1 - 2 / (1 + 2^(2 log2(e) |z|))) with the MUFU ex2 / rcp
+// approximations (absolute error <= 1.8e-7 over all floats, scripts/micro/tanh_err.cu: 20000x
+// below the bf16 rounding of z) in 7 instructions instead of 16.  Every kernel that evaluates E
+// for a given storage type uses this function, so STASH and RECOMPUTE stay bit-identical.
+template <typename T>
+__device__ __forceinline__ float att_tanh(float z) {
+  if constexpr (sizeof(T) == 4) {
+    return tanhf(z);
+  } else {
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(z) * 2.8853900817779268f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+    return copysignf(__fmaf_rn(-2.0f, r, 1.0f), z);
+  }
+}
+
 constexpr int ATT_THREADS = 256;
 constexpr int ATT_WARPS = ATT_THREADS / 32;
 
@@ -67,7 +85,7 @@ __device__ __forceinline__ float score_row(const T* __restrict__ kp_row, const f
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       z[k] = St<T>::round(__fadd_rn(qp_s[iv * V + k], kv[k]));
-      acc = __fmaf_rn(tanhf(z[k]), v_s[iv * V + k], acc);
+      acc = __fmaf_rn(att_tanh<T>(z[k]), v_s[iv * V + k], acc);
     }
     if (Z_out) st16(Z_out + iv * V, z);
   }
@@ -406,7 +424,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(echo_attn_desc d,
       ldf<V>(dkp_row + iv * V, dk);
 #pragma unroll
       for (int k = 0; k < V; ++k) {
-        const float e = tanhf(z[k]);
+        const float e = att_tanh<T>(z[k]);
         const float dE = __fmul_rn(__fmul_rn(ds, v_s[iv * V + k]), __fsub_rn(1.0f, __fmul_rn(e, e)));
         dk[k] = __fadd_rn(dk[k], dE);
         wq_w[iv * V + k] = __fadd_rn(wq_w[iv * V + k], dE);
@@ -556,7 +574,7 @@ __device__ __forceinline__ float score_partial(const T* kz_row, const T* qps, co
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       z[k] = z_of<T>(add_qp ? q[k] : 0.0f, kz[k], add_qp);
-      e[k] = tanhf(z[k]);
+      e[k] = att_tanh<T>(z[k]);
       acc = __fmaf_rn(e[k], vv[k], acc);
     }
     if (z_out) stg4(z_out + c4 * 4, z);
@@ -578,7 +596,7 @@ __device__ __forceinline__ float score_partial_r(const T* kz_row, const float (&
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       z[k] = z_of<T>(add_qp ? qr[k] : 0.0f, kz[k], add_qp);
-      e[k] = tanhf(z[k]);
+      e[k] = att_tanh<T>(z[k]);
       acc = __fmaf_rn(e[k], vr[k], acc);
     }
     if (z_out) stg4(z_out + c4 * 4, z);
@@ -966,7 +984,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             z[q] = z_of<T>(recompute ? qr[q] : 0.0f, kzv[q], recompute);
-            e[q] = tanhf(z[q]);
+            e[q] = att_tanh<T>(z[q]);
             psc[j] = __fmaf_rn(e[q], vr[q], psc[j]);
           }
           *reinterpret_cast<float4*>(E + (size_t)s * Wb + lane * 4) = make_float4(e[0], e[1], e[2], e[3]);
@@ -1149,7 +1167,7 @@ __global__ void __launch_bounds__(256) attn_dkp_finish_kernel(echo_attn_desc d, 
       for (int t = Td - 1; t >= 0; --t) {
         const float z = rec ? St<T>::round(__fadd_rn(qs[t * FIN_COLS + c], kz))
                             : to_f(Z_all[(((long)t * B + b) * Ts + s) * A + a]);
-        const float e = tanhf(z);
+        const float e = att_tanh<T>(z);
         const float dE = __fmul_rn(__fmul_rn(dss[t * Ts + s], vc), __fsub_rn(1.0f, __fmul_rn(e, e)));
         acc = __fadd_rn(acc, dE);
       }
