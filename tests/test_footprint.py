@@ -205,3 +205,20 @@ def test_regenerated_masks_reading_r30(est):
         _compare(est, g, ("mirror", "echo"), {"regenerate_masks": True})
         assert est(g, {"strategy": "echo", "regenerate_masks": True})["stash_bytes"] <= \
             est(g, {"strategy": "echo"})["stash_bytes"], seed
+
+
+def test_nmt_embedding_dropout_graph(est):
+    """R31 graph: C++ == oracle for every plan with and without regenerated masks; Echo keeps the
+    1-bit masks and nothing of the dropped embeddings, regenerated masks keep neither, the Baseline
+    keeps the dropped embeddings and byte masks."""
+    from synth.configs import SMALL_NMT_DROP as cfg
+    doc = Gr.nmt(cfg)
+    _compare(est, doc)
+    _compare(est, doc, ("mirror", "echo"), {"regenerate_masks": True})
+    n = (cfg.Ts + cfg.Td) * cfg.B * cfg.E
+    plain = est(Gr.nmt(SMALL_NMT), {"strategy": "echo"})["stash_bytes"]
+    assert est(doc, {"strategy": "echo"})["stash_bytes"] - plain == n // 8
+    assert est(doc, {"strategy": "echo", "regenerate_masks": True})["stash_bytes"] == plain
+    b0 = est(Gr.nmt(SMALL_NMT), {"strategy": "baseline"})["stash_bytes"]
+    b1 = est(doc, {"strategy": "baseline"})["stash_bytes"]
+    assert b1 - b0 == n                      # + byte masks; the dropped embeddings replace the embeddings
