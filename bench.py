@@ -476,16 +476,20 @@ def run_ours(args):
                 "launches_per_step": {k: len(v) // K for k, v in per.items()}}
 
     out = {}
+    # Rank-0-only extras below must not call collectives (the other ranks are already waiting in the
+    # final barrier): timed() (barriers, max-over-ranks, allreduce in the runner) only runs at N = 1;
+    # the plan comparisons (STASH, Mirror), the secondary legs and the CPU baseline are N = 1 results.
     if rank == 0 and not args.quick:
         other = abi.STASH if mode == abi.RECOMPUTE else abi.RECOMPUTE
-        try:
-            m2 = build(other)
-            ms_other, _ = timed(m2, use_graph, args.steps, args.warmup)
-            del m2
-            torch.cuda.empty_cache()
-        except Exception as ex:
-            ms_other = None
-            print(f"[bench] {('stash', 'recompute')[other]} timing failed: {ex}", file=sys.stderr)
+        ms_other = None
+        if ws == 1:
+            try:
+                m2 = build(other)
+                ms_other, _ = timed(m2, use_graph, args.steps, args.warmup)
+                del m2
+                torch.cuda.empty_cache()
+            except Exception as ex:
+                print(f"[bench] {('stash', 'recompute')[other]} timing failed: {ex}", file=sys.stderr)
         mem = {}
         for md in (abi.STASH, abi.RECOMPUTE):
             try:
@@ -493,13 +497,16 @@ def run_ours(args):
             except torch.OutOfMemoryError:
                 mem[md] = (None, None)
         try:                                                     # prior-work Mirror plan (Table 1 analogue)
+            if ws > 1:
+                raise RuntimeError("N = 1 comparison")
             m3 = build(abi.RECOMPUTE, mirror=True)
             ms_mirror, _ = timed(m3, use_graph, args.steps, args.warmup)
             del m3
             torch.cuda.empty_cache()
             out["mirror"] = {"ms_per_step": ms_mirror, "mem": peak_activation(abi.RECOMPUTE, mirror=True)}
         except Exception as ex:
-            print(f"[bench] mirror plan failed: {ex}", file=sys.stderr)
+            if ws == 1:
+                print(f"[bench] mirror plan failed: {ex}", file=sys.stderr)
         out["ms_other"] = ms_other
         out["mem"] = mem
         out["kern"] = time_attn_bwd(cfg, dtype)
@@ -578,7 +585,7 @@ def run_ours(args):
             line[f"{other_name}_mode"] = {"value": samples / (out["ms_other"] / 1e3), "ms_per_step": out["ms_other"]}
             if mode == abi.RECOMPUTE:
                 line["recompute_overhead"] = ms / out["ms_other"] - 1.0
-    if rank == 0 and not args.quick and args.legs:
+    if rank == 0 and ws == 1 and not args.quick and args.legs:
         extra = {}
         for leg in [x for x in args.legs.split(",") if x]:
             try:
@@ -586,7 +593,7 @@ def run_ours(args):
             except Exception as ex:                               # a secondary leg never breaks the line
                 extra[leg] = {"error": f"{type(ex).__name__}: {ex}"[:200]}
         line["configs_extra"] = extra
-    if rank == 0 and not args.quick and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.quick and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line), flush=True)
     if ws > 1:

@@ -13,11 +13,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_bench_two_ranks(cuda_dev):
+@pytest.mark.parametrize("quick", [True, False], ids=["quick", "full"])
+def test_bench_two_ranks(quick, cuda_dev):
+    """quick: the timed path only; full: also rank 0's extras (memory peaks, a6 probe / roofline),
+    which must not issue collectives while the other ranks wait in the final barrier."""
     env = dict(os.environ, ECHO_DP_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
-           "--warmup", "3", "--quick", "--no-cpu", "--legs", ""]
+           "127.0.0.1", "--master-port", "29541" if quick else "29542", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--no-cpu"] + (["--quick"] if quick else [])
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
@@ -25,3 +28,5 @@ def test_bench_two_ranks(cuda_dev):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 2 * d["config"]["batch_per_gpu"]
     assert d["value"] > 0 and d["scaling"] == "weak"
+    if not quick:
+        assert d["roofline"]["frac"] > 0 and "memory" in d and "configs_extra" not in d
