@@ -26,6 +26,9 @@ Readings (R11-R13, R22-R25):
   * Memory is exact integer bytes; `stack` is a view (its inputs are written into its buffer).
 This module recomputes the stash set from scratch for every decision (no incremental state) and
 counts live bytes by brute force over the schedule: slow and obviously correct.
+Pins of the liveness / peak model (`schedule`, `live_timeline`): hand-counted timelines of Fig. 6
+and Fig. 4 under all three plans and hand-counted peaks (value and step) of a T = 2 LSTM layer under
+the baseline and Echo (tests/test_footprint_liveness.py).
 """
 from __future__ import annotations
 

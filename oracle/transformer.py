@@ -7,7 +7,9 @@ and binarizes the dropout feature maps.  Block k (reading R27):
   O_h = P_d V_h ;  y = concat_h(O_h) Wo^T + x   (residual)
 Loss = mean over the B*L positions of y_final . r.
 Pins: tests/test_oracle_transformer.py (FD; p = 0 with one block and one head reduces to the
-plain attention formula written with torch.softmax).
+plain attention formula written with torch.softmax; heads = 4, p = 0.1, two blocks against a torch
+fp64 model that takes each head as a column slice and applies the same keep-mask -- forward and
+every gradient to 1e-12).
 """
 from __future__ import annotations
 

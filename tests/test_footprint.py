@@ -138,8 +138,11 @@ def test_echo_vs_exhaustive_optimum():
     assert checked >= 10
 
 
-def test_planner_matches_bruteforce_on_c2(est):
-    """C2 (3,999 nodes): the C++ runs the whole pipeline in well under 300 ms."""
+def test_planner_c2_runtime_and_ratio(est):
+    """C2 (3,999 nodes): the C++ runs the whole pipeline in well under 300 ms and Echo's
+    plan reaches the north_star ratio.  (The brute-force oracle takes ~76 s on C2, too slow for the CPU
+    suite; its peak model is pinned by hand counts in tests/test_footprint_liveness.py and compared with
+    the C++ timeline on every smaller graph in this file.)"""
     doc = Gr.nmt(C2)
     t = time.perf_counter()
     e = est(doc, {"strategy": "echo"})
