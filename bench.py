@@ -186,14 +186,14 @@ def time_attn_bwd(cfg, dtype, reps=20):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     st = torch.cuda.current_stream()
     for _ in range(3):
-        abi.echo_attn_bwd(desc, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, dvp, creg)
+        abi.echo_attn_bwd_recompute(desc, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, None, creg, dvp)
     times = []
     for _ in range(reps):
         flush.sum()              # read-flush: L2 ends up holding clean lines
         torch.cuda._sleep(200000)  # GPU busy while the host enqueues e0 / launch / e1: no host gap is timed
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        abi.echo_attn_bwd(desc, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, dvp, creg)
+        abi.echo_attn_bwd_recompute(desc, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, None, creg, dvp)
         e1.record(st)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
@@ -220,7 +220,7 @@ def c5_a6_roofline(m, cfg, dt, reps=2):
     pk = _peaks()
     l_ms = statistics.mean(lt)
     ach = nbytes / (l_ms / 1e3) / 1e9
-    return {"kernel": "echo_attn_bwd (a6, RECOMPUTE)", "launch_us": 1e3 * l_ms, "bytes_per_launch": nbytes,
+    return {"kernel": "echo_attn_bwd_recompute (a6, RECOMPUTE)", "launch_us": 1e3 * l_ms, "bytes_per_launch": nbytes,
             "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
             "timing": "CUDA events on the launch stream around each of the 50 a6 launches per step, inside "
                       "replays of the C5 step graph (event-record nodes)"}
@@ -552,7 +552,7 @@ def run_ours(args):
         else:
             l_ms, timing, share = k["ms"], "CUDA events, L2 flushed (256 MiB read) before each launch", cfg.Td * k["ms"] / ms
         achieved = k["bytes"] / (l_ms / 1e3) / 1e9
-        line["roofline"] = {"bound": "hbm", "kernel": "echo_attn_bwd (a6, RECOMPUTE)", "achieved": achieved,
+        line["roofline"] = {"bound": "hbm", "kernel": "echo_attn_bwd_recompute (a6, RECOMPUTE)", "achieved": achieved,
                             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                             "traffic": (out["traffic"] or {}).get("bytes"),
                             "traffic_source": (out["traffic"] or {}).get("source"), "peak_source": pk["source"],

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ECHO_ABI_VERSION 1
+#define ECHO_ABI_VERSION 2
 
 typedef enum {
   ECHO_OK = 0,
@@ -64,7 +64,7 @@ int echo_abi_version(void);
  *   c_t = f * c_{t-1} + i * g ;  h_t = o * tanh(c_t)
  * Feature maps (Echo plan, DESIGN.md table T3): both modes stash the gates
  * [B,4H]; STASH additionally keeps c_t (fp32), tanh(c_t) and h_t; RECOMPUTE
- * regenerates c (echo_lstm_cscan) and tanh(c), h (echo_lstm_bwd) in the
+ * regenerates c (a2) and tanh(c), h (a3, echo_lstm_bwd_recompute) in the
  * backward pass.  Time order is the caller's processing order (a reverse-
  * direction layer simply processes t = T-1..0).
  */
@@ -136,7 +136,7 @@ echo_status echo_lstm_seq_fwd(const echo_lstm_desc* d, int32_t T, int32_t k0, in
  * echo_lstm_cscan_parts: c_1..c_T of the layer into c_ws [T,B,H] fp32 (processing order) from
  *   c0; step k's parts at parts + k * step_stride (|step_stride| >= 4*B*H; negative walks a
  *   time-ordered buffer backwards for a reverse-direction layer).
- * echo_lstm_bwd_parts: as echo_lstm_bwd in RECOMPUTE mode with the gates regenerated from the
+ * echo_lstm_bwd_parts: as echo_lstm_bwd_recompute in RECOMPUTE mode with the gates regenerated from the
  *   parts and no h output (h_t is kept); dA_t [B,4H] s OUT may alias part 0 of the step.
  * Device pointers, 16-byte aligned; desc->mode is not used.  Errors: ECHO_ERR_INVALID.           */
 echo_status echo_lstm_fwd_parts(const echo_lstm_desc* d, int32_t n_parts, const void* parts_t,
@@ -152,19 +152,37 @@ echo_status echo_lstm_bwd_parts(const echo_lstm_desc* d, int32_t n_parts, const 
 /* 1 if echo_lstm_seq_fwd has a co-resident tile for this (B, H, dtype) on the current device. */
 int32_t echo_lstm_seq_supported(int32_t B, int32_t H, int32_t dtype);
 
-/* a3 — backward step with fused recomputation (Echo-dagger fusion).
- *  gates_t [B,4H] s    stashed i|f|g|o
- *  c_prev  [B,H] fp32  c_{t-1} (c_0, the STASH c buffer, or the a2 workspace)
- *  c_t     [B,H] fp32  RECOMPUTE: c_t from a2; STASH: NULL
- *  tc_t    [B,H] s     STASH: stashed tanh(c_t); RECOMPUTE: NULL
- *  dh_t    [B,H] fp32  total dLoss/dh_t (from above + recurrent)
- *  dc      [B,H] fp32  IN dLoss/dc_t carried from t+1; OUT dLoss/dc_{t-1}
- *  dA_t    [B,4H] s    OUT dLoss/dA_t (pre-activations); may alias gates_t
- *  h_regen [B,H] s     RECOMPUTE: OUT regenerated h_t (for the caller's dW GEMMs) or NULL;
- *                      STASH: must be NULL                                           */
-echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_t, const float* c_prev,
-                          const float* c_t, const void* tc_t, const float* dh_t, float* dc,
-                          void* dA_t, void* h_regen, void* stream);
+/* a3 (+ a2) — backward step with fused recomputation (Echo-dagger fusion; the
+ * recomputation path of the mirrored c-chain, Fig. 4 step 4, and Fig. 8(c)).
+ * One call per backward step t = T-1 .. 0 (processing order) of one layer (direction):
+ *   RECOMPUTE: regenerate i,f,g,o from the stashed gates, tanh(c_t) and h_t from c_t, then
+ *              do = dh tc ; dc = carry + dh o (1 - tc^2) ; di = dc g ; dg = dc i ; df = dc c_{t-1}
+ *              carry' = dc f ; dA = [di i(1-i) | df f(1-f) | dg (1-g^2) | do o(1-o)]
+ *   STASH:     the same gradient from the stashed gates, c and tanh(c) (the paper's Baseline).
+ *  T, t      steps of the layer and this step, 0 <= t < T
+ *  flags     ECHO_BWD_REGEN_C (RECOMPUTE only): first run the a2 scan, c_1..c_T into ws from the
+ *            gates and c0 (pass it on the first backward call, t = T-1; or fill ws with
+ *            echo_lstm_cscan, which can also regenerate the layer outputs h)
+ *  gates     [T,B,4H] s  stashed i|f|g|o of every step (both modes)
+ *  c0        [B,H] fp32  initial cell state
+ *  c_st      STASH: [T,B,H] fp32 c_1..c_T (c_{t-1} is read for t > 0); RECOMPUTE: NULL
+ *  tc_st     STASH: [T,B,H] s tanh(c_t);                                RECOMPUTE: NULL
+ *  dh_t      [B,H] fp32  total dLoss/dh_t (from above + recurrent)
+ *  dc        [B,H] fp32  IN dLoss/dc_t carried from t+1; OUT dLoss/dc_{t-1}
+ *  dA_t      [B,4H] s    OUT dLoss/dA_t (pre-activations); may alias step t of gates
+ *  h_regen_t [B,H] s     RECOMPUTE: OUT regenerated h_t, bit-identical to a1's (for the caller's
+ *                        dW GEMMs) or NULL; STASH: NULL
+ *  ws        RECOMPUTE: caller-owned workspace holding c_1..c_T fp32 across the layer's backward
+ *            calls; STASH: NULL.   ws_bytes: two-call convention -- with ws == NULL and ws_bytes
+ *            != NULL the call only writes the needed size (T*B*H*4 in RECOMPUTE, 0 in STASH) and
+ *            returns ECHO_OK; with ws != NULL a non-NULL *ws_bytes is its capacity (checked).
+ * Errors: ECHO_ERR_INVALID (t out of range, missing / misaligned buffer for the mode, unknown
+ * flags), ECHO_ERR_CAPACITY (ws too small), ECHO_ERR_CUDA.                                     */
+#define ECHO_BWD_REGEN_C 1u
+echo_status echo_lstm_bwd_recompute(const echo_lstm_desc* d, int32_t T, int32_t t, uint32_t flags,
+                                    const void* gates, const float* c0, const float* c_st, const void* tc_st,
+                                    const float* dh_t, float* dc, void* dA_t, void* h_regen_t, void* ws,
+                                    size_t* ws_bytes, void* stream);
 
 /* ===================================================================== MLP attention
  * PAPER.md §2 lines 129-133 and Fig. 7 (the scoring function as
@@ -174,7 +192,7 @@ echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_t, const fl
  * One query per row (the NMT decoder calls this once per target step).
  * Feature maps (Echo plan, DESIGN.md table T4): STASH keeps the tanh feature
  * map [B,Ts,A] s and alpha [B,Ts] fp32 (and the caller keeps ctx); RECOMPUTE
- * keeps nothing and echo_attn_bwd regenerates it, the scores, alpha and ctx.
+ * keeps nothing and echo_attn_bwd_recompute regenerates it, the scores, alpha and ctx.
  * The tanh feature map is stored as its input Z = round_s(qp + Kp) (same bytes
  * as E = tanh(Z); E and tanh' = 1 - E^2 are evaluated in fp32 from Z in both
  * modes, which keeps bf16 gradients accurate near saturation; R15).
@@ -197,29 +215,43 @@ echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, const void* K
                           const void* Hs, const int32_t* src_len, void* ctx, void* E_st,
                           float* alpha_st, void* stream);
 
-/* a6 — backward with fused recomputation.
+/* a6 — backward with fused recomputation (Fig. 10: the add / tanh feature maps
+ * stay on the mirror path).  Per decoder step (reverse order), per row b:
+ *   regenerate E_s = tanh(round_s(qp_b + Kp_{b,s})), score, alpha and ctx_b (RECOMPUTE), or read
+ *   the stashed Z, alpha (STASH);  dalpha_s = dctx_b . Hs_{b,s};  ds = alpha (dalpha - sum alpha dalpha)
+ *   dE_s = ds_s v (1 - E_s^2);  dqp_b = sum_s dE_s;  dKp_{b,s} += dE_s;  dHs_{b,s} += alpha_s dctx_b;
+ *   dv += sum_{b,s} ds_s E_s (per-row partials in ws, reduced in ascending b: no atomics)
  *  qp, Kp           RECOMPUTE: required (E is regenerated from them); STASH: may be NULL
  *  E_st, alpha_st   STASH inputs from a5 (NULL in RECOMPUTE)
  *  dctx   [B,Hk] fp32    dLoss/dctx
  *  dqp    [B,A] fp32     OUT dLoss/dqp (overwritten)
  *  dKp    [B,Ts,A] fp32  ACCUMULATED (+=) dLoss/dKp, same strides as Kp
  *  dHs    [B,Ts,Hk] fp32 ACCUMULATED (+=) dLoss/dHs, same strides as Hs
- *  dv_part [B,A] fp32    ACCUMULATED (+=) per-row partials of dLoss/dv; reduce
- *                        with echo_attn_dv_reduce (fixed order, no atomics)
- *  ctx_regen [B,Hk] s    OUT regenerated ctx (RECOMPUTE; bit-identical to a5's) or NULL */
-echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
-                          const void* Hs, const int32_t* src_len, const void* E_st,
-                          const float* alpha_st, const float* dctx, float* dqp, float* dKp,
-                          float* dHs, float* dv_part, void* ctx_regen, void* stream);
+ *  dv     [A] fp32       OUT or NULL: when non-NULL, dv = sum_b ws[b,:] (ascending b) after this
+ *                        step's partials were added -- pass it on the last call of a backward pass
+ *  ctx_regen [B,Hk] s    OUT regenerated ctx (RECOMPUTE; bit-identical to a5's) or NULL
+ *  ws     [B,A] fp32     caller-owned per-row dv partials, ACCUMULATED (+=) across the calls of one
+ *                        backward pass; zero it before the first call.  ws_bytes: two-call
+ *                        convention -- ws == NULL with ws_bytes != NULL writes B*A*4 and returns
+ *                        ECHO_OK without launching; otherwise a non-NULL *ws_bytes is checked.
+ * Errors: ECHO_ERR_INVALID (shape, stride, missing buffer for the mode, misalignment),
+ * ECHO_ERR_CAPACITY (ws too small), ECHO_ERR_CUDA.                                             */
+echo_status echo_attn_bwd_recompute(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
+                                    const void* Hs, const int32_t* src_len, const void* E_st,
+                                    const float* alpha_st, const float* dctx, float* dqp, float* dKp,
+                                    float* dHs, float* dv, void* ctx_regen, void* ws, size_t* ws_bytes,
+                                    void* stream);
 
 /* a6, deferred accumulation (the algorithmic-minimum variant).  The same step as
- * echo_attn_bwd without the per-step dKp / dH_s read-modify-write: it writes this step's
+ * echo_attn_bwd_recompute without the per-step dKp / dH_s read-modify-write: it writes this step's
  * softmax-backward rows instead and echo_attn_bwd_finish accumulates dKp / dH_s over all steps
  * once, with the per-step expressions in the per-step order (t = Td-1 .. 0): results are
- * bit-identical to calling echo_attn_bwd every step.
+ * bit-identical to calling echo_attn_bwd_recompute every step.
  *  ds_out     [B,Ts] fp32 OUT  ds_s = alpha_s (dalpha_s - sum alpha dalpha) (0 for s >= len_b)
  *  alpha_out  [B,Ts] fp32 OUT  regenerated alpha (RECOMPUTE; NULL in STASH, where alpha is stashed)
- * Other arguments as echo_attn_bwd.  Errors as echo_attn_bwd; ECHO_ERR_UNSUPPORTED where only the
+ * dv_part [B,A] fp32 ACCUMULATED per-row dv partials (the ws of echo_attn_bwd_recompute; reduce them
+ * with one final echo_attn_bwd_recompute call or by summing rows in ascending b).
+ * Other arguments as echo_attn_bwd_recompute.  Errors as echo_attn_bwd_recompute; ECHO_ERR_UNSUPPORTED where only the
  * generic (non-TMA) kernel fits (Ts > 256).                                                      */
 echo_status echo_attn_bwd_deferred(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
                                    const void* Hs, const int32_t* src_len, const void* E_st,
@@ -230,7 +262,7 @@ echo_status echo_attn_bwd_deferred(const echo_attn_desc* d, const void* qp, cons
  *   dKp[b,s,:] = sum_{t=Td-1..0} (ds_t[b,s] v) (1 - tanh(z_t[b,s,:])^2),
  *   z_t = round_s(qp_t[b,:] + Kp[b,s,:]) (RECOMPUTE) or the stashed z_t (STASH)
  *   dHs[b,s,:] = sum_{t=Td-1..0} alpha_t[b,s] dctx_t[b,:]          (both OVERWRITTEN)
- *  qp_all [Td,B,A] s (RECOMPUTE) | E_st_all [Td,B,Ts,A] s (STASH); Kp as in echo_attn_bwd
+ *  qp_all [Td,B,A] s (RECOMPUTE) | E_st_all [Td,B,Ts,A] s (STASH); Kp as in echo_attn_bwd_recompute
  *  ds_all, alpha_all [Td,B,Ts] fp32 (the per-step ds_out / alpha_out, or the stashed alpha)
  *  dctx_all [Td,B,Hk] fp32 (the per-step dctx)
  * Errors: ECHO_ERR_INVALID, ECHO_ERR_CAPACITY (Td*Ts too large for the staged rows).               */
@@ -241,7 +273,7 @@ echo_status echo_attn_bwd_finish(const echo_attn_desc* d, int32_t Td, const void
 
 /* One decoder step of the deferred accumulation, added to the running sums: dKp[b,s,:] += dE_t and
  * dH_s[b,s,:] += alpha_t[b,s] dctx_t[b,:] for s < len_b (rows s >= len_b untouched), with exactly
- * the per-step expressions of echo_attn_bwd (same bits when called for t = Td-1 .. 0 in order).
+ * the per-step expressions of echo_attn_bwd_recompute (same bits when called for t = Td-1 .. 0 in order).
  * Lets the caller run the read-modify-write of step t OFF the critical path (e.g. on a second
  * stream after echo_attn_bwd_deferred of step t) while the recurrence continues.
  *  qp_t [B,A], E_st_t [B,Ts,A] (STASH), ds_t / alpha_t [B,Ts] fp32, dctx_t [B,Hk] fp32: step t's rows. */
@@ -250,7 +282,8 @@ echo_status echo_attn_bwd_accumulate(const echo_attn_desc* d, const void* qp_t, 
                                      const float* alpha_t, const float* dctx_t, float* dKp, float* dHs,
                                      void* stream);
 
-/* dv[a] (+)= sum_b dv_part[b,a] in ascending b (deterministic).  accumulate != 0 adds to dv. */
+/* dv[a] (+)= sum_b dv_part[b,a] in ascending b (deterministic; the reduction echo_attn_bwd_recompute
+ * runs when given dv), for the deferred variants above.  accumulate != 0 adds to dv.            */
 echo_status echo_attn_dv_reduce(int32_t B, int32_t A, const float* dv_part, float* dv,
                                 int32_t accumulate, void* stream);
 

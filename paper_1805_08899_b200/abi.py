@@ -18,14 +18,19 @@ ECHO_OK, ECHO_ERR_INVALID, ECHO_ERR_GRAPH, ECHO_ERR_CAPACITY, ECHO_ERR_MISMATCH,
 FP32, BF16 = 0, 1
 STASH, RECOMPUTE = 0, 1
 
-EXPORTED = ("echo_last_error", "echo_abi_version", "echo_lstm_fwd", "echo_lstm_cscan", "echo_lstm_bwd",
-            "echo_attn_fwd", "echo_attn_bwd", "echo_attn_dv_reduce", "echo_dot_softmax_fwd",
+# the five entry points BASELINE.json north_star names
+NORTH_STAR = ("echo_lstm_fwd", "echo_lstm_bwd_recompute", "echo_attn_fwd", "echo_attn_bwd_recompute",
+              "echo_footprint_estimate")
+ECHO_BWD_REGEN_C = 1
+
+EXPORTED = NORTH_STAR + (
+            "echo_last_error", "echo_abi_version", "echo_lstm_cscan", "echo_attn_dv_reduce",
+            "echo_dot_softmax_fwd",
             "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum", "echo_lstm_seq_fwd",
             "echo_lstm_seq_supported", "echo_gemm_f32", "echo_gemm_f32_supported",
             "echo_attn_bwd_deferred", "echo_attn_bwd_finish", "echo_attn_bwd_accumulate", "echo_tanh_bwd",
             "echo_lstm_fwd_parts", "echo_lstm_cscan_parts", "echo_lstm_bwd_parts",
-            "echo_dropout_fwd", "echo_dropout_apply",
-            "echo_footprint_estimate")
+            "echo_dropout_fwd", "echo_dropout_apply")
 
 
 class EchoError(RuntimeError):
@@ -72,9 +77,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     sigs = {
         "echo_lstm_fwd": [ctypes.POINTER(LstmDesc)] + [vp] * 9,
         "echo_lstm_cscan": [ctypes.POINTER(LstmDesc), i32, vp, vp, vp, vp, vp],
-        "echo_lstm_bwd": [ctypes.POINTER(LstmDesc)] + [vp] * 9,
+        "echo_lstm_bwd_recompute": [ctypes.POINTER(LstmDesc), i32, i32, ctypes.c_uint32] + [vp] * 11,
         "echo_attn_fwd": [ctypes.POINTER(AttnDesc)] + [vp] * 9,
-        "echo_attn_bwd": [ctypes.POINTER(AttnDesc)] + [vp] * 14,
+        "echo_attn_bwd_recompute": [ctypes.POINTER(AttnDesc)] + [vp] * 16,
         "echo_attn_dv_reduce": [i32, i32, vp, vp, i32, vp],
         "echo_attn_bwd_deferred": [ctypes.POINTER(AttnDesc)] + [vp] * 14,
         "echo_attn_bwd_finish": [ctypes.POINTER(AttnDesc), i32] + [vp] * 11,
@@ -142,10 +147,22 @@ def echo_lstm_cscan(d, T, gates, c0, c_ws, h_ws=None, stream=None):
     _check(load().echo_lstm_cscan(ctypes.byref(d), int(T), _p(gates), _p(c0), _p(c_ws), _p(h_ws), _stream(stream)))
 
 
-def echo_lstm_bwd(d, gates_t, c_prev, c_t, tc_t, dh_t, dc, dA_t, h_regen, stream=None):
-    LAUNCHES["count"] += 1
-    _check(load().echo_lstm_bwd(ctypes.byref(d), _p(gates_t), _p(c_prev), _p(c_t), _p(tc_t), _p(dh_t), _p(dc),
-                                _p(dA_t), _p(h_regen), _stream(stream)))
+def echo_lstm_bwd_recompute(d, T, t, flags, gates, c0, c_st, tc_st, dh_t, dc, dA_t, h_regen_t, ws, ws_bytes=None,
+                            stream=None):
+    """ws_bytes: None, or an int capacity of ws (checked by the library)."""
+    LAUNCHES["count"] += 1 + (1 if flags & ECHO_BWD_REGEN_C else 0)
+    n = None if ws_bytes is None else ctypes.byref(ctypes.c_size_t(int(ws_bytes)))
+    _check(load().echo_lstm_bwd_recompute(ctypes.byref(d), int(T), int(t), int(flags), _p(gates), _p(c0), _p(c_st),
+                                          _p(tc_st), _p(dh_t), _p(dc), _p(dA_t), _p(h_regen_t), _p(ws), n,
+                                          _stream(stream)))
+
+
+def echo_lstm_bwd_ws_bytes(d, T) -> int:
+    """Two-call convention: the workspace echo_lstm_bwd_recompute needs (bytes; nothing launched)."""
+    n = ctypes.c_size_t(0)
+    _check(load().echo_lstm_bwd_recompute(ctypes.byref(d), int(T), 0, 0, None, None, None, None, None, None, None,
+                                          None, None, ctypes.byref(n), None))
+    return n.value
 
 
 # ---------------------------------------------------------------- MLP attention
@@ -155,10 +172,22 @@ def echo_attn_fwd(d, qp, Kp, v, Hs, src_len, ctx, E_st, alpha_st, stream=None):
                                 _p(alpha_st), _stream(stream)))
 
 
-def echo_attn_bwd(d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part, ctx_regen, stream=None):
-    LAUNCHES["count"] += 1
-    _check(load().echo_attn_bwd(ctypes.byref(d), _p(qp), _p(Kp), _p(v), _p(Hs), _p(src_len), _p(E_st), _p(alpha_st),
-                                _p(dctx), _p(dqp), _p(dKp), _p(dHs), _p(dv_part), _p(ctx_regen), _stream(stream)))
+def echo_attn_bwd_recompute(d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, dKp, dHs, dv, ctx_regen, ws,
+                            ws_bytes=None, stream=None):
+    """ws: [B,A] fp32 dv partials accumulated across one backward pass (zeroed by the caller first);
+    dv: None, or [A] fp32 written from ws after this step."""
+    LAUNCHES["count"] += 1 + (1 if dv is not None else 0)
+    n = None if ws_bytes is None else ctypes.byref(ctypes.c_size_t(int(ws_bytes)))
+    _check(load().echo_attn_bwd_recompute(ctypes.byref(d), _p(qp), _p(Kp), _p(v), _p(Hs), _p(src_len), _p(E_st),
+                                          _p(alpha_st), _p(dctx), _p(dqp), _p(dKp), _p(dHs), _p(dv), _p(ctx_regen),
+                                          _p(ws), n, _stream(stream)))
+
+
+def echo_attn_bwd_ws_bytes(d) -> int:
+    """Two-call convention: the dv-partials workspace echo_attn_bwd_recompute needs (nothing launched)."""
+    n = ctypes.c_size_t(0)
+    _check(load().echo_attn_bwd_recompute(ctypes.byref(d), *([None] * 14), ctypes.byref(n), None))
+    return n.value
 
 
 def echo_attn_dv_reduce(B, A, dv_part, dv, accumulate, stream=None):

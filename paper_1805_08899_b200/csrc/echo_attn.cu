@@ -1489,12 +1489,29 @@ static echo_status attn_bwd_impl(const char* fn, const echo_attn_desc* d, const 
   return check_launch(fn);
 }
 
-extern "C" echo_status echo_attn_bwd(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
-                                     const void* Hs, const int32_t* src_len, const void* E_st,
-                                     const float* alpha_st, const float* dctx, float* dqp, float* dKp, float* dHs,
-                                     float* dv_part, void* ctx_regen, void* stream) {
-  return attn_bwd_impl("echo_attn_bwd", d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, dKp, dHs, dv_part,
-                       ctx_regen, nullptr, nullptr, stream);
+extern "C" echo_status echo_attn_bwd_recompute(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
+                                               const void* Hs, const int32_t* src_len, const void* E_st,
+                                               const float* alpha_st, const float* dctx, float* dqp, float* dKp,
+                                               float* dHs, float* dv, void* ctx_regen, void* ws, size_t* ws_bytes,
+                                               void* stream) {
+  const char* fn = "echo_attn_bwd_recompute";
+  echo_status s = check_attn(fn, d);
+  if (s) return s;
+  const size_t need = sizeof(float) * (size_t)d->B * d->A;   // per-row dv partials [B,A] fp32
+  if (!ws) {                                                // two-call workspace convention
+    if (!ws_bytes) return fail(ECHO_ERR_INVALID, "%s: ws and ws_bytes are both NULL", fn);
+    *ws_bytes = need;
+    return ECHO_OK;
+  }
+  if (ws_bytes && *ws_bytes < need) return fail(ECHO_ERR_CAPACITY, "%s: ws has %zu bytes, needs %zu", fn, *ws_bytes, need);
+  if (dv && !aligned16(dv)) return fail(ECHO_ERR_INVALID, "%s: dv is not 16-byte aligned", fn);
+  s = attn_bwd_impl(fn, d, qp, Kp, v, Hs, src_len, E_st, alpha_st, dctx, dqp, dKp, dHs, (float*)ws, ctx_regen, nullptr,
+                    nullptr, stream);
+  if (s || !dv) return s;
+  const cudaError_t e = launch(dv_reduce_kernel, dim3((d->A + 127) / 128), dim3(128), 0, (cudaStream_t)stream, 1, d->B,
+                               d->A, (const float*)ws, dv, 0);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
 }
 
 extern "C" echo_status echo_attn_bwd_deferred(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
@@ -1574,6 +1591,7 @@ extern "C" int echo_debug_phase_times(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, echo::g_echo_phase, sizeof(unsigned long long) * (size_t)n);
 }
 #endif
+
 
 extern "C" echo_status echo_attn_dv_reduce(int32_t B, int32_t A, const float* dv_part, float* dv, int32_t accumulate,
                                            void* stream) {

@@ -746,25 +746,21 @@ extern "C" echo_status echo_lstm_cscan(const echo_lstm_desc* d, int32_t T, const
   return check_launch(fn);
 }
 
-extern "C" echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_t, const float* c_prev,
-                                     const float* c_t, const void* tc_t, const float* dh_t, float* dc, void* dA_t,
-                                     void* h_regen, void* stream) {
-  const char* fn = "echo_lstm_bwd";
-  echo_status s = check_desc(d);
-  if (s) return s;
-  ECHO_REQ(gates_t, "gates_t");
+// a3 per step (internal): c_prev / c_t / tc_t already resolved by echo_lstm_bwd_recompute.
+static echo_status lstm_bwd_step(const char* fn, const echo_lstm_desc* d, const void* gates_t, const float* c_prev,
+                                 const float* c_t, const void* tc_t, const float* dh_t, float* dc, void* dA_t,
+                                 void* h_regen, void* stream) {
+  ECHO_REQ(gates_t, "gates");
   ECHO_REQ(c_prev, "c_prev");
   ECHO_REQ(dh_t, "dh_t");
   ECHO_REQ(dc, "dc");
   ECHO_REQ(dA_t, "dA_t");
   if (d->mode == ECHO_STASH) {
-    ECHO_REQ(tc_t, "tc_t");
-    if (c_t) return fail(ECHO_ERR_INVALID, "%s: c_t must be NULL in STASH mode", fn);
-    if (h_regen) return fail(ECHO_ERR_INVALID, "%s: h_regen must be NULL in STASH mode", fn);
+    ECHO_REQ(tc_t, "tc_st");
+    if (h_regen) return fail(ECHO_ERR_INVALID, "%s: h_regen_t must be NULL in STASH mode", fn);
   } else {
-    ECHO_REQ(c_t, "c_t");
-    ECHO_OPT(h_regen, "h_regen");
-    if (tc_t) return fail(ECHO_ERR_INVALID, "%s: tc_t must be NULL in RECOMPUTE mode", fn);
+    ECHO_REQ(c_t, "ws");
+    ECHO_OPT(h_regen, "h_regen_t");
   }
   cudaStream_t st = (cudaStream_t)stream;
   const bool bf = d->dtype != ECHO_FP32;
@@ -783,6 +779,46 @@ extern "C" echo_status echo_lstm_bwd(const echo_lstm_desc* d, const void* gates_
 #undef ECHO_BWD_LAUNCH
   if (e_ != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e_));
   return check_launch(fn);
+}
+
+extern "C" echo_status echo_lstm_bwd_recompute(const echo_lstm_desc* d, int32_t T, int32_t t, uint32_t flags,
+                                               const void* gates, const float* c0, const float* c_st,
+                                               const void* tc_st, const float* dh_t, float* dc, void* dA_t,
+                                               void* h_regen_t, void* ws, size_t* ws_bytes, void* stream) {
+  const char* fn = "echo_lstm_bwd_recompute";
+  echo_status s = check_desc(d);
+  if (s) return s;
+  if (T <= 0 || t < 0 || t >= T) return fail(ECHO_ERR_INVALID, "%s: t=%d out of range for T=%d", fn, t, T);
+  if (flags & ~(uint32_t)ECHO_BWD_REGEN_C) return fail(ECHO_ERR_INVALID, "%s: unknown flags 0x%x", fn, flags);
+  const bool rec = d->mode == ECHO_RECOMPUTE;
+  const size_t BH = (size_t)d->B * d->H;
+  const size_t need = rec ? sizeof(float) * (size_t)T * BH : 0;
+  if (!ws && ws_bytes) {                                  // two-call workspace convention: size query
+    *ws_bytes = need;
+    return ECHO_OK;
+  }
+  if (ws_bytes && *ws_bytes < need)
+    return fail(ECHO_ERR_CAPACITY, "%s: ws has %zu bytes, needs %zu", fn, *ws_bytes, need);
+  ECHO_REQ(gates, "gates");
+  ECHO_REQ(c0, "c0");
+  const size_t es = d->dtype == ECHO_FP32 ? 4 : 2;
+  const char* g_t = (const char*)gates + (size_t)t * 4 * BH * es;
+  if (rec) {
+    if (c_st || tc_st) return fail(ECHO_ERR_INVALID, "%s: c_st / tc_st must be NULL in RECOMPUTE mode", fn);
+    ECHO_REQ(ws, "ws");
+    float* cw = (float*)ws;
+    if (flags & ECHO_BWD_REGEN_C) {                       // a2 prologue: c_1..c_T into ws
+      s = echo_lstm_cscan(d, T, gates, c0, cw, nullptr, stream);
+      if (s) return s;
+    }
+    return lstm_bwd_step(fn, d, g_t, t == 0 ? c0 : cw + (size_t)(t - 1) * BH, cw + (size_t)t * BH, nullptr, dh_t, dc,
+                         dA_t, h_regen_t, stream);
+  }
+  if (flags) return fail(ECHO_ERR_INVALID, "%s: ECHO_BWD_REGEN_C needs RECOMPUTE mode", fn);
+  ECHO_REQ(tc_st, "tc_st");
+  if (t > 0) ECHO_REQ(c_st, "c_st");
+  return lstm_bwd_step(fn, d, g_t, t == 0 ? c0 : c_st + (size_t)(t - 1) * BH, nullptr,
+                       (const char*)tc_st + (size_t)t * BH * es, dh_t, dc, dA_t, nullptr, stream);
 }
 
 extern "C" echo_status echo_lstm_seq_fwd(const echo_lstm_desc* d, int32_t T, int32_t k0, int32_t k1, int32_t reverse,

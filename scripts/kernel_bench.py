@@ -86,11 +86,11 @@ for md, mname in ((abi.RECOMPUTE, "recompute"), (abi.STASH, "stash")):
     if want("lstm_bwd"):
         if md == abi.STASH:
             tcs = rn(B, H).to(sd)
-            ms = timeit(lambda: abi.echo_lstm_bwd(d, gts, cp, None, tcs, dh, dc, dA, None))
+            ms = timeit(lambda: abi.echo_lstm_bwd_recompute(d, 1, 0, 0, gts, cp, None, tcs, dh, dc, dA, None, None))
             nb = BH * (4 * s + 4 + s + 4 + 2 * 4 + 4 * s)
         else:
             hr = torch.empty(B, H, device="cuda", dtype=sd)
-            ms = timeit(lambda: abi.echo_lstm_bwd(d, gts, cp, co, None, dh, dc, dA, hr))
+            ms = timeit(lambda: abi.echo_lstm_bwd_recompute(d, 1, 0, 0, gts, cp, None, None, dh, dc, dA, hr, co))
             nb = BH * (4 * s + 4 + 4 + 4 + 2 * 4 + 4 * s + s)
         report(f"lstm_bwd a3 ({mname})", ms, nb)
 if want("cscan"):
@@ -123,10 +123,10 @@ for md, mname in ((abi.RECOMPUTE, "recompute"), (abi.STASH, "stash")):
     creg = torch.empty(B, Hk, device="cuda", dtype=sd) if md == abi.RECOMPUTE else None
     if want("attn_bwd"):
         if md == abi.RECOMPUTE:
-            ms = timeit(lambda: abi.echo_attn_bwd(d, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, dvp, creg))
+            ms = timeit(lambda: abi.echo_attn_bwd_recompute(d, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, None, creg, dvp))
             nb = rows * (A * s + Hk * s + 2 * A * 4 + 2 * Hk * 4)
         else:
-            ms = timeit(lambda: abi.echo_attn_bwd(d, None, None, v, Hs, sl, Z, al, dctx, dqp, dKp, dHs, dvp, None))
+            ms = timeit(lambda: abi.echo_attn_bwd_recompute(d, None, None, v, Hs, sl, Z, al, dctx, dqp, dKp, dHs, None, None, dvp))
             nb = rows * (A * s + 4 + Hk * s + 2 * A * 4 + 2 * Hk * 4)
         nb += B * A * s + B * Hk * 4 + B * A * 4 + 2 * B * A * 4 + B * Hk * s
         report(f"attn_bwd a6 ({mname})", ms, nb)

@@ -17,10 +17,10 @@ dHs = torch.zeros(Ts, B, H, device="cuda"); dvp = torch.zeros(B, A, device="cuda
 d = abi.AttnDesc(B, Ts, A, H, abi.FP32, abi.RECOMPUTE, A, B * A, H, B * H)
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
 for _ in range(3):
-    abi.echo_attn_bwd(d, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, dvp, creg)
+    abi.echo_attn_bwd_recompute(d, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, None, creg, dvp)
 flush.sum(); torch.cuda._sleep(200000)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record(); abi.echo_attn_bwd(d, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, dvp, creg); e1.record(); e1.synchronize()
+e0.record(); abi.echo_attn_bwd_recompute(d, qp, Kp, v, Hs, sl, None, None, dctx, dqp, dKp, dHs, None, creg, dvp); e1.record(); e1.synchronize()
 print("kernel ms", e0.elapsed_time(e1))
 buf = np.zeros((16, 8192), dtype=np.uint64)
 fn(buf.ctypes.data, 16 * 8192)

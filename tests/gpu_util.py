@@ -43,3 +43,22 @@ def relerr_fro(x, y):
     y = np.asarray(y, np.float64)
     den = np.linalg.norm(y)
     return float(np.linalg.norm(x - y) / (den if den > 0 else 1.0))
+
+
+def check_grads(g, ref, storage, fro_only=(), what=""):
+    """Per-tensor gate at north_star's tolerance: max relative error (inf-norm, reading R14) <= TOL for
+    every tensor, except the tensors named in `fro_only` (bf16 storage only; each one is listed with its
+    measured numbers and bf16 noise floor in DESIGN.md R14b), which are gated on the Frobenius relative
+    error instead.  Both metrics are printed for every tensor (pytest -s / -rA shows them)."""
+    tol = TOL[storage]
+    bad = []
+    for k, v in ref.items():
+        e_inf, e_fro = relerr(g[k], v), relerr_fro(g[k], v)
+        print(f"[parity] {what} {storage} {k}: inf {e_inf:.3e} fro {e_fro:.3e}")
+        if k in fro_only:
+            assert storage == "bf16", k
+            if e_fro > tol:
+                bad.append((k, "fro", e_fro, e_inf))
+        elif e_inf > tol:
+            bad.append((k, "inf", e_inf, e_fro))
+    assert not bad, bad

@@ -21,10 +21,36 @@ def _declared():
     return sorted(set(re.findall(r"\b(echo_[a-z_0-9]+)\s*\(", src)))
 
 
-def test_header_declares_the_five_entry_points():
+NORTH_STAR = ("echo_lstm_fwd", "echo_lstm_bwd_recompute", "echo_attn_fwd", "echo_attn_bwd_recompute",
+              "echo_footprint_estimate")          # BASELINE.json north_star (1), SURVEY.md §8(b)
+
+
+def test_header_declares_the_five_entry_points(lib):
+    from paper_1805_08899_b200 import abi
     names = _declared()
-    for n in ("echo_lstm_fwd", "echo_lstm_bwd", "echo_attn_fwd", "echo_attn_bwd", "echo_footprint_estimate"):
+    assert abi.NORTH_STAR == NORTH_STAR
+    for n in NORTH_STAR:
         assert n in names
+    out = subprocess.run(["nm", "-D", "--defined-only", abi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (echo_[a-z_0-9]+)$", out, flags=re.M))
+    assert set(NORTH_STAR) <= exported
+    for old in ("echo_lstm_bwd", "echo_attn_bwd"):       # the round-1 names are gone
+        assert old not in exported
+
+
+def test_workspace_queries_without_gpu(lib):
+    """Two-call workspace convention: ws == NULL returns the size and launches nothing,
+    so it runs on a host without a GPU."""
+    from paper_1805_08899_b200 import abi
+    T, B, H = 50, 128, 512
+    assert abi.echo_lstm_bwd_ws_bytes(abi.LstmDesc(B, H, abi.FP32, abi.RECOMPUTE), T) == T * B * H * 4
+    assert abi.echo_lstm_bwd_ws_bytes(abi.LstmDesc(B, H, abi.BF16, abi.RECOMPUTE), T) == T * B * H * 4
+    assert abi.echo_lstm_bwd_ws_bytes(abi.LstmDesc(B, H, abi.FP32, abi.STASH), T) == 0
+    d = abi.AttnDesc(B, 50, 512, 512, abi.BF16, abi.RECOMPUTE, 512, B * 512, 512, B * 512)
+    assert abi.echo_attn_bwd_ws_bytes(d) == B * 512 * 4
+    with pytest.raises(abi.EchoError) as e:                   # t out of range is rejected before the query
+        abi.echo_lstm_bwd_recompute(abi.LstmDesc(B, H, abi.FP32, abi.RECOMPUTE), T, T, 0, *([None] * 9), stream=0)
+    assert e.value.status == abi.ECHO_ERR_INVALID
 
 
 def test_every_declared_symbol_is_exported(lib):

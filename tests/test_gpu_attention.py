@@ -41,9 +41,9 @@ def _run_attn(abi, d, storage, mode, layout):
     dHs = torch.zeros_like(Hs, dtype=torch.float32)
     dvp = torch.zeros(B, A, device="cuda")
     creg = torch.empty_like(ctx) if mode == abi.RECOMPUTE else None
-    abi.echo_attn_bwd(desc, qp, Kp, v, Hs, sl, E, al, dctx, dqp, dKp, dHs, dvp, creg)
+    assert abi.echo_attn_bwd_ws_bytes(desc) == B * A * 4          # two-call workspace query
     dv = torch.empty(A, device="cuda")
-    abi.echo_attn_dv_reduce(B, A, dvp, dv, 0)
+    abi.echo_attn_bwd_recompute(desc, qp, Kp, v, Hs, sl, E, al, dctx, dqp, dKp, dHs, dv, creg, dvp, B * A * 4)
     if layout != "bsk":
         dKp = dKp.transpose(0, 1)
         dHs = dHs.transpose(0, 1)
@@ -166,8 +166,8 @@ def test_attention_deferred_bitwise(storage, B, Ts, A, Hk, Td, cuda_dev):
                     abi.echo_attn_bwd_deferred(desc, *args, v, Hs, sl, *e_a, dctxs[t], dqp[t], dvp,
                                                None if st else creg[t], ds_all[t], None if st else al_all[t])
                 else:
-                    abi.echo_attn_bwd(desc, *args, v, Hs, sl, *e_a, dctxs[t], dqp[t], dKp, dHs, dvp,
-                                      None if st else creg[t])
+                    abi.echo_attn_bwd_recompute(desc, *args, v, Hs, sl, *e_a, dctxs[t], dqp[t], dKp, dHs, None,
+                                                None if st else creg[t], dvp)
             if deferred:
                 abi.echo_attn_bwd_finish(desc, Td, None if st else qps, None if st else Kp, E if st else None, v, sl,
                                          ds_all, al_all, dctxs, dKp, dHs)
@@ -181,7 +181,9 @@ def test_attention_deferred_bitwise(storage, B, Ts, A, Hk, Td, cuda_dev):
 @pytest.mark.parametrize("storage", ["fp32", "bf16"])
 def test_attention_c5_launch_sampled_rows(storage, cuda_dev):
     """C5's launch configuration (B = 24576 rows, Ts = 50, A = Hk = 512: the shape bench.py's C5
-    leg times) on sampled rows the oracle computes one by one; every row's softmax sums to one."""
+    leg times), both modes, on sampled rows the oracle computes one by one; every row's softmax sums
+    to one; RECOMPUTE's regenerated ctx equals the forward's and its gradients equal STASH's, bitwise
+    over all rows."""
     abi = _abi()
     B, Ts, A, Hk = 24576, 50, 512, 512
     dt = abi.FP32 if storage == "fp32" else abi.BF16
@@ -193,29 +195,42 @@ def test_attention_c5_launch_sampled_rows(storage, cuda_dev):
     v = (torch.randn(A, device="cuda", generator=g) * 0.2).to(sd)
     sl = torch.randint(1, Ts + 1, (B,), device="cuda", generator=g).to(torch.int32)
     dctx = torch.randn(B, Hk, device="cuda", generator=g)
-    desc = abi.AttnDesc(B, Ts, A, Hk, dt, abi.STASH, A, B * A, Hk, B * Hk)
-    ctx = torch.empty(B, Hk, device="cuda", dtype=sd)
-    Z = torch.empty(B, Ts, A, device="cuda", dtype=sd)
-    al = torch.empty(B, Ts, device="cuda")
-    abi.echo_attn_fwd(desc, qp, Kp, v, Hs, sl, ctx, Z, al)
-    dqp = torch.empty(B, A, device="cuda")
-    dKp = torch.zeros(Ts, B, A, device="cuda")
-    dHs = torch.zeros(Ts, B, Hk, device="cuda")
-    dvp = torch.zeros(B, A, device="cuda")
-    abi.echo_attn_bwd(desc, None, None, v, Hs, sl, Z, al, dctx, dqp, dKp, dHs, dvp, None)
-    torch.cuda.synchronize()
-    rows = al.sum(1)
-    assert torch.allclose(rows, torch.ones_like(rows), atol=1e-5)
-    for b in (0, 1, 4097, 12345, B - 1):
-        n = int(sl[b])
-        f64 = lambda x: x.double().cpu().numpy()
-        ref = OA.backward(f64(qp[b:b + 1]), f64(Kp[:, b:b + 1].transpose(0, 1)), f64(v),
-                          f64(Hs[:, b:b + 1].transpose(0, 1)), f64(dctx[b:b + 1]), src_len=np.array([n], np.int32))
-        assert_close(host(ctx[b:b + 1]), ref["ctx"], storage, f"ctx[{b}]")
-        assert_close(host(dqp[b:b + 1]), ref["dqp"], storage, f"dqp[{b}]")
-        assert_close(host(dKp[:, b:b + 1].transpose(0, 1)), ref["dKp"], storage, f"dKp[{b}]")
-        assert_close(host(dHs[:, b:b + 1].transpose(0, 1)), ref["dHs"], storage, f"dHs[{b}]")
-        assert_close(host(dvp[b]), ref["dv"], storage, f"dv[{b}]")
+    res = {}
+    for mode in (abi.STASH, abi.RECOMPUTE):
+        st = mode == abi.STASH
+        desc = abi.AttnDesc(B, Ts, A, Hk, dt, mode, A, B * A, Hk, B * Hk)
+        ctx = torch.empty(B, Hk, device="cuda", dtype=sd)
+        Z = torch.empty(B, Ts, A, device="cuda", dtype=sd) if st else None
+        al = torch.empty(B, Ts, device="cuda") if st else None
+        abi.echo_attn_fwd(desc, qp, Kp, v, Hs, sl, ctx, Z, al)
+        dqp = torch.empty(B, A, device="cuda")
+        dKp = torch.zeros(Ts, B, A, device="cuda")
+        dHs = torch.zeros(Ts, B, Hk, device="cuda")
+        dvp = torch.zeros(B, A, device="cuda")
+        dv = torch.empty(A, device="cuda")
+        creg = None if st else torch.empty_like(ctx)
+        abi.echo_attn_bwd_recompute(desc, None if st else qp, None if st else Kp, v, Hs, sl, Z, al, dctx, dqp, dKp,
+                                    dHs, dv, creg, dvp)
+        torch.cuda.synchronize()
+        if st:
+            rows = al.sum(1)
+            assert torch.allclose(rows, torch.ones_like(rows), atol=1e-5)
+            del Z, al
+        else:
+            assert bits_equal(creg, ctx)
+        for b in (0, 1, 4097, 12345, B - 1):
+            n = int(sl[b])
+            f64 = lambda x: x.double().cpu().numpy()
+            ref = OA.backward(f64(qp[b:b + 1]), f64(Kp[:, b:b + 1].transpose(0, 1)), f64(v),
+                              f64(Hs[:, b:b + 1].transpose(0, 1)), f64(dctx[b:b + 1]), src_len=np.array([n], np.int32))
+            assert_close(host(ctx[b:b + 1]), ref["ctx"], storage, f"ctx[{b}]")
+            assert_close(host(dqp[b:b + 1]), ref["dqp"], storage, f"dqp[{b}]")
+            assert_close(host(dKp[:, b:b + 1].transpose(0, 1)), ref["dKp"], storage, f"dKp[{b}]")
+            assert_close(host(dHs[:, b:b + 1].transpose(0, 1)), ref["dHs"], storage, f"dHs[{b}]")
+            assert_close(host(dvp[b]), ref["dv"], storage, f"dv[{b}]")
+        res[mode] = (ctx, dqp, dKp, dHs, dvp, dv)
+    for k, (x, y) in enumerate(zip(res[abi.STASH], res[abi.RECOMPUTE])):
+        assert bits_equal(x, y), k
 
 
 def test_attention_rejects_bad_arguments(cuda_dev):

@@ -54,10 +54,10 @@ def test_cell_fwd_bwd_step(storage, mode, B, H, cuda_dev):
     dc = dev(d["dc"], dtype=torch.float32)
     dA = torch.empty_like(A)
     hreg = torch.empty_like(h) if m == abi.RECOMPUTE else None
-    if m == abi.STASH:
-        abi.echo_lstm_bwd(desc, gates, cp, None, tc, dh, dc, dA, None)
-    else:
-        abi.echo_lstm_bwd(desc, gates, cp, c, None, dh, dc, dA, hreg)
+    if m == abi.STASH:                      # one step: T = 1, t = 0, c_0 = c_prev
+        abi.echo_lstm_bwd_recompute(desc, 1, 0, 0, gates, cp, None, tc, dh, dc, dA, None, None)
+    else:                                   # the a2 workspace holds c_1 = c
+        abi.echo_lstm_bwd_recompute(desc, 1, 0, 0, gates, cp, None, None, dh, dc, dA, hreg, c)
         assert bits_equal(hreg, h)          # regenerated h_t bit-identical to the forward's
     rdA, rdc = O.cell_backward(np.asarray(d["A"], np.float64), np.asarray(d["c_prev"], np.float64),
                                np.asarray(d["dh"], np.float64), np.asarray(d["dc"], np.float64))
@@ -123,6 +123,63 @@ def test_cscan_matches_forward_c_bitwise(cuda_dev):
     abi.echo_lstm_cscan(abi.LstmDesc(B, H, abi.FP32, abi.RECOMPUTE), T, S.gates, S.c0, cws, hws)
     assert bits_equal(cws, S.c)
     assert bits_equal(hws, S.h)          # mirrored layer outputs regenerate bit-identically
+
+
+@pytest.mark.parametrize("storage", STORAGES)
+def test_bwd_recompute_regen_flag_and_ws_query(storage, cuda_dev):
+    """echo_lstm_bwd_recompute with ECHO_BWD_REGEN_C on the first backward call (the a2 prologue
+    inside the entry point, workspace sized by the two-call query) == the layer driver's separate
+    scan + per-step calls, bitwise; the STASH calls through the same entry point agree too."""
+    abi = _abi()
+    from paper_1805_08899_b200.lstm import LSTMLayer
+    T, B, I, H = 12, 6, 16, 40
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    d = lstm_layer_inputs(8, T, B, I, H, storage)
+    ins = lambda: (dev(d["X"], storage), dev(d["Wx"], storage), dev(d["Wh"], storage), dev(d["b"], dtype=torch.float32),
+                   dev(d["h0"], storage), dev(d["c0"], dtype=torch.float32))
+    dH = dev(d["dH"], dtype=torch.float32)
+    res = {}
+    for mode in (abi.STASH, abi.RECOMPUTE):
+        L = LSTMLayer(T, B, H, dt, mode)
+        L.forward_seq(*ins())
+        desc = abi.LstmDesc(B, H, dt, mode)
+        nb = abi.echo_lstm_bwd_ws_bytes(desc, T)
+        assert nb == (T * B * H * 4 if mode == abi.RECOMPUTE else 0)
+        ws = torch.full((max(nb, 4) // 4,), float("nan"), device="cuda")
+        gates = L.gates.clone()
+        dc = torch.zeros(B, H, device="cuda")
+        hreg = torch.empty(T, B, H, device="cuda", dtype=L.sd)
+        for t in reversed(range(T)):
+            if mode == abi.RECOMPUTE:
+                abi.echo_lstm_bwd_recompute(desc, T, t, abi.ECHO_BWD_REGEN_C if t == T - 1 else 0, gates, L.c0, None,
+                                            None, dH[t], dc, gates[t], hreg[t], ws, nb)
+            else:
+                abi.echo_lstm_bwd_recompute(desc, T, t, 0, gates, L.c0, L.c, L.tc, dH[t], dc, gates[t], None, None)
+        res[mode] = (gates, dc)
+        if mode == abi.RECOMPUTE:
+            assert bits_equal(hreg, L.h)
+        # the driver's path (separate scan + per-step calls) on the same stashed gates
+        L.prepare_backward()
+        dc2 = torch.zeros(B, H, device="cuda")
+        for t in reversed(range(T)):
+            L.bwd_step(t, dH[t], dc2)
+        assert bits_equal(L.gates, gates) and bits_equal(dc2, dc)
+    assert bits_equal(res[abi.STASH][0], res[abi.RECOMPUTE][0]) and bits_equal(res[abi.STASH][1], res[abi.RECOMPUTE][1])
+    # validation: t out of range, flag in STASH mode, workspace too small
+    desc = abi.LstmDesc(B, H, dt, abi.RECOMPUTE)
+    g = torch.empty(T, B, 4 * H, device="cuda", dtype=L.sd)
+    c0 = torch.zeros(B, H, device="cuda")
+    for args, st in (((T, T, 0), abi.ECHO_ERR_INVALID), ((T, 0, 4), abi.ECHO_ERR_INVALID)):
+        with pytest.raises(abi.EchoError) as e:
+            abi.echo_lstm_bwd_recompute(desc, *args, g, c0, None, None, c0, c0.clone(), g[0], None, ws)
+        assert e.value.status == st
+    with pytest.raises(abi.EchoError) as e:
+        abi.echo_lstm_bwd_recompute(desc, T, 0, 0, g, c0, None, None, c0, c0.clone(), g[0], None, ws, 16)
+    assert e.value.status == abi.ECHO_ERR_CAPACITY
+    with pytest.raises(abi.EchoError) as e:
+        abi.echo_lstm_bwd_recompute(abi.LstmDesc(B, H, dt, abi.STASH), T, 0, abi.ECHO_BWD_REGEN_C, g, c0, g, g, c0,
+                                    c0.clone(), g[0], None, None)
+    assert e.value.status == abi.ECHO_ERR_INVALID
 
 
 def test_validation_errors(cuda_dev):
@@ -206,5 +263,6 @@ def test_mirror_parts_kernels(storage, n_parts, B, H, cuda_dev):
         abi.echo_lstm_fwd(desc, A[T - 1].contiguous(), None, None, c[T - 1], gates, cc, None, hh)
         dc2 = dc_in.clone()
         dA2 = torch.empty_like(dA)
-        abi.echo_lstm_bwd(desc, gates, c[T - 1], c[T], None, dh, dc2, dA2, None)
+        abi.echo_lstm_bwd_recompute(abi.LstmDesc(B, H, abi.FP32, abi.RECOMPUTE), 1, 0, 0, gates, c[T - 1], None, None,
+                                    dh, dc2, dA2, None, c[T])
         assert bits_equal(dA, dA2) and bits_equal(dc, dc2)

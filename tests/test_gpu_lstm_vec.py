@@ -37,9 +37,9 @@ dc = torch.from_numpy(np.asarray(d["dc"], np.float32)).cuda()
 dA = torch.empty_like(A)
 hreg = torch.empty_like(h) if m == abi.RECOMPUTE else None
 if m == abi.STASH:
-    abi.echo_lstm_bwd(desc, gates, cp, None, tc, dh, dc, dA, None)
+    abi.echo_lstm_bwd_recompute(desc, 1, 0, 0, gates, cp, None, tc, dh, dc, dA, None, None)
 else:
-    abi.echo_lstm_bwd(desc, gates, cp, c, None, dh, dc, dA, hreg)
+    abi.echo_lstm_bwd_recompute(desc, 1, 0, 0, gates, cp, None, None, dh, dc, dA, hreg, c)
 T = 7
 G = torch.rand(T, B, 4 * H, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3)).to(sd)
 cws = torch.empty(T, B, H, device="cuda"); hws = torch.empty(T, B, H, device="cuda", dtype=sd)

@@ -7,11 +7,15 @@ import torch
 from oracle import nmt as O
 from synth.configs import C1, SMALL_NMT, C2, NMTConfig
 from synth.data import nmt_params, nmt_batch
-from tests.gpu_util import relerr, relerr_fro, bits_equal
+from tests.gpu_util import relerr, bits_equal, check_grads
 
 pytestmark = pytest.mark.gpu
 
 RAGGED = NMTConfig("ragged", B=5, Ts=11, Td=7, E=24, H=40, A=32, V=50, enc_layers=2, dec_layers=2)
+
+# bf16 storage: tensors gated on the Frobenius relative error instead of the inf-norm (reading R14b,
+# DESIGN.md, with each tensor's measured error and bf16 noise floor).  Everything else: inf-norm.
+FRO_ONLY = {}
 
 
 @pytest.fixture(autouse=True)
@@ -46,10 +50,7 @@ def test_nmt_step_parity_and_bit_identity(cfg, storage, cuda_dev):
         m, loss = _run(cfg, params, batch, dt, mode)
         assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"]), (loss, ref["loss"])
         g = m.grads_numpy()
-        # fp32: inf-norm relative <= 1e-4; bf16 storage: Frobenius relative <= 2e-2 (reading R14)
-        metric = relerr if storage == "fp32" else relerr_fro
-        for k, v in ref["grads"].items():
-            assert metric(g[k], v) <= tol, (k, metric(g[k], v), relerr(g[k], v))
+        check_grads(g, ref["grads"], storage, FRO_ONLY.get((cfg.name, storage), ()), f"{cfg.name}/{mode}")
         res[mode] = (m.gflat.clone(), m.loss.clone())
     assert bits_equal(res[abi.STASH][0], res[abi.RECOMPUTE][0])
     assert bits_equal(res[abi.STASH][1], res[abi.RECOMPUTE][1])
@@ -93,20 +94,24 @@ def test_nmt_c2_eager_graph_bitwise(storage, cuda_dev):
 
 @pytest.mark.parametrize("storage", ["fp32", "bf16"])
 def test_nmt_c2_full_size_parity(storage, cuda_dev):
-    """C2 (B=128, T=50, H=512, V=8192) one step vs the fp64 oracle (all gradients), RECOMPUTE,
-    in the launch configuration bench.py times."""
+    """C2 (B=128, T=50, H=512, V=8192) one step vs the fp64 oracle (all gradients) in the launch
+    configuration bench.py times, in BOTH modes; STASH == RECOMPUTE bitwise (loss and every gradient)
+    at full size."""
     from paper_1805_08899_b200 import abi
     cfg = C2
     params = nmt_params(3, cfg, storage)
     batch = nmt_batch(4, cfg, lengths="random")
     ref = O.step(params, batch, cfg)
-    m, loss = _run(cfg, params, batch, abi.FP32 if storage == "fp32" else abi.BF16, abi.RECOMPUTE)
     tol = 1e-4 if storage == "fp32" else 2e-2
-    metric = relerr if storage == "fp32" else relerr_fro
-    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
-    g = m.grads_numpy()
-    for k, v in ref["grads"].items():
-        assert metric(g[k], v) <= tol, (k, metric(g[k], v))
+    res = {}
+    for mode in (abi.RECOMPUTE, abi.STASH):
+        m, loss = _run(cfg, params, batch, abi.FP32 if storage == "fp32" else abi.BF16, mode)
+        assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
+        check_grads(m.grads_numpy(), ref["grads"], storage, FRO_ONLY.get((cfg.name, storage), ()), f"C2/{mode}")
+        res[mode] = (m.gflat.clone(), m.loss.clone())
+        del m
+    assert bits_equal(res[abi.STASH][0], res[abi.RECOMPUTE][0])
+    assert bits_equal(res[abi.STASH][1], res[abi.RECOMPUTE][1])
 
 
 def test_stash_bytes_ratio_c2(cuda_dev):
@@ -186,15 +191,13 @@ def test_nmt_mirror_plan_parity_and_graph(cfg, storage, cuda_dev):
     ref = O.step(params, batch, cfg)
     dt = abi.FP32 if storage == "fp32" else abi.BF16
     tol = 1e-4 if storage == "fp32" else 2e-2
-    metric = relerr if storage == "fp32" else relerr_fro
     m = NMTModel(cfg, dt, abi.RECOMPUTE, mirror=True)
     m.load_params(params)
     m.upload_batch(batch)
     loss = m.train_step(lr=0.0)
     assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"]), (loss, ref["loss"])
     g = m.grads_numpy()
-    for k, v in ref["grads"].items():
-        assert metric(g[k], v) <= tol, (k, metric(g[k], v))
+    check_grads(g, ref["grads"], storage, FRO_ONLY.get((cfg.name, storage), ()), f"{cfg.name}/mirror")
     eager = m.gflat.clone()
     m.capture(0.0)
     m.gflat.zero_()
@@ -225,7 +228,6 @@ def test_nmt_embedding_dropout_plans(cfg, storage, cuda_dev):
     ref = O.step(params, batch, cfg)
     dt = abi.FP32 if storage == "fp32" else abi.BF16
     tol = 1e-4 if storage == "fp32" else 2e-2
-    metric = relerr if storage == "fp32" else relerr_fro
     doc = json.dumps(Gr.nmt(cfg, "f32" if storage == "fp32" else "bf16"))
     plans = {"stash": (abi.STASH, False, False, "baseline"), "echo": (abi.RECOMPUTE, False, False, "echo"),
              "echo-regen": (abi.RECOMPUTE, False, True, "echo"), "mirror": (abi.RECOMPUTE, True, False, "mirror")}
@@ -242,8 +244,7 @@ def test_nmt_embedding_dropout_plans(cfg, storage, cuda_dev):
         loss = float(m.loss.item())
         assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"]), (name, loss, ref["loss"])
         g = m.grads_numpy()
-        for k, v in ref["grads"].items():
-            assert metric(g[k], v) <= tol, (name, k, metric(g[k], v))
+        check_grads(g, ref["grads"], storage, FRO_ONLY.get((cfg.name, storage), ()), f"{cfg.name}/{name}")
         res[name] = m.gflat.clone()
     assert bits_equal(res["stash"], res["echo"]) and bits_equal(res["stash"], res["echo-regen"])
 

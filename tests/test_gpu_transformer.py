@@ -10,7 +10,7 @@ import torch
 from oracle import transformer as O
 from synth.configs import SMALL_TX, C4
 from synth.data import tx_params, tx_batch
-from tests.gpu_util import relerr, relerr_fro, bits_equal
+from tests.gpu_util import relerr, bits_equal, check_grads
 
 pytestmark = pytest.mark.gpu
 
@@ -28,8 +28,13 @@ def _run(cfg, params, batch, dtype, mode, mirror=False, regen=False):
     return m, m.train_step(lr=0.0)
 
 
-@pytest.mark.parametrize("cfg,storage", [(SMALL_TX, "fp32"), (SMALL_TX, "bf16"),
-                                         (replace(C4, blocks=2), "fp32")], ids=["small-fp32", "small-bf16", "C4x2-fp32"])
+# bf16 storage: tensors gated on the Frobenius relative error (reading R14b); the rest on the inf-norm.
+FRO_ONLY = {}
+
+
+@pytest.mark.parametrize("cfg,storage", [(SMALL_TX, "fp32"), (SMALL_TX, "bf16"), (replace(C4, blocks=2), "fp32"),
+                                         (replace(C4, blocks=2), "bf16")],
+                         ids=["small-fp32", "small-bf16", "C4x2-fp32", "C4x2-bf16"])
 def test_tx_parity_and_bit_identity(cfg, storage, cuda_dev):
     from paper_1805_08899_b200 import abi
     params = tx_params(1, cfg, storage)
@@ -37,7 +42,6 @@ def test_tx_parity_and_bit_identity(cfg, storage, cuda_dev):
     ref = O.step(params, batch, cfg)
     dt = abi.FP32 if storage == "fp32" else abi.BF16
     tol = 1e-4 if storage == "fp32" else 2e-2
-    metric = relerr if storage == "fp32" else relerr_fro
     res = {}
     plans = ((abi.STASH, False, False), (abi.RECOMPUTE, False, False), (abi.RECOMPUTE, True, False),
              (abi.RECOMPUTE, False, True), (abi.RECOMPUTE, True, True))
@@ -45,8 +49,8 @@ def test_tx_parity_and_bit_identity(cfg, storage, cuda_dev):
         m, loss = _run(cfg, params, batch, dt, mode, mirror, regen)
         assert abs(loss - ref["loss"]) <= tol * max(abs(ref["loss"]), 1e-3), (loss, ref["loss"])
         g = m.grads_numpy()
-        for k, v in ref["grads"].items():
-            assert metric(g[k], v) <= tol, (k, metric(g[k], v))
+        check_grads(g, ref["grads"], storage, FRO_ONLY.get((cfg.name, cfg.blocks, storage), ()),
+                    f"{cfg.name}/{mode}/{mirror}/{regen}")
         res[(mode, mirror, regen)] = m.gflat.clone()
     for p in plans[1:]:               # Echo, Mirror, and both with regenerated masks: the same gradients
         assert bits_equal(res[plans[0]], res[p]), p
