@@ -6,7 +6,9 @@ Every .cu / .cpp under csrc/ is compiled with
     -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo
 (no --use_fast_math: the rounding contract relies on IEEE expf/tanhf and
 explicit __f*_rn intrinsics) and linked into paper_1805_08899_b200/libecho.so.
-Rebuilds only when a source or header is newer than the library.
+Rebuilds when a source or header is newer than the library or when the build flags (ECHO_NVCC_EXTRA)
+differ from the ones recorded in the stamp file next to it (libecho.so.flags), so an instrumented
+build (e.g. -DECHO_PHASE_TIMING) is never picked up silently by a later plain build() call.
 """
 from __future__ import annotations
 
@@ -33,8 +35,21 @@ def _deps():
         [os.path.join(ROOT, "include", "echo.h"), os.path.abspath(__file__)]
 
 
+STAMP = LIB + ".flags"
+
+
+def _flags() -> str:
+    return " ".join(os.environ.get("ECHO_NVCC_EXTRA", "").split())
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(STAMP) as f:
+            if f.read().strip() != _flags():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(p) > t for p in _deps())
@@ -64,6 +79,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(_flags() + "\n")
     return LIB
 
 

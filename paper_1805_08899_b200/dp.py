@@ -47,6 +47,81 @@ def allreduce_mean_(flat: torch.Tensor) -> torch.Tensor:
     return flat
 
 
+def backend_name():
+    return dist.get_backend() if dist.is_initialized() else None
+
+
+def world_size() -> int:
+    return dist.get_world_size() if dist.is_initialized() else 1
+
+
+class BucketAllreduce:
+    """Overlapped gradient exchange (SURVEY.md §8(e) option): each bucket -- a contiguous slice of the
+    flat fp32 gradient whose values are final -- is summed across ranks on a dedicated communication
+    stream as soon as the backward pass reaches it, while the compute stream goes on with the rest of
+    the backward (the NMT decoder / attention / output bucket overlaps the encoder backward).
+    finish() makes the compute stream wait for every launched bucket and divides by the world size,
+    so the result equals allreduce_mean_ of the whole buffer."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.cuda = self.device.type == "cuda"
+        self.stream = torch.cuda.Stream(device=self.device) if self.cuda else None
+        self.works = []
+
+    def launch(self, bucket: torch.Tensor):
+        if world_size() == 1:
+            return
+        if not self.cuda:                                  # host tensors (the gloo CPU tests)
+            self.works.append((dist.all_reduce(bucket, op=dist.ReduceOp.SUM, async_op=True), bucket))
+            return
+        cur = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(cur)                       # the bucket's producers are done
+        with torch.cuda.stream(self.stream):
+            self.works.append((dist.all_reduce(bucket, op=dist.ReduceOp.SUM, async_op=True), bucket))
+            bucket.record_stream(self.stream)
+
+    def finish(self, flat: torch.Tensor):
+        if world_size() == 1:
+            return flat
+        for w, _ in self.works:
+            w.wait()                                       # compute stream waits (NCCL) / host waits (gloo)
+        if self.cuda:
+            torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        self.works = []
+        flat.div_(world_size())
+        return flat
+
+
+def time_allreduce(numel: int, device, steps: int = 20, warmup: int = 3) -> dict:
+    """The step's gradient exchange in isolation: `steps` sum-allreduces of a `numel` fp32 buffer,
+    CUDA events on the launching stream, max over ranks.  algbw = bytes / time; busbw = algbw *
+    2 (N-1) / N (the ring-equivalent bytes each GPU moves)."""
+    n = world_size()
+    buf = torch.zeros(numel, dtype=torch.float32, device=device)
+    for _ in range(warmup):
+        dist.all_reduce(buf)
+    torch.cuda.synchronize(device)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        dist.all_reduce(buf)
+    e1.record()
+    torch.cuda.synchronize(device)
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, device)
+    nbytes = numel * 4
+    algbw = nbytes / (ms / 1e3) / 1e9
+    out = {"bytes": nbytes, "ms": ms, "algbw_GBps": algbw, "busbw_GBps": algbw * 2 * (n - 1) / n,
+           "backend": dist.get_backend(), "nranks": n, "timing": f"{steps} allreduces, CUDA events, max over ranks"}
+    try:
+        v = torch.cuda.nccl.version()
+        out["nccl_version"] = ".".join(map(str, v)) if isinstance(v, tuple) else str(v)
+    except Exception:
+        pass
+    return out
+
+
 def max_over_ranks(x: float, device=None) -> float:
     if not (dist.is_initialized() and dist.get_world_size() > 1):
         return x

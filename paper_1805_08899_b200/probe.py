@@ -40,6 +40,7 @@ class GraphStep:
         """with_probe=True also records timing events around every hot-path launch; after a replay,
         kernel_times() returns their durations for that step."""
         global ACTIVE
+        self.graph_seeds = self.seed_state()
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
@@ -59,6 +60,18 @@ class GraphStep:
 
     def replay(self):
         self.graph.replay()
+
+    def seed_state(self):
+        """The host-side dropout Philox keys this driver passes to its kernels (kernel arguments, so a
+        captured graph bakes them in); None if it has none."""
+        return None
+
+    def check_seeds(self, new):
+        """Refuse new dropout keys once a graph is captured (replay would silently reuse the
+        captured masks).  Re-capture to change them."""
+        if getattr(self, "graph_seeds", None) is not None and tuple(new) != tuple(self.graph_seeds):
+            raise ValueError(f"dropout seeds {tuple(new)} differ from the ones captured in the step graph "
+                             f"{tuple(self.graph_seeds)}: they are kernel arguments; re-capture() to change them")
 
     def kernel_times(self):
         """{name: [ms per launch]} of the probed launches in the most recent replay (synchronizes)."""

@@ -72,13 +72,19 @@ class TXModel(probe.GraphStep):
     def upload_batch(self, batch):
         x = batch["x"] if isinstance(batch["x"], torch.Tensor) else torch.from_numpy(np.ascontiguousarray(batch["x"]))
         self.x.copy_(x.reshape(self.x.shape).to(self.sd), non_blocking=True)
-        self.seeds = [int(s) for s in batch["seeds"]]
+        seeds = [int(s) for s in batch["seeds"]]
+        if self.cfg.dropout_p > 0.0:
+            self.check_seeds(seeds)
+        self.seeds = seeds
 
     def input_bytes(self):
         return self.x.numel() * self.x.element_size()
 
     def grads_numpy(self):
         return {k: v.detach().double().cpu().numpy() for k, v in self.G.items()}
+
+    def seed_state(self):
+        return tuple(self.seeds) if self.cfg.dropout_p > 0.0 else None
 
     def stash_bytes(self):
         seen, total = set(), 0

@@ -35,7 +35,14 @@ def _worker(rank, world, port, out):
     batch = nmt_batch(dp.shard_seed(7, rank), cfg, lengths="random")
     g = O.step(params, batch, cfg)["grads"]
     flat = torch.cat([torch.from_numpy(g[n].astype(np.float32).reshape(-1)) for n, _ in nmt_param_shapes(cfg)])
+    buck = flat.clone()
     dp.allreduce_mean_(flat)
+    ar = dp.BucketAllreduce("cpu")                         # the overlapped two-bucket exchange, same result
+    n0 = buck.numel() // 3
+    ar.launch(buck[:n0])
+    ar.launch(buck[n0:])
+    ar.finish(buck)
+    assert torch.equal(buck, flat)
     m = dp.max_over_ranks(float(rank))
     if rank == 0:
         out.put((flat.numpy(), m))

@@ -30,3 +30,17 @@ def test_bench_two_ranks(quick, cuda_dev):
     assert d["value"] > 0 and d["scaling"] == "weak"
     if not quick:
         assert d["roofline"]["frac"] > 0 and "memory" in d and "configs_extra" not in d
+
+
+def test_bench_gpus_flag_relaunches(cuda_dev):
+    """`python bench.py --gpus 2` (no torchrun) re-executes itself under torch.distributed.run with two
+    ranks (sharing the pool's single GPU over gloo) and reports n_gpus = 2 and the isolated allreduce."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+                        "--quick"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
+    assert d["allreduce"]["nranks"] == 2 and d["allreduce"]["bytes"] > 0
+

@@ -15,7 +15,8 @@ RAGGED = NMTConfig("ragged", B=5, Ts=11, Td=7, E=24, H=40, A=32, V=50, enc_layer
 
 # bf16 storage: tensors gated on the Frobenius relative error instead of the inf-norm (reading R14b,
 # DESIGN.md, with each tensor's measured error and bf16 noise floor).  Everything else: inf-norm.
-FRO_ONLY = {}
+_QUERY_PATH = ("att.bq", "att.Wq", "att.v")
+FRO_ONLY = {("small-nmt", "bf16"): _QUERY_PATH, ("ragged", "bf16"): _QUERY_PATH, ("ragged-drop", "bf16"): _QUERY_PATH}
 
 
 @pytest.fixture(autouse=True)
@@ -283,3 +284,21 @@ def test_dropout_kernels(storage, n, p, cuda_dev):
         outs[kind] = dx
         assert bits_equal(dx, dy * torch.from_numpy(np.where(keep, ik, np.float32(0.0))).cuda())
     assert bits_equal(outs[abi.MASK_NONE], outs[abi.MASK_BITS]) and bits_equal(outs[abi.MASK_BITS], outs[abi.MASK_BYTES])
+
+
+def test_graph_refuses_new_dropout_seeds(cuda_dev):
+    """The Philox keys are kernel arguments baked into the captured step graph: after capture(),
+    upload_batch() with different keys raises instead of silently replaying the old masks (ADVICE r1);
+    the same keys are accepted."""
+    from paper_1805_08899_b200 import abi
+    from paper_1805_08899_b200.nmt import NMTModel
+    cfg = RAGGED_DROP
+    m = NMTModel(cfg, abi.FP32, abi.RECOMPUTE)
+    m.load_params(nmt_params(1, cfg))
+    b = nmt_batch(2, cfg, lengths="random")
+    m.upload_batch(b)
+    m.capture(0.0)
+    m.upload_batch(b)
+    b2 = dict(b, drop_seeds=np.asarray(b["drop_seeds"]) + 1)
+    with pytest.raises(ValueError):
+        m.upload_batch(b2)
