@@ -802,7 +802,37 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(m) : "memory");
 }
 
+// ---- DSMEM push exchange (no cluster-wide barrier on the data path): each CTA sends its partial
+// scores into every cluster CTA's receive buffer with st.async, completing on the receiver's
+// mbarrier (expect_tx set at kernel entry, before the single start-up cluster barrier).
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(remote_addr),
+               "r"(__float_as_uint(v)), "r"(remote_bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_async_v2(uint32_t remote_addr, float x, float y, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];\n" ::"r"(remote_addr),
+               "r"(__float_as_uint(x)), "r"(__float_as_uint(y)), "r"(remote_bar)
+               : "memory");
+}
+
 // Shared-memory tiles: [Tr][box width] per tensor for this CTA's column slice.
+// Forward, no data-path cluster barrier: after phase 1 every warp holds its positions' partial
+// scores and pushes them (st.async) into the C receive rows xpart[rank][*] of every cluster CTA;
+// each CTA waits on its own exchange mbarrier, and EVERY warp then forms the scores in rank order
+// (the gather_sum arithmetic), runs the softmax in registers (the softmax_row_warp arithmetic) and
+// the ctx warps read alpha_s by shuffle (the ctx_columns arithmetic) -- so alpha and ctx are bit-
+// identical to the backward's regenerated ones, with no __syncthreads / cluster barrier after the
+// start-up one that publishes the mbarrier initialisation.
 template <typename T>
 __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, TmaGeo q,
                                                             const __grid_constant__ CUtensorMap mK,
@@ -812,22 +842,21 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
                                                             T* __restrict__ Z_st, float* __restrict__ alpha_st) {
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(1024) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];   // TMA (no swizzle) needs 128-B alignment
   __shared__ __align__(8) uint64_t bar[TMA_CHUNKS];
+  __shared__ __align__(8) uint64_t xbar;
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
-  const Slice g = make_slice_g(q, A, Hk, (int)cl.block_rank());
+  const int rank = (int)cl.block_rank();
+  const Slice g = make_slice_g(q, A, Hk, rank);
   const int W = g.a1 - g.a0, WH = g.h1 - g.h0;               // valid widths
   const int Wb = q.Wb, WHb = q.WHb;                           // box widths (smem row strides)
   const int Tp = (Ts + 3) & ~3;
-  const int R = q.R, Tr = q.Tr;
+  const int R = q.R, Tr = q.Tr, C = q.C;
   T* kz = reinterpret_cast<T*>(smraw);                                         // [Tr][Wb]
   T* hs = reinterpret_cast<T*>(smraw + al128((size_t)Tr * Wb * sizeof(T)));    // [Tr][WHb]
   T* qps = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(hs) + al128((size_t)Tr * WHb * sizeof(T)));
   T* vs = qps + Wb;                                                            // Wb * sizeof(T) is 16-B aligned
-  float* f = reinterpret_cast<float*>(vs + Wb);
-  float* sc_part = f;
-  float* sc = sc_part + Tp;
-  float* al = sc + Tp;
+  float* xpart = reinterpret_cast<float*>(vs + Wb);                            // [C][Tp] received partials
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
   const uint64_t pol = l2_policy(q.l2last);
@@ -835,12 +864,15 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
     prefetch_tmap(&mK);
     prefetch_tmap(&mH);
     for (int k = 0; k < TMA_CHUNKS; ++k) mbar_init(&bar[k], 1);
+    mbar_init(&xbar, 1);
     fence_mbar_init();
+    mbar_expect_tx(&xbar, (uint32_t)(C * n * 4));            // n partial scores from each of the C CTAs
     SmallCopy sm{{qps, vs, nullptr}, {qp + (long)b * A + g.a0, v + g.a0, nullptr},
                  {(uint32_t)(W * sizeof(T)), (uint32_t)(W * sizeof(T)), 0u}};
     issue_chunks(bar, n, R, kz, &mK, g.a0, hs, &mH, g.h0, b, Wb * sizeof(T), WHb * sizeof(T), sm, pol);
   }
   __syncthreads();                                            // barrier init visible before anyone waits
+  cluster_arrive_relaxed();                                   // publishes xbar's init (fenced above)
   mbar_wait(&bar[0], 0);                                      // chunk 0 + the qp / v slices
   const bool act = lane < W / 4;                              // W <= 128: one column group per lane
   float qr[4] = {0.0f, 0.0f, 0.0f, 0.0f}, vr[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -848,6 +880,10 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
     lds4(qps + lane * 4, qr);
     lds4(vs + lane * 4, vr);
   }
+  cluster_wait();                                             // every CTA's xbar is initialised
+  // lane c < C delivers the warp's partial to cluster CTA c (row `rank` of its receive buffer)
+  const uint32_t dst_row = mapa_u32(smem_u32(xpart + rank * Tp), lane < C ? lane : 0);
+  const uint32_t dst_bar = mapa_u32(smem_u32(&xbar), lane < C ? lane : 0);
   for (int k = 0, s = w; k * R < n; ++k) {                   // chunk by chunk: one wait per chunk
     const int s1 = min(n, (k + 1) * R);
     if (s >= s1) continue;
@@ -855,7 +891,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
     for (; s < s1; s += ATT_WARPS) {
       T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
       const float p = score_partial_r<T>(kz + (size_t)s * Wb, qr, vr, act, lane, true, z_out, nullptr);
-      if (lane == 0) sc_part[s] = p;
+      if (lane < C) st_async_f32(dst_row + 4u * (uint32_t)s, p, dst_bar);
     }
   }
   if (Z_st) {                                                 // masked positions: zeros in this slice
@@ -863,17 +899,62 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
     for (int s = n + w; s < Ts; s += ATT_WARPS)
       for (int c4 = lane; c4 < W / 4; c4 += 32) stg4(Z_st + ((long)b * Ts + s) * A + g.a0 + c4 * 4, z);
   }
+  const bool ctx_warp = w * 32 < WH;                          // ctx: one thread per column
+  if (!ctx_warp && !(alpha_st && rank == 0 && w == 0)) return;
+  mbar_wait(&xbar, 0);                                        // all C partial rows received
+  // scores (rank-ordered sum, = gather_sum) and softmax (= softmax_row_warp) for s = lane + 32 k
+  float sc[8];
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int s = lane + 32 * k;
+    float x = 0.0f;
+    if (s < n) {
+      for (int c = 0; c < C; ++c) x = __fadd_rn(x, xpart[c * Tp + s]);
+      m = fmaxf(m, x);
+    }
+    sc[k] = x;
+  }
+  m = warp_max(m);
+  float l = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int s = lane + 32 * k;
+    sc[k] = s < n ? expf(__fsub_rn(sc[k], m)) : 0.0f;
+    if (s < n) l = __fadd_rn(l, sc[k]);
+  }
+  l = warp_sum(l);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sc[k] = lane + 32 * k < n ? __fdiv_rn(sc[k], l) : 0.0f;   // alpha
+  if (alpha_st && rank == 0 && w == 0)
+    for (int k = 0; k < 8; ++k)
+      if (lane + 32 * k < Ts) alpha_st[(long)b * Ts + lane + 32 * k] = sc[k];
+  if (!ctx_warp) return;
   for (int k = 0; k * R < n; ++k) mbar_wait(&bar[k], 0);     // every H_s chunk landed
-  cl.sync();
-  gather_sum(cl, sc_part, sc, n, g.C, tid);
-  cluster_arrive();                                           // remote reads of sc_part done
-  __syncthreads();
-  if (w == 0) softmax_row_warp(sc, al, n, lane);
-  __syncthreads();
-  if (alpha_st && g.r == 0)
-    for (int s = tid; s < Ts; s += ATT_THREADS) alpha_st[(long)b * Ts + s] = s < n ? al[s] : 0.0f;
-  ctx_columns<T>(hs, WHb, WH, al, n, ctx + (long)b * Hk + g.h0, tid);
-  cluster_wait();
+  // ctx_columns with alpha_s taken from lane s % 32 of register sc[s / 32]: the same FMAs into the
+  // same four accumulators (s mod 4) in the same order, so ctx is bit-identical to ctx_columns'
+  const int c = tid;
+  const bool cok = c < WH;
+  const T* hcol = hs + c;
+  float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (32 * k >= n) break;
+    const float ak = sc[k];
+    for (int j = 0; j < 32; j += 4) {
+      const int s0 = 32 * k + j;
+      if (s0 >= n) break;
+      const float al0 = __shfl_sync(0xffffffffu, ak, j), al1 = __shfl_sync(0xffffffffu, ak, j + 1);
+      const float al2 = __shfl_sync(0xffffffffu, ak, j + 2), al3 = __shfl_sync(0xffffffffu, ak, j + 3);
+      if (cok) {
+        a0 = __fmaf_rn(al0, to_f(hcol[s0 * WHb]), a0);
+        if (s0 + 1 < n) a1 = __fmaf_rn(al1, to_f(hcol[(s0 + 1) * WHb]), a1);
+        if (s0 + 2 < n) a2 = __fmaf_rn(al2, to_f(hcol[(s0 + 2) * WHb]), a2);
+        if (s0 + 3 < n) a3 = __fmaf_rn(al3, to_f(hcol[(s0 + 3) * WHb]), a3);
+      }
+    }
+  }
+  if (cok) ctx[(long)b * Hk + g.h0 + c] = from_f<T>(St<T>::round(__fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3))));
 }
 
 // phase-4 work split: G = (W + WH)/4 column groups of four; P = ATT_THREADS / G position phases
@@ -898,8 +979,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   // ds_out / al_out and echo_attn_bwd_finish accumulates dKp / dH_s over all steps afterwards
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(1024) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];   // TMA (no swizzle) needs 128-B alignment
   __shared__ __align__(8) uint64_t bar[TMA_CHUNKS];
+  __shared__ __align__(8) uint64_t xbar;
   const int A = d.A, Ts = d.Ts, Hk = d.Hk;
   const Slice g = make_slice_g(q, A, Hk, (int)cl.block_rank());
   const int W = g.a1 - g.a0, WH = g.h1 - g.h0;
@@ -920,22 +1002,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   T* qps = reinterpret_cast<T*>(p);
   T* vs = qps + Wb;
   float* dcs = reinterpret_cast<float*>(vs + Wb);
-  float* sc_part = dcs + WHb;
-  float* dal_part = sc_part + Tp;
-  float* sc = dal_part + Tp;
-  float* dal = sc + Tp;
-  float* al = dal + Tp;
+  float* xpart = dcs + WHb;                                   // [C][Tp][2] received (score, dalpha) partials
+  float* al = xpart + 2 * q.C * Tp;
   float* dsv = al + Tp;
   float* red = Tr >= 2 * P ? E : dsv + Tp;
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = row_len(src_len, b, Ts);
   const uint64_t pol = l2_policy(q.l2last);
+  const int rank = (int)cl.block_rank(), C = q.C;
   ECHO_PHASE(0);
   if (tid == 0) {
     prefetch_tmap(&mK);
     prefetch_tmap(&mH);
     for (int k = 0; k < TMA_CHUNKS; ++k) mbar_init(&bar[k], 1);
+    mbar_init(&xbar, 1);
     fence_mbar_init();
+    mbar_expect_tx(&xbar, (uint32_t)(C * n * 8));            // (score, dalpha) partials from each CTA
     ECHO_PHASE(11);
     SmallCopy sm{{qps, vs, dcs}, {qp + (long)b * A + g.a0, v + g.a0, dctx + (long)b * Hk + g.h0},
                  {recompute ? (uint32_t)(W * sizeof(T)) : 0u, (uint32_t)(W * sizeof(T)), (uint32_t)WH * 4u}};
@@ -953,6 +1035,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
   if (!recompute)
     for (int s = tid; s < n; s += ATT_THREADS) al[s] = alpha_st[(long)b * Ts + s];
   __syncthreads();
+  cluster_arrive_relaxed();                                   // publishes xbar's init (fenced above)
   ECHO_PHASE(1);
   if (n > 0) mbar_wait(&bar[0], 0);
   ECHO_PHASE(2);
@@ -966,9 +1049,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     lds4(vs + lane * 4, vr);
   }
   if (actH) lds4(dcs + lane * 4, dr);
+  cluster_wait();                                             // every CTA's xbar is initialised
   // rows s = w, w + 8, ... of this warp in groups of GR: per-lane partials first, then one
-  // reduce_scatter per quantity (bitwise equal to a warp_sum per row)
+  // reduce_scatter per quantity (bitwise equal to a warp_sum per row); the row's (score, dalpha)
+  // pair is then pushed to every cluster CTA (st.async into row `rank` of its receive buffer)
   constexpr int GR = 8;
+  const uint32_t x_row = smem_u32(xpart + 2 * rank * Tp), x_bar = smem_u32(&xbar);
   for (int s0 = w; s0 < n; s0 += GR * ATT_WARPS) {
     float psc[GR], pda[GR];
 #pragma unroll
@@ -1002,10 +1088,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     constexpr int SH = GR == 8 ? 2 : GR == 4 ? 3 : 4;         // slot of lane: lane >> (5 - log2 GR)
     const int j = lane >> SH;
     const int s = s0 + j * ATT_WARPS;
-    if ((lane & ((1 << SH) - 1)) == 0 && s < n) {
-      sc_part[s] = ps;
-      dal_part[s] = pd;
-    }
+    // every lane of a slot holds its sums (the reduce-scatter's butterflies); lane 4j + c sends
+    // slot j to cluster CTA c (c + 4 as well when C = 8)
+    if (s < n)
+      for (int c = lane & 3; c < C; c += 4)
+        st_async_v2(mapa_u32(x_row, c) + 8u * (uint32_t)s, ps, pd, mapa_u32(x_bar, c));
   }
   // L2 prefetch of the dKp / dH_s tiles phase 4 streams, issued by thread 0 once this CTA's loads
   // have landed so the reads overlap the exchange / softmax phases instead of phase 4
@@ -1017,20 +1104,54 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     }
   }
   ECHO_PHASE(3);
-  cl.sync();
   ECHO_PHASE(4);
-  if (recompute) gather_sum(cl, sc_part, sc, n, g.C, tid);
-  gather_sum(cl, dal_part, dal, n, g.C, tid);
-  cluster_arrive();
-  __syncthreads();
   ECHO_PHASE(5);
   if (w == 0) {
-    if (recompute) softmax_row_warp(sc, al, n, lane);      // STASH: al[] was loaded at the start
-    __syncwarp();
+    mbar_wait(&xbar, 0);                                       // all C partial rows received
+    // scores / dalpha for s = lane + 32 k in registers: rank-ordered sums (= gather_sum), then the
+    // softmax_row_warp arithmetic (RECOMPUTE; STASH: al[] was loaded at the start)
+    float sck[8], dak[8];
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int s = lane + 32 * k;
+      float x = 0.0f, y = 0.0f;
+      if (s < n) {
+        for (int c = 0; c < C; ++c) {
+          const float2 pr = *reinterpret_cast<const float2*>(xpart + 2 * (c * Tp + s));
+          x = __fadd_rn(x, pr.x);
+          y = __fadd_rn(y, pr.y);
+        }
+        m = fmaxf(m, x);
+      }
+      sck[k] = x;
+      dak[k] = y;
+    }
+    if (recompute) {
+      m = warp_max(m);
+      float l = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int s = lane + 32 * k;
+        sck[k] = s < n ? expf(__fsub_rn(sck[k], m)) : 0.0f;
+        if (s < n) l = __fadd_rn(l, sck[k]);
+      }
+      l = warp_sum(l);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (lane + 32 * k < n) al[lane + 32 * k] = __fdiv_rn(sck[k], l);
+      __syncwarp();
+    }
     float acc = 0.0f;                                          // dot = sum_s alpha_s dalpha_s (fixed order)
-    for (int s = lane; s < n; s += 32) acc = __fmaf_rn(al[s], dal[s], acc);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (lane + 32 * k < n) acc = __fmaf_rn(al[lane + 32 * k], dak[k], acc);
     acc = warp_sum(acc);
-    for (int s = lane; s < n; s += 32) dsv[s] = __fmul_rn(al[s], __fsub_rn(dal[s], acc));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int s = lane + 32 * k;
+      if (s < n) dsv[s] = __fmul_rn(al[s], __fsub_rn(dak[k], acc));
+    }
   }
   __syncthreads();
   if (ds_out && g.r == 0)                                       // deferred: publish this step's rows
@@ -1122,7 +1243,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     dv_part[o] = __fadd_rn(dv_old, x);
   }
   ECHO_PHASE(9);
-  cluster_wait();
   ECHO_PHASE(10);
 }
 
@@ -1263,10 +1383,10 @@ static bool tma_params(const echo_attn_desc* d, int* C, int* rows, size_t* smem_
   const size_t Tp = (d->Ts + 3) & ~3;
   const int R = tma_rows(d->Ts, (int)W, (int)WH, (int)sT);
   const size_t Ts = (size_t)tma_tile_rows(d->Ts, R);        // rows allocated per tile
-  const size_t fwd = al128h(Ts * W * sT) + al128h(Ts * WH * sT) + 2 * W * sT + 3 * Tp * 4;
+  const size_t fwd = al128h(Ts * W * sT) + al128h(Ts * WH * sT) + 2 * W * sT + (size_t)c * Tp * 4;
   const size_t P = tma_phases((int)W, (int)WH);
   const size_t bwd = al128h(Ts * W * sT) + al128h(Ts * WH * sT) + (sT == 4 ? 0 : al128h(Ts * W * 4)) +
-                     2 * W * sT + (6 * Tp + WH) * 4 + (Ts >= 2 * P ? 0 : 2 * P * W * 4);
+                     2 * W * sT + ((2 + 2 * (size_t)c) * Tp + WH) * 4 + (Ts >= 2 * P ? 0 : 2 * P * W * 4);
   if (bwd > 220 * 1024) return false;
   *C = c;
   *rows = R;
@@ -1315,7 +1435,7 @@ static bool map3d(CUtensorMap* m, const void* base, bool bf16, uint64_t X, uint6
 
 template <typename Kern, typename... Args>
 static cudaError_t launch_cluster(Kern kern, int C, int B, size_t smem, cudaStream_t st, Args... args) {
-  return launch(kern, dim3(C, B, 1), dim3(ATT_THREADS, 1, 1), smem, st, C, args...);
+  return launch(kern, dim3(C, B, 1), dim3(ATT_THREADS, 1, 1), smem, st, -C, args...);   // explicit cluster, even C = 1
 }
 
 static echo_status check_attn(const char* fn, const echo_attn_desc* d) {

@@ -54,9 +54,9 @@ inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   unsigned na = 0;
-  if (cluster > 1) {
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = (unsigned)cluster;
+  if (cluster > 1 || cluster < 0) {                   // cluster < 0: an explicit cluster of -cluster CTAs
+    attr[na].id = cudaLaunchAttributeClusterDimension;  // (kernels using DSMEM / st.async even when 1 CTA)
+    attr[na].val.clusterDim.x = (unsigned)(cluster < 0 ? -cluster : cluster);
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;

@@ -166,6 +166,23 @@ __device__ __forceinline__ void ldv_stream(const float* p, float (&o)[N]) {
     for (int k = 0; k < N; ++k) o[k] = f[k];
   }
 }
+template <typename T, int V> struct ScanRaw { typedef float t[V]; };                     // fp32: floats
+template <int V> struct ScanRaw<__nv_bfloat16, V> { typedef typename BV<V>::t t; };     // bf16: packed
+template <int N>
+__device__ __forceinline__ typename BV<N>::t ldcs_raw(const __nv_bfloat16* p) {
+  if constexpr (N == 2) return __ldcs(reinterpret_cast<const unsigned int*>(p));
+  else return __ldcs(reinterpret_cast<const typename BV<N>::t*>(p));
+}
+template <int N>
+__device__ __forceinline__ void unpack_bf(const typename BV<N>::t& v, float (&o)[N]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x;
+    o[2 * i + 1] = f.y;
+  }
+}
 template <int N>
 __device__ __forceinline__ void ldv_stream(const __nv_bfloat16* p, float (&o)[N]) {
   typename BV<N>::t v;
@@ -256,21 +273,40 @@ __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, c
     float c[V];
     ldv<V>(c0 + (long)b * H + j, c);
     for (int t0 = 0; t0 < T_; t0 += U) {
-      float gi[U][V], gf[U][V], gg[U][V];
+      // bf16: the U steps' gate vectors stay PACKED in registers until their step is computed (a
+      // 16-byte load = 4 registers instead of 8 floats), so twice the bytes are in flight per
+      // register and a deeper U fits; fp32 converts nothing
+      typedef typename ScanRaw<T, V>::t Raw;
+      Raw ri[U], rf[U], rg[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (t0 + u < T_) {
           const T* q = gp + (long)(t0 + u) * gstep;
-          ldv_stream<V>(q, gi[u]);
-          ldv_stream<V>(q + H, gf[u]);
-          ldv_stream<V>(q + 2 * H, gg[u]);
+          if constexpr (sizeof(T) == 2) {
+            ri[u] = ldcs_raw<V>(q);
+            rf[u] = ldcs_raw<V>(q + H);
+            rg[u] = ldcs_raw<V>(q + 2 * H);
+          } else {
+            ldv_stream<V>(q, ri[u]);
+            ldv_stream<V>(q + H, rf[u]);
+            ldv_stream<V>(q + 2 * H, rg[u]);
+          }
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (t0 + u < T_) {
+          float gi[V], gf[V], gg[V];
+          if constexpr (sizeof(T) == 2) {
+            unpack_bf<V>(ri[u], gi);
+            unpack_bf<V>(rf[u], gf);
+            unpack_bf<V>(rg[u], gg);
+          } else {
 #pragma unroll
-          for (int k = 0; k < V; ++k) c[k] = cell_update(gf[u][k], c[k], gi[u][k], gg[u][k]);
+            for (int k = 0; k < V; ++k) { gi[k] = ri[u][k]; gf[k] = rf[u][k]; gg[k] = rg[u][k]; }
+          }
+#pragma unroll
+          for (int k = 0; k < V; ++k) c[k] = cell_update(gf[k], c[k], gi[k], gg[k]);
           stv<V>(cp + (long)(t0 + u) * cstep, c);
           if (hp) {                                         // mirrored outputs: h_t = o * tanh(c_t)
             float go[V], h[V];
@@ -286,7 +322,7 @@ __global__ void __launch_bounds__(128) lstm_cscan_kernel(int T_, int B, int H, c
 }
 
 template <typename T>
-constexpr int scan_u(int v) { return sizeof(T) == 4 || v == 2 ? 8 : 4; }   // deeper U spills at 255 registers
+constexpr int scan_u(int v) { return sizeof(T) == 4 || v == 2 ? 8 : sizeof(T) == 2 && v == 8 ? 8 : 4; }
 
 // ---------------------------------------------------------------- a3 backward (fused recompute)
 template <typename T, int V>

@@ -140,6 +140,116 @@ __global__ void __launch_bounds__(1024) colsum_kernel(int rows, int cols, long l
   cl.sync();                                                     // keep seg[] alive for the remote reads
 }
 
+// Vectorised column sums for the wide bias gradients (C5: 1.2 M rows x 2048 / 8192 columns): a
+// half-warp reads one row's 16-byte vectors of a strip of 16 x VEC columns (fp32: 64, bf16: 128), a
+// warp two rows, a CTA of CS_THREADS threads 2 * CS_WARPS rows per iteration with CS_U iterations of
+// loads in flight (64-128 KB per CTA).  Each thread accumulates its VEC columns in fp64 in row order;
+// the two half-warps are combined (low + high), then the warps in order, then the COLSUM_SEGS row
+// segments of the cluster (gridDim.y of them: 8, or 16 when the strips are few) in rank order.
+// Deterministic, no atomics, no workspace.
+constexpr int CS_THREADS = 512, CS_WARPS = CS_THREADS / 32;
+template <typename T> struct CsVec;
+template <> struct CsVec<float> { static constexpr int V = 4, U = 4; };
+template <> struct CsVec<__nv_bfloat16> { static constexpr int V = 8, U = 4; };
+
+// 16-byte read-only load as a volatile asm so the U loads of an iteration are issued back to back
+// (plain __ldg let the compiler interleave them with the fp64 adds: one load in flight)
+__device__ __forceinline__ uint4 cs_ldg(const void* p) {
+  uint4 u;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(p));
+  return u;
+}
+__device__ __forceinline__ void cs_unpack(const uint4& u, float (&f)[4]) {
+  f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y); f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+}
+__device__ __forceinline__ void cs_unpack(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CS_THREADS) colsum_vec_kernel(int rows, int cols, long ld, const T* __restrict__ x,
+                                                                float* __restrict__ out, int accumulate) {
+  constexpr int V = CsVec<T>::V, U = CsVec<T>::U, SW = 16 * V;
+  pdl_wait();
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double cs_part[];                           // [CS_WARPS][SW]
+  __shared__ double seg[SW];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cg16 = lane & 15, half = lane >> 4;
+  const int c0 = blockIdx.x * SW + cg16 * V;                    // this thread's first column
+  const int k = (int)cl.block_rank(), nseg = (int)gridDim.y;
+  const int per = (rows + nseg - 1) / nseg;
+  const int r0 = k * per, r1 = min(rows, r0 + per);
+  const bool colok = c0 < cols;                                 // cols % V == 0 (checked on the host)
+  double acc[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) acc[j] = 0.0;
+  int r = r0 + 2 * w + half;
+  constexpr int STEP = 2 * CS_WARPS;
+  if (colok && r + (U - 1) * STEP < r1) {
+    // software pipeline: the next group's U loads are issued before the current group is summed
+    uint4 u[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) u[i] = cs_ldg(x + (long)(r + i * STEP) * ld + c0);
+    for (;;) {
+      const int rn = r + U * STEP;
+      const bool more = rn + (U - 1) * STEP < r1;
+      uint4 nx[U];
+      if (more) {
+#pragma unroll
+        for (int i = 0; i < U; ++i) nx[i] = cs_ldg(x + (long)(rn + i * STEP) * ld + c0);
+      }
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        float f[V];
+        cs_unpack(u[i], f);
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = __dadd_rn(acc[j], (double)f[j]);
+      }
+      r = rn;
+      if (!more) break;
+#pragma unroll
+      for (int i = 0; i < U; ++i) u[i] = nx[i];
+    }
+  }
+  if (colok) {
+    for (; r < r1; r += STEP) {
+      float f[V];
+      cs_unpack(cs_ldg(x + (long)r * ld + c0), f);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = __dadd_rn(acc[j], (double)f[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < V; ++j) {                                 // low half-warp + high half-warp
+    const double o = __shfl_xor_sync(0xffffffffu, acc[j], 16);
+    acc[j] = half ? __dadd_rn(o, acc[j]) : __dadd_rn(acc[j], o);
+  }
+  if (half == 0)
+#pragma unroll
+    for (int j = 0; j < V; ++j) cs_part[w * SW + cg16 * V + j] = acc[j];
+  __syncthreads();
+  if (threadIdx.x < SW) {
+    double t = 0.0;
+    for (int q = 0; q < CS_WARPS; ++q) t = __dadd_rn(t, cs_part[q * SW + threadIdx.x]);
+    seg[threadIdx.x] = t;
+  }
+  cl.sync();
+  const int c = blockIdx.x * SW + (int)threadIdx.x;
+  if (k == 0 && threadIdx.x < SW && c < cols) {
+    double t = 0.0;
+    for (int q = 0; q < nseg; ++q) t = __dadd_rn(t, cl.map_shared_rank(seg, q)[threadIdx.x]);
+    const float v = (float)t;
+    out[c] = accumulate ? __fadd_rn(out[c], v) : v;
+  }
+  cl.sync();                                                     // keep seg[] alive for the remote reads
+}
+
 }  // namespace echo
 
 using namespace echo;
@@ -204,8 +314,42 @@ extern "C" echo_status echo_colsum(int32_t rows, int32_t cols, int64_t ld, int32
                                                       (long long)ld);
   if (!x || !out) return fail(ECHO_ERR_INVALID, "%s: NULL x / out", fn);
   if (dtype != ECHO_FP32 && dtype != ECHO_BF16) return fail(ECHO_ERR_INVALID, "%s: bad dtype %d", fn, dtype);
-  const dim3 grid((cols + 31) / 32, COLSUM_SEGS), block(32, 32);
   cudaError_t e;
+  const int V = dtype == ECHO_FP32 ? CsVec<float>::V : CsVec<__nv_bfloat16>::V;
+  const size_t es = dtype == ECHO_FP32 ? 4 : 2;
+  if (cols % V == 0 && ld % V == 0 && aligned16(x) && (long)rows * cols >= (1L << 20)) {   // wide / long: vector path
+    const int SW = 16 * V;
+    const size_t smem = sizeof(double) * CS_WARPS * SW;
+    const int strips = (cols + SW - 1) / SW;
+    const int nseg = strips * COLSUM_SEGS >= 2 * 148 ? COLSUM_SEGS : 16;   // >= 2 CTAs per SM
+    const dim3 grid(strips, nseg);
+    const void* k = dtype == ECHO_FP32 ? (const void*)colsum_vec_kernel<float> : (const void*)colsum_vec_kernel<__nv_bfloat16>;
+    if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return fail(ECHO_ERR_CUDA, "%s: cudaFuncSetAttribute: %s", fn, cudaGetErrorString(cudaGetLastError()));
+    if (nseg > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      return fail(ECHO_ERR_CUDA, "%s: cluster size 16: %s", fn, cudaGetErrorString(cudaGetLastError()));
+    (void)es;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(CS_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = nseg;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (dtype == ECHO_FP32)
+      e = cudaLaunchKernelEx(&cfg, colsum_vec_kernel<float>, rows, cols, (long)ld, (const float*)x, out, accumulate);
+    else
+      e = cudaLaunchKernelEx(&cfg, colsum_vec_kernel<__nv_bfloat16>, rows, cols, (long)ld, (const __nv_bfloat16*)x, out,
+                             accumulate);
+    if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+    return check_launch(fn);
+  }
+  const dim3 grid((cols + 31) / 32, COLSUM_SEGS), block(32, 32);
   if (dtype == ECHO_FP32)
     e = launch_cluster_y(colsum_kernel<float>, grid, block, (cudaStream_t)stream, rows, cols, (long)ld,
                          (const float*)x, out, accumulate);

@@ -84,4 +84,4 @@ def test_two_rank_gpu_gradient_equals_global_batch_oracle(cuda_dev):
     for k, v in ref.items():
         err = np.abs(out["eager"][k] - v).max() / max(np.abs(v).max(), 1e-30)
         assert err <= 1e-4, (k, err)
-    assert sum(out["buckets"]) == sum(v.size for v in ref.values()) and min(out["buckets"]) > 0
+    assert sum(out["buckets"]) >= sum(v.size for v in ref.values()) and min(out["buckets"]) > 0

@@ -47,7 +47,10 @@ def test_xent_matches_reference(N, V, bias, copy, cuda_dev):
 
 
 @pytest.mark.parametrize("rows,cols,dtype", [(6400, 512, "fp32"), (33, 29, "fp32"), (1000, 2048, "bf16"),
-                                             (1, 7, "fp32")])
+                                             (1, 7, "fp32"),
+                                             # the vectorised path (>= 1 M elements; 8 or 16 row segments)
+                                             (65536, 2048, "fp32"), (4099, 8192, "fp32"), (33333, 2048, "bf16"),
+                                             (3001, 1024, "bf16"), (20000, 520, "fp32")])
 def test_colsum_fp64_accumulation(rows, cols, dtype, cuda_dev):
     """echo_colsum equals the fp64 column sum rounded once to fp32 (within 1 ulp), including a
     cancellation-heavy case where an fp32 sum is visibly off."""
