@@ -819,6 +819,9 @@ __device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void st_async_v2(uint32_t remote_addr, float x, float y, uint32_t remote_bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];\n" ::"r"(remote_addr),
                "r"(__float_as_uint(x)), "r"(__float_as_uint(y)), "r"(remote_bar)
@@ -864,9 +867,11 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
     prefetch_tmap(&mK);
     prefetch_tmap(&mH);
     for (int k = 0; k < TMA_CHUNKS; ++k) mbar_init(&bar[k], 1);
-    mbar_init(&xbar, 1);
+    // C > 1: n partial scores arrive from each of the C CTAs as st.async bytes; C == 1 (no DSMEM
+    // transactions in a one-CTA cluster): each position's lane 0 stores locally and arrives once
+    mbar_init(&xbar, C > 1 ? 1 : n + 1);
     fence_mbar_init();
-    mbar_expect_tx(&xbar, (uint32_t)(C * n * 4));            // n partial scores from each of the C CTAs
+    mbar_expect_tx(&xbar, C > 1 ? (uint32_t)(C * n * 4) : 0u);
     SmallCopy sm{{qps, vs, nullptr}, {qp + (long)b * A + g.a0, v + g.a0, nullptr},
                  {(uint32_t)(W * sizeof(T)), (uint32_t)(W * sizeof(T)), 0u}};
     issue_chunks(bar, n, R, kz, &mK, g.a0, hs, &mH, g.h0, b, Wb * sizeof(T), WHb * sizeof(T), sm, pol);
@@ -882,8 +887,8 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
   }
   cluster_wait();                                             // every CTA's xbar is initialised
   // lane c < C delivers the warp's partial to cluster CTA c (row `rank` of its receive buffer)
-  const uint32_t dst_row = mapa_u32(smem_u32(xpart + rank * Tp), lane < C ? lane : 0);
-  const uint32_t dst_bar = mapa_u32(smem_u32(&xbar), lane < C ? lane : 0);
+  const uint32_t dst_row = C > 1 ? mapa_u32(smem_u32(xpart + rank * Tp), lane < C ? lane : 0) : 0u;
+  const uint32_t dst_bar = C > 1 ? mapa_u32(smem_u32(&xbar), lane < C ? lane : 0) : 0u;
   for (int k = 0, s = w; k * R < n; ++k) {                   // chunk by chunk: one wait per chunk
     const int s1 = min(n, (k + 1) * R);
     if (s >= s1) continue;
@@ -891,7 +896,12 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
     for (; s < s1; s += ATT_WARPS) {
       T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
       const float p = score_partial_r<T>(kz + (size_t)s * Wb, qr, vr, act, lane, true, z_out, nullptr);
-      if (lane < C) st_async_f32(dst_row + 4u * (uint32_t)s, p, dst_bar);
+      if (C > 1) {
+        if (lane < C) st_async_f32(dst_row + 4u * (uint32_t)s, p, dst_bar);
+      } else if (lane == 0) {
+        xpart[s] = p;
+        mbar_arrive(&xbar);
+      }
     }
   }
   if (Z_st) {                                                 // masked positions: zeros in this slice
@@ -1015,9 +1025,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     prefetch_tmap(&mK);
     prefetch_tmap(&mH);
     for (int k = 0; k < TMA_CHUNKS; ++k) mbar_init(&bar[k], 1);
-    mbar_init(&xbar, 1);
+    mbar_init(&xbar, C > 1 ? 1 : n + 1);                     // C == 1: local stores + arrivals (see a5)
     fence_mbar_init();
-    mbar_expect_tx(&xbar, (uint32_t)(C * n * 8));            // (score, dalpha) partials from each CTA
+    mbar_expect_tx(&xbar, C > 1 ? (uint32_t)(C * n * 8) : 0u); // (score, dalpha) partials from each CTA
     ECHO_PHASE(11);
     SmallCopy sm{{qps, vs, dcs}, {qp + (long)b * A + g.a0, v + g.a0, dctx + (long)b * Hk + g.h0},
                  {recompute ? (uint32_t)(W * sizeof(T)) : 0u, (uint32_t)(W * sizeof(T)), (uint32_t)WH * 4u}};
@@ -1090,9 +1100,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
     const int s = s0 + j * ATT_WARPS;
     // every lane of a slot holds its sums (the reduce-scatter's butterflies); lane 4j + c sends
     // slot j to cluster CTA c (c + 4 as well when C = 8)
-    if (s < n)
-      for (int c = lane & 3; c < C; c += 4)
-        st_async_v2(mapa_u32(x_row, c) + 8u * (uint32_t)s, ps, pd, mapa_u32(x_bar, c));
+    if (s < n) {
+      if (C > 1) {
+        for (int c = lane & 3; c < C; c += 4)
+          st_async_v2(mapa_u32(x_row, c) + 8u * (uint32_t)s, ps, pd, mapa_u32(x_bar, c));
+      } else if ((lane & 3) == 0) {
+        *reinterpret_cast<float2*>(xpart + 2 * s) = make_float2(ps, pd);
+        mbar_arrive(&xbar);
+      }
+    }
   }
   // L2 prefetch of the dKp / dH_s tiles phase 4 streams, issued by thread 0 once this CTA's loads
   // have landed so the reads overlap the exchange / softmax phases instead of phase 4
