@@ -123,6 +123,22 @@ echo_status echo_lstm_seq_fwd(const echo_lstm_desc* d, int32_t T, int32_t k0, in
                               const void* gx, const void* Wh, const float* bias, const void* h0,
                               const float* c0, void* gates, float* c, int32_t c_ring, void* tc, void* h,
                               void* stream);
+/* a0 + a1 fused on the 5th-generation tensor cores (Echo-dagger fusion; SURVEY §8(f)
+ * row 3): one forward step with the recurrent contraction on tcgen05.mma (accumulator in TMEM, TMA-
+ * staged 128-byte-swizzled operands) and the a1 cell applied to the accumulator read back with
+ * tcgen05.ld:  G = round_bf16(gx_t + h_prev W_h^T) ; A = G + bias ; then exactly a1's gate / cell /
+ * hidden device functions.  Same outputs as echo_lstm_fwd after the caller's beta = 1 GEMM into gx_t,
+ * up to the GEMM's accumulation order; STASH and RECOMPUTE give identical gates / c / h.
+ *  gx_t    [B,4H] bf16  x_t W_x^T (no bias); may alias gates_t
+ *  h_prev  [B,H] bf16   dense;  Wh [4H,H] bf16 dense row-major (gate blocks i|f|g|o);  bias [4H] fp32
+ *  c_prev, c_out, gates_t, tc_t, h_out as echo_lstm_fwd
+ * Requirements (echo_lstm_fwd_tc_supported): bf16 storage, B <= 128, H a multiple of 64, H <= 512.
+ * Grid: H/16 CTAs of 128 threads, ~193 KB shared memory each.  Errors: ECHO_ERR_UNSUPPORTED, ECHO_ERR_INVALID. */
+echo_status echo_lstm_fwd_tc(const echo_lstm_desc* d, const void* gx_t, const void* h_prev, const void* Wh,
+                             const float* bias, const float* c_prev, void* gates_t, float* c_out, void* tc_t,
+                             void* h_out, void* stream);
+int32_t echo_lstm_fwd_tc_supported(int32_t B, int32_t H, int32_t dtype);
+
 /* ---- Mirror plan (the prior-work baseline, Chen et al.; Table 1, 749, 951;
  * estimator strategy "mirror", R25).  Mirror recomputes every cheap op of the cell,
  * so per step it keeps the INPUTS of the pre-activation adds -- the n_parts separate FC outputs

@@ -28,6 +28,7 @@ EXPORTED = NORTH_STAR + (
             "echo_dot_softmax_fwd",
             "echo_dot_softmax_bwd", "echo_xent_fwd_bwd", "echo_colsum", "echo_lstm_seq_fwd",
             "echo_lstm_seq_supported", "echo_gemm_f32", "echo_gemm_f32_supported",
+            "echo_lstm_fwd_tc", "echo_lstm_fwd_tc_supported",
             "echo_attn_bwd_deferred", "echo_attn_bwd_finish", "echo_attn_bwd_accumulate", "echo_tanh_bwd",
             "echo_lstm_fwd_parts", "echo_lstm_cscan_parts", "echo_lstm_bwd_parts",
             "echo_dropout_fwd", "echo_dropout_apply")
@@ -77,6 +78,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     sigs = {
         "echo_lstm_fwd": [ctypes.POINTER(LstmDesc)] + [vp] * 9,
         "echo_lstm_cscan": [ctypes.POINTER(LstmDesc), i32, vp, vp, vp, vp, vp],
+        "echo_lstm_fwd_tc": [ctypes.POINTER(LstmDesc)] + [vp] * 10,
+        "echo_lstm_fwd_tc_supported": [i32, i32, i32],
         "echo_lstm_bwd_recompute": [ctypes.POINTER(LstmDesc), i32, i32, ctypes.c_uint32] + [vp] * 11,
         "echo_attn_fwd": [ctypes.POINTER(AttnDesc)] + [vp] * 9,
         "echo_attn_bwd_recompute": [ctypes.POINTER(AttnDesc)] + [vp] * 16,
@@ -140,6 +143,16 @@ def echo_lstm_fwd(d, gx_t, gh_t, bias, c_prev, gates_t, c_out, tc_t, h_out, stre
     LAUNCHES["count"] += 1
     _check(load().echo_lstm_fwd(ctypes.byref(d), _p(gx_t), _p(gh_t), _p(bias), _p(c_prev), _p(gates_t), _p(c_out),
                                 _p(tc_t), _p(h_out), _stream(stream)))
+
+
+def echo_lstm_fwd_tc(d, gx_t, h_prev, Wh, bias, c_prev, gates_t, c_out, tc_t, h_out, stream=None):
+    LAUNCHES["count"] += 1
+    _check(load().echo_lstm_fwd_tc(ctypes.byref(d), _p(gx_t), _p(h_prev), _p(Wh), _p(bias), _p(c_prev), _p(gates_t),
+                                   _p(c_out), _p(tc_t), _p(h_out), _stream(stream)))
+
+
+def echo_lstm_fwd_tc_supported(B, H, dtype) -> bool:
+    return bool(load().echo_lstm_fwd_tc_supported(int(B), int(H), int(dtype)))
 
 
 def echo_lstm_cscan(d, T, gates, c0, c_ws, h_ws=None, stream=None):

@@ -12,6 +12,7 @@
 #include "echo_common.cuh"
 
 #include <cooperative_groups.h>
+#include <cuda.h>
 #include <type_traits>
 
 namespace echo {
@@ -693,6 +694,188 @@ static bool seq_plan(int B, int H, int dtype, SeqGeom* out, const void** kern) {
   return false;
 }
 
+
+// ================================================================ a0 + a1 fused on the tensor cores
+// One LSTM forward step with the recurrent contraction h_{t-1} W_h^T on the 5th-generation tensor
+// cores (tcgen05.mma, accumulator in TMEM) and the a1 cell epilogue applied to the accumulator
+// straight out of TMEM (Echo-dagger fusion):
+//   G = round_bf16(gx_t + h_{t-1} W_h^T)   (the per-step path's cuBLAS beta = 1 output)
+//   A = G + b ;  i,f,g,o = gates_of(A) ;  c_t = cell_update ;  h_t = hidden(o, tanh_c(c_t))
+// with the SAME device functions and rounding points as a1, so it differs from the per-step path
+// only in the GEMM's accumulation order (and STASH / RECOMPUTE give identical results).
+// CTA j owns hidden units [16 j, 16 j + 16): the 64 gate rows {g H + 16 j + u} of W_h form the MMA's
+// B operand (N = 64), the whole h_{t-1} (B <= 128 rows, zero-padded by TMA) the A operand (M = 128),
+// K = H in 64-element atoms (128-byte rows, 128-byte swizzle).  Thread 0 issues every TMA load (one
+// mbarrier per K atom, all resident: H <= 512 -> 192 KB) and then the 4 x H/64 MMAs as the atoms
+// land; tcgen05.commit signals the epilogue; thread b (= TMEM lane b) reads its row's 64 fp32
+// accumulators with tcgen05.ld and finishes the cell for its 16 units.
+constexpr int TC_U = 16, TC_N = 4 * TC_U, TC_M = 128, TC_KA = 64;
+constexpr int TC_A_ATOM = TC_M * TC_KA * 2, TC_B_ATOM = TC_N * TC_KA * 2;   // 16 KB, 8 KB
+
+__device__ __forceinline__ uint32_t tc_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tc_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(tc_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc_smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(tc_smem_u32(bar)), "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tc_tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          tc_smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(tc_smem_u32(bar))
+      : "memory");
+}
+// K-major operand tile in the canonical 128-byte-swizzle layout: rows of 64 bf16 (128 B), 8-row
+// groups 1024 B apart (SBO), LBO unused (1), descriptor version 1 (sm_100), layout SWIZZLE_128B (2)
+__device__ __forceinline__ uint64_t tc_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);            // start address
+  d |= (uint64_t)1 << 16;                            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                  // SBO
+  d |= (uint64_t)1 << 46;                            // version
+  d |= (uint64_t)2 << 61;                            // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: kind::f16, A = B = BF16, D = F32, both K-major, M = 128, N = TC_N
+__host__ __device__ constexpr uint32_t tc_idesc() {
+  return (1u << 4)                 // D format F32
+         | (1u << 7)               // A format BF16
+         | (1u << 10)              // B format BF16
+         | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(tc_idesc()), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int MODE_STASH>
+__global__ void __launch_bounds__(128, 1) lstm_fwd_tc_kernel(const __grid_constant__ CUtensorMap mH,
+                                                            const __grid_constant__ CUtensorMap mW, int B, int H,
+                                                            const __nv_bfloat16* gx, const float* __restrict__ bias,
+                                                            const float* __restrict__ c_prev, __nv_bfloat16* gates,
+                                                            float* __restrict__ c_out, __nv_bfloat16* __restrict__ tc_out,
+                                                            __nv_bfloat16* __restrict__ h_out) {
+  typedef __nv_bfloat16 T;
+  pdl_wait();
+  extern __shared__ __align__(1024) unsigned char tc_sm[];
+  __shared__ __align__(8) uint64_t full[8];
+  __shared__ __align__(8) uint64_t done;
+  __shared__ uint32_t tmem_holder;
+  const int nk = H / TC_KA;
+  const int tid = threadIdx.x, w = tid >> 5;
+  const int j0 = blockIdx.x * TC_U;
+  unsigned char* sA = tc_sm;                                   // nk atoms of [128 rows][128 B]
+  unsigned char* sB = tc_sm + (size_t)nk * TC_A_ATOM;          // nk atoms of [64 rows][128 B]
+  if (w == 0) {                                                // TMEM: 64 fp32 columns x 128 lanes
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc_smem_u32(&tmem_holder)),
+                 "n"(TC_N)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (tid == 32) {
+    for (int k = 0; k < nk; ++k) tc_mbar_init(&full[k], 1);
+    tc_mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tmem_holder;
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mH) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mW) : "memory");
+    for (int k = 0; k < nk; ++k) {                             // every K atom in flight at once
+      tc_mbar_expect_tx(&full[k], TC_A_ATOM + TC_B_ATOM);
+      tc_tma_2d(sA + (size_t)k * TC_A_ATOM, &mH, k * TC_KA, 0, &full[k]);
+#pragma unroll
+      for (int g = 0; g < 4; ++g)                              // gate g's 16 rows of W_h
+        tc_tma_2d(sB + (size_t)k * TC_B_ATOM + g * (TC_U * 128), &mW, k * TC_KA, g * H + j0, &full[k]);
+    }
+    for (int k = 0; k < nk; ++k) {                             // MMAs in K order as the atoms land
+      tc_mbar_wait(&full[k], 0);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t a0 = tc_smem_u32(sA + (size_t)k * TC_A_ATOM), b0 = tc_smem_u32(sB + (size_t)k * TC_B_ATOM);
+#pragma unroll
+      for (int kk = 0; kk < TC_KA / 16; ++kk)                   // K = 16 per MMA: +32 B inside the swizzle atom
+        tc_mma(tmem, tc_desc_sw128(a0 + 32 * kk), tc_desc_sw128(b0 + 32 * kk), (k | kk) != 0);
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tc_smem_u32(&done))
+                 : "memory");
+  }
+  __syncwarp();
+  tc_mbar_wait(&done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // epilogue: thread = TMEM lane = row b; accumulator column g * 16 + u = gate g of unit j0 + u
+  float acc[4][16];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) tc_ld16(tmem + ((uint32_t)(32 * w) << 16) + (uint32_t)(g * 16), acc[g]);
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  const int b = tid;
+  if (b < B) {
+    const long row4 = (long)b * 4 * H;
+    float a[4][16];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      float x[16], bb[16];
+      ldv<8>(gx + row4 + g * H + j0, *reinterpret_cast<float(*)[8]>(&x[0]));
+      ldv<8>(gx + row4 + g * H + j0 + 8, *reinterpret_cast<float(*)[8]>(&x[8]));
+      ldv<8>(bias + g * H + j0, *reinterpret_cast<float(*)[8]>(&bb[0]));
+      ldv<8>(bias + g * H + j0 + 8, *reinterpret_cast<float(*)[8]>(&bb[8]));
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        a[g][u] = __fadd_rn(St<T>::round(__fadd_rn(x[u], acc[g][u])), bb[u]);   // G = round(gx + gh); A = G + b
+    }
+    float cp[16];
+    ldv<8>(c_prev + (long)b * H + j0, *reinterpret_cast<float(*)[8]>(&cp[0]));
+    ldv<8>(c_prev + (long)b * H + j0 + 8, *reinterpret_cast<float(*)[8]>(&cp[8]));
+    float gi[16], gf[16], gg[16], go[16], c[16], tc[16], h[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      gates_of<T>(a[0][u], a[1][u], a[2][u], a[3][u], gi[u], gf[u], gg[u], go[u]);
+      c[u] = cell_update(gf[u], cp[u], gi[u], gg[u]);
+      tc[u] = tanh_c<T>(c[u]);
+      h[u] = hidden<T>(go[u], tc[u]);
+    }
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const int o = 8 * hlf;
+      stv<8>(gates + row4 + 0 * H + j0 + o, *reinterpret_cast<float(*)[8]>(&gi[o]));
+      stv<8>(gates + row4 + 1 * H + j0 + o, *reinterpret_cast<float(*)[8]>(&gf[o]));
+      stv<8>(gates + row4 + 2 * H + j0 + o, *reinterpret_cast<float(*)[8]>(&gg[o]));
+      stv<8>(gates + row4 + 3 * H + j0 + o, *reinterpret_cast<float(*)[8]>(&go[o]));
+      stv<8>(c_out + (long)b * H + j0 + o, *reinterpret_cast<float(*)[8]>(&c[o]));
+      if (MODE_STASH) stv<8>(tc_out + (long)b * H + j0 + o, *reinterpret_cast<float(*)[8]>(&tc[o]));
+      stv<8>(h_out + (long)b * H + j0 + o, *reinterpret_cast<float(*)[8]>(&h[o]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TC_N) : "memory");
+}
+
 // ---------------------------------------------------------------- validation
 static echo_status check_desc(const echo_lstm_desc* d) {
   if (!d) return fail(ECHO_ERR_INVALID, "lstm: desc is NULL");
@@ -1014,4 +1197,79 @@ extern "C" echo_status echo_lstm_bwd_parts(const echo_lstm_desc* d, int32_t n_pa
   ECHO_REQ(dA_t, "dA_t");
   ECHO_PARTS_LAUNCH(lstm_bwd_parts_kernel, d->B, d->H, (const TT*)parts_t, (long)part_stride, bias, c_prev, c_t,
                     dh_t, dc, (TT*)dA_t);
+}
+
+// ---- host side of the tcgen05 step (a0 + a1 fused)
+namespace echo {
+typedef CUresult (*TcEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                               const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TcEncodeFn tc_encode() {
+  static TcEncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (TcEncodeFn)p;
+  }
+  return fn;
+}
+// 2-D bf16 map over a dense [rows][cols] tensor, box {64 cols, box_rows}, 128-byte swizzle
+static bool tc_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  TcEncodeFn fn = tc_encode();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)TC_KA, box_rows};
+  cuuint32_t el[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, el,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static size_t tc_smem(int H) { return (size_t)(H / TC_KA) * (TC_A_ATOM + TC_B_ATOM) + 1024; }
+}  // namespace echo
+
+extern "C" int32_t echo_lstm_fwd_tc_supported(int32_t B, int32_t H, int32_t dtype) {
+  return dtype == ECHO_BF16 && B >= 1 && B <= TC_M && H >= TC_KA && H % TC_KA == 0 && H / TC_KA <= 8 ? 1 : 0;
+}
+
+extern "C" echo_status echo_lstm_fwd_tc(const echo_lstm_desc* d, const void* gx_t, const void* h_prev, const void* Wh,
+                                        const float* bias, const float* c_prev, void* gates_t, float* c_out,
+                                        void* tc_t, void* h_out, void* stream) {
+  const char* fn = "echo_lstm_fwd_tc";
+  echo_status s = check_desc(d);
+  if (s) return s;
+  if (!echo_lstm_fwd_tc_supported(d->B, d->H, d->dtype))
+    return fail(ECHO_ERR_UNSUPPORTED, "%s: needs bf16 storage, B <= %d, H a multiple of %d up to %d (B=%d H=%d)", fn,
+                TC_M, TC_KA, 8 * TC_KA, d->B, d->H);
+  ECHO_REQ(gx_t, "gx_t");
+  ECHO_REQ(h_prev, "h_prev");
+  ECHO_REQ(Wh, "Wh");
+  ECHO_REQ(bias, "bias");
+  ECHO_REQ(c_prev, "c_prev");
+  ECHO_REQ(gates_t, "gates_t");
+  ECHO_REQ(c_out, "c_out");
+  ECHO_REQ(h_out, "h_out");
+  if (d->mode == ECHO_STASH) { ECHO_REQ(tc_t, "tc_t"); }
+  else if (tc_t) return fail(ECHO_ERR_INVALID, "%s: tc_t must be NULL in RECOMPUTE mode", fn);
+  if (c_out == c_prev) return fail(ECHO_ERR_INVALID, "%s: c_out must not alias c_prev", fn);
+  CUtensorMap mH, mW;
+  if (!tc_map(&mH, h_prev, d->H, d->B, TC_M) || !tc_map(&mW, Wh, d->H, 4 * d->H, TC_U))
+    return fail(ECHO_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed", fn);
+  const size_t smem = tc_smem(d->H);
+  typedef __nv_bfloat16 bf;
+  const void* k = d->mode == ECHO_STASH ? (const void*)lstm_fwd_tc_kernel<1> : (const void*)lstm_fwd_tc_kernel<0>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: cudaFuncSetAttribute: %s", fn, cudaGetErrorString(e));
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 grid(d->H / TC_U);
+  if (d->mode == ECHO_STASH)
+    e = launch(lstm_fwd_tc_kernel<1>, grid, dim3(128), smem, st, 1, mH, mW, d->B, d->H, (const bf*)gx_t, bias, c_prev,
+               (bf*)gates_t, c_out, (bf*)tc_t, (bf*)h_out);
+  else
+    e = launch(lstm_fwd_tc_kernel<0>, grid, dim3(128), smem, st, 1, mH, mW, d->B, d->H, (const bf*)gx_t, bias, c_prev,
+               (bf*)gates_t, c_out, (bf*)nullptr, (bf*)h_out);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
 }
