@@ -133,7 +133,7 @@ echo_status echo_lstm_seq_fwd(const echo_lstm_desc* d, int32_t T, int32_t k0, in
  *  h_prev  [B,H] bf16   dense;  Wh [4H,H] bf16 dense row-major (gate blocks i|f|g|o);  bias [4H] fp32
  *  c_prev, c_out, gates_t, tc_t, h_out as echo_lstm_fwd
  * Requirements (echo_lstm_fwd_tc_supported): bf16 storage, B <= 128, H a multiple of 64, H <= 512.
- * Grid: H/16 CTAs of 128 threads, ~193 KB shared memory each.  Errors: ECHO_ERR_UNSUPPORTED, ECHO_ERR_INVALID. */
+ * Grid: H/16 CTAs of 512 threads, ~193 KB shared memory each.  Errors: ECHO_ERR_UNSUPPORTED, ECHO_ERR_INVALID. */
 echo_status echo_lstm_fwd_tc(const echo_lstm_desc* d, const void* gx_t, const void* h_prev, const void* Wh,
                              const float* bias, const float* c_prev, void* gates_t, float* c_out, void* tc_t,
                              void* h_out, void* stream);

@@ -707,8 +707,9 @@ static bool seq_plan(int B, int H, int dtype, SeqGeom* out, const void** kern) {
 // B operand (N = 64), the whole h_{t-1} (B <= 128 rows, zero-padded by TMA) the A operand (M = 128),
 // K = H in 64-element atoms (128-byte rows, 128-byte swizzle).  Thread 0 issues every TMA load (one
 // mbarrier per K atom, all resident: H <= 512 -> 192 KB) and then the 4 x H/64 MMAs as the atoms
-// land; tcgen05.commit signals the epilogue; thread b (= TMEM lane b) reads its row's 64 fp32
-// accumulators with tcgen05.ld and finishes the cell for its 16 units.
+// land; tcgen05.commit signals the epilogue.  The epilogue spreads over 16 warps: warp w reads TMEM
+// lanes 32 (w % 4) .. + 31 (rows b) and the accumulator columns of units 4 (w / 4) .. + 3 (four
+// tcgen05.ld of 4 columns, one per gate), and each thread finishes the cell for its row and 4 units.
 constexpr int TC_U = 16, TC_N = 4 * TC_U, TC_M = 128, TC_KA = 64;
 constexpr int TC_A_ATOM = TC_M * TC_KA * 2, TC_B_ATOM = TC_N * TC_KA * 2;   // 16 KB, 8 KB
 
@@ -758,6 +759,14 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db
       "l"(da), "l"(db), "r"(tc_idesc()), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void tc_ld4(uint32_t taddr, float (&v)[4]) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -770,8 +779,9 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+constexpr int TC_THREADS = 512;
 template <int MODE_STASH>
-__global__ void __launch_bounds__(128, 1) lstm_fwd_tc_kernel(const __grid_constant__ CUtensorMap mH,
+__global__ void __launch_bounds__(TC_THREADS, 1) lstm_fwd_tc_kernel(const __grid_constant__ CUtensorMap mH,
                                                             const __grid_constant__ CUtensorMap mW, int B, int H,
                                                             const __nv_bfloat16* gx, const float* __restrict__ bias,
                                                             const float* __restrict__ c_prev, __nv_bfloat16* gates,
@@ -827,48 +837,44 @@ __global__ void __launch_bounds__(128, 1) lstm_fwd_tc_kernel(const __grid_consta
   __syncwarp();
   tc_mbar_wait(&done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  // epilogue: thread = TMEM lane = row b; accumulator column g * 16 + u = gate g of unit j0 + u
-  float acc[4][16];
+  // epilogue: warp w -> TMEM lanes (rows) 32 (w % 4) + lane, units j0 + 4 (w / 4) + 0..3; the
+  // accumulator column of gate g, unit u is g * 16 + u
+  const int lg = w & 3, ug = w >> 2;
+  float acc[4][4];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) tc_ld16(tmem + ((uint32_t)(32 * w) << 16) + (uint32_t)(g * 16), acc[g]);
+  for (int g = 0; g < 4; ++g) tc_ld4(tmem + ((uint32_t)(32 * lg) << 16) + (uint32_t)(g * TC_U + 4 * ug), acc[g]);
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-  const int b = tid;
+  const int b = 32 * lg + (tid & 31);
+  const int j = j0 + 4 * ug;
   if (b < B) {
     const long row4 = (long)b * 4 * H;
-    float a[4][16];
+    float a[4][4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-      float x[16], bb[16];
-      ldv<8>(gx + row4 + g * H + j0, *reinterpret_cast<float(*)[8]>(&x[0]));
-      ldv<8>(gx + row4 + g * H + j0 + 8, *reinterpret_cast<float(*)[8]>(&x[8]));
-      ldv<8>(bias + g * H + j0, *reinterpret_cast<float(*)[8]>(&bb[0]));
-      ldv<8>(bias + g * H + j0 + 8, *reinterpret_cast<float(*)[8]>(&bb[8]));
+      float x[4], bb[4];
+      ldv<4>(gx + row4 + g * H + j, x);
+      ldv<4>(bias + g * H + j, bb);
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
+      for (int u = 0; u < 4; ++u)
         a[g][u] = __fadd_rn(St<T>::round(__fadd_rn(x[u], acc[g][u])), bb[u]);   // G = round(gx + gh); A = G + b
     }
-    float cp[16];
-    ldv<8>(c_prev + (long)b * H + j0, *reinterpret_cast<float(*)[8]>(&cp[0]));
-    ldv<8>(c_prev + (long)b * H + j0 + 8, *reinterpret_cast<float(*)[8]>(&cp[8]));
-    float gi[16], gf[16], gg[16], go[16], c[16], tc[16], h[16];
+    float cp[4];
+    ldv<4>(c_prev + (long)b * H + j, cp);
+    float gi[4], gf[4], gg[4], go[4], c[4], tc[4], h[4];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
+    for (int u = 0; u < 4; ++u) {
       gates_of<T>(a[0][u], a[1][u], a[2][u], a[3][u], gi[u], gf[u], gg[u], go[u]);
       c[u] = cell_update(gf[u], cp[u], gi[u], gg[u]);
       tc[u] = tanh_c<T>(c[u]);
       h[u] = hidden<T>(go[u], tc[u]);
     }
-#pragma unroll
-    for (int hlf = 0; hlf < 2; ++hlf) {
-      const int o = 8 * hlf;
-      stv<8>(gates + row4 + 0 * H + j0 + o, *reinterpret_cast<float(*)[8]>(&gi[o]));
-      stv<8>(gates + row4 + 1 * H + j0 + o, *reinterpret_cast<float(*)[8]>(&gf[o]));
-      stv<8>(gates + row4 + 2 * H + j0 + o, *reinterpret_cast<float(*)[8]>(&gg[o]));
-      stv<8>(gates + row4 + 3 * H + j0 + o, *reinterpret_cast<float(*)[8]>(&go[o]));
-      stv<8>(c_out + (long)b * H + j0 + o, *reinterpret_cast<float(*)[8]>(&c[o]));
-      if (MODE_STASH) stv<8>(tc_out + (long)b * H + j0 + o, *reinterpret_cast<float(*)[8]>(&tc[o]));
-      stv<8>(h_out + (long)b * H + j0 + o, *reinterpret_cast<float(*)[8]>(&h[o]));
-    }
+    stv<4>(gates + row4 + 0 * H + j, gi);
+    stv<4>(gates + row4 + 1 * H + j, gf);
+    stv<4>(gates + row4 + 2 * H + j, gg);
+    stv<4>(gates + row4 + 3 * H + j, go);
+    stv<4>(c_out + (long)b * H + j, c);
+    if (MODE_STASH) stv<4>(tc_out + (long)b * H + j, tc);
+    stv<4>(h_out + (long)b * H + j, h);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -1265,10 +1271,10 @@ extern "C" echo_status echo_lstm_fwd_tc(const echo_lstm_desc* d, const void* gx_
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid(d->H / TC_U);
   if (d->mode == ECHO_STASH)
-    e = launch(lstm_fwd_tc_kernel<1>, grid, dim3(128), smem, st, 1, mH, mW, d->B, d->H, (const bf*)gx_t, bias, c_prev,
+    e = launch(lstm_fwd_tc_kernel<1>, grid, dim3(TC_THREADS), smem, st, 1, mH, mW, d->B, d->H, (const bf*)gx_t, bias, c_prev,
                (bf*)gates_t, c_out, (bf*)tc_t, (bf*)h_out);
   else
-    e = launch(lstm_fwd_tc_kernel<0>, grid, dim3(128), smem, st, 1, mH, mW, d->B, d->H, (const bf*)gx_t, bias, c_prev,
+    e = launch(lstm_fwd_tc_kernel<0>, grid, dim3(TC_THREADS), smem, st, 1, mH, mW, d->B, d->H, (const bf*)gx_t, bias, c_prev,
                (bf*)gates_t, c_out, (bf*)nullptr, (bf*)h_out);
   if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);

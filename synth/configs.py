@@ -25,6 +25,11 @@ class NMTConfig:
     enc_layers: int
     dec_layers: int
     dropout: float = 0.0  # embedding dropout rate (reading R31; 0 = none, the C1/C2 configs)
+    dropout_hidden: float = 0.0  # inter-layer LSTM output and attention-hidden dropout (reading R33)
+
+    def hidden_drop_sites(self) -> int:
+        """Philox sites of reading R33: encoder l -> l+1, decoder l -> l+1, attention hidden -> output."""
+        return (self.enc_layers - 1) + (self.dec_layers - 1) + 1 if self.dropout_hidden > 0 else 0
 
     @property
     def Hk(self) -> int:  # key / value width = encoder hidden

@@ -155,6 +155,9 @@ def nmt_batch(seed, cfg: NMTConfig, lengths="full"):
         src_len[0] = cfg.Ts
     # Philox keys of the two embedding-dropout sites (source, target), drawn per batch (R31)
     seeds = g.integers(1, 2 ** 62, size=2).astype(np.uint64)
+    nh = cfg.hidden_drop_sites()
+    if nh:                                                   # reading R33: one key per hidden site, after
+        seeds = np.concatenate([seeds, g.integers(1, 2 ** 62, size=nh).astype(np.uint64)])   # the two above
     return {"src": src, "tgt_in": tgt[:, :-1].copy(), "tgt_out": tgt[:, 1:].copy(), "src_len": src_len,
             "drop_seeds": seeds}
 

@@ -190,6 +190,11 @@ def nmt(cfg, s="f32"):
     def drop(x):                                         # R31: embedding dropout (keep-mask = output 1)
         return g.op("dropout", [x], tag="embed", nout=2, p=p)[0] if p > 0 else x
 
+    ph = getattr(cfg, "dropout_hidden", 0.0)
+
+    def hdrop(x, tag):                                   # R33: inter-layer / output dropout
+        return g.op("dropout", [x], tag=tag, nout=2, p=ph)[0] if ph > 0 else x
+
     # encoder
     xs = [drop(g.op("embedding", [g.op("slice", [src], tag="embed", axis=0, begin=t, end=t + 1, squeeze=1), emb_s],
                     tag="embed")) for t in range(Ts)]
@@ -201,7 +206,7 @@ def nmt(cfg, s="f32"):
             gx = g.op("fully_connected", [xs[t], Wx, b], tag="rnn")
             h, c = lstm_cell(g, gx, h, c, Wh, H, B, s, tag="rnn")
             hs.append(h)
-        xs = hs
+        xs = [hdrop(h, "rnn") for h in hs] if l < cfg.enc_layers - 1 else hs
     Hs = g.op("stack", xs, tag="rnn")                                          # [Ts, B, H]
     Kp = g.op("fully_connected", [Hs, Wk, bq], tag="attention")               # [Ts, B, A]
     # decoder
@@ -224,7 +229,7 @@ def nmt(cfg, s="f32"):
                 extra = None
             h, c = lstm_cell(g, gx, hst[l], cst[l], Wh, H, B, s, tag="rnn", gh=(t > 0), extra=extra)
             hst[l], cst[l] = h, c
-            x = h
+            x = hdrop(h, "rnn") if l < cfg.dec_layers - 1 else h
         q = x
         qp = g.op("fully_connected", [q, Wq], tag="attention")                 # [B, A]
         z = g.op("broadcast_add", [qp, Kp], tag="attention")                  # [Ts, B, A]
@@ -238,7 +243,7 @@ def nmt(cfg, s="f32"):
         a_all.append(a_t)
         a_prev = a_t
     Aall = g.op("stack", a_all, tag="output")                                  # [Td, B, H]
-    logits = g.op("fully_connected", [Aall, Wo, bo], tag="output", dtype="f32")   # [Td, B, V]
+    logits = g.op("fully_connected", [hdrop(Aall, "output"), Wo, bo], tag="output", dtype="f32")   # [Td, B, V]
     loss, probs = g.op("softmax_ce_loss", [logits, labels], tag="output", nout=2)
     g.output(loss)
     return g.doc()

@@ -225,3 +225,24 @@ def test_nmt_embedding_dropout_graph(est):
     b0 = est(Gr.nmt(SMALL_NMT), {"strategy": "baseline"})["stash_bytes"]
     b1 = est(doc, {"strategy": "baseline"})["stash_bytes"]
     assert b1 - b0 == n                      # + byte masks; the dropped embeddings replace the embeddings
+
+
+def test_nmt_hidden_dropout_graph_reading_r33(est):
+    """R33 graph (dropout on the inter-layer LSTM inputs and where a_t enters the output layer):
+    C++ == oracle for every plan, with and without regenerated masks.  Echo keeps exactly one bit per
+    dropped element more than without the sites (the dropped tensors are mirrored), regenerated masks
+    nothing more; the Baseline keeps each site's dropout output and byte mask, and the last-step h of
+    each dropped layer is no longer a feature map (the layer above reads the dropout's output)."""
+    from dataclasses import replace
+    cfg = replace(SMALL_NMT, dropout_hidden=0.3)
+    doc = Gr.nmt(cfg)
+    _compare(est, doc)
+    _compare(est, doc, ("mirror", "echo"), {"regenerate_masks": True})
+    B, Ts, Td, H = cfg.B, cfg.Ts, cfg.Td, cfg.H
+    sites = [Ts * B * H] * (cfg.enc_layers - 1) + [Td * B * H] * (cfg.dec_layers - 1) + [Td * B * H]
+    plain = {s: est(Gr.nmt(SMALL_NMT), {"strategy": s})["stash_bytes"] for s in ("baseline", "echo")}
+    assert est(doc, {"strategy": "echo"})["stash_bytes"] - plain["echo"] == sum(n // 8 for n in sites)
+    assert est(doc, {"strategy": "echo", "regenerate_masks": True})["stash_bytes"] == plain["echo"]
+    dropped_layers = (cfg.enc_layers - 1) + (cfg.dec_layers - 1)
+    assert est(doc, {"strategy": "baseline"})["stash_bytes"] - plain["baseline"] == \
+        sum(n * (4 + 1) for n in sites) - dropped_layers * B * H * 4

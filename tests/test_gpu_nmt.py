@@ -302,3 +302,56 @@ def test_graph_refuses_new_dropout_seeds(cuda_dev):
     b2 = dict(b, drop_seeds=np.asarray(b["drop_seeds"]) + 1)
     with pytest.raises(ValueError):
         m.upload_batch(b2)
+
+
+RAGGED_HDROP = NMTConfig("ragged-hdrop", B=5, Ts=11, Td=7, E=24, H=40, A=32, V=50, enc_layers=2, dec_layers=2,
+                         dropout=0.1, dropout_hidden=0.3)
+C2_HDROP = NMTConfig("C2-hdrop", B=128, Ts=50, Td=50, E=512, H=512, A=512, V=8192, enc_layers=2, dec_layers=2,
+                     dropout=0.1, dropout_hidden=0.3)
+FRO_ONLY[("ragged-hdrop", "bf16")] = _QUERY_PATH
+
+
+@pytest.mark.parametrize("cfg,storage", [(RAGGED_HDROP, "fp32"), (RAGGED_HDROP, "bf16"), (C2_HDROP, "bf16")],
+                         ids=lambda x: getattr(x, "name", x))
+def test_nmt_hidden_dropout_plans(cfg, storage, cuda_dev):
+    """Reading R33: 1-bit / regenerated dropout masks on the inter-layer LSTM inputs
+    (encoder and decoder) and on a_t where it enters the output layer, plus the embedding sites.  Every
+    plan (STASH: dropout outputs + byte masks; Echo: 1-bit masks, dropped tensors regenerated from the
+    regenerated h / kept a_t; Echo with Philox-regenerated masks: nothing) matches the fp64 oracle,
+    keeps exactly the estimator's bytes, and the three give bitwise-equal gradients; the Echo step's
+    CUDA-graph replay equals its eager step bitwise."""
+    import json
+    from paper_1805_08899_b200 import abi
+    from paper_1805_08899_b200.nmt import NMTModel
+    from synth import graphs as Gr
+    params = nmt_params(11, cfg, storage)
+    batch = nmt_batch(12, cfg, lengths="random")
+    assert len(batch["drop_seeds"]) == 5
+    ref = O.step(params, batch, cfg)
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    tol = 1e-4 if storage == "fp32" else 2e-2
+    doc = json.dumps(Gr.nmt(cfg, "f32" if storage == "fp32" else "bf16"))
+    plans = {"stash": (abi.STASH, False, "baseline"), "echo": (abi.RECOMPUTE, False, "echo"),
+             "echo-regen": (abi.RECOMPUTE, True, "echo")}
+    res = {}
+    for name, (mode, regen, strat) in plans.items():
+        m = NMTModel(cfg, dt, mode, regen_masks=regen)
+        m.load_params(params)
+        m.upload_batch(batch)
+        acts = m._forward()
+        rep = json.loads(abi.echo_footprint_estimate(doc, json.dumps({"strategy": strat, "regenerate_masks": regen})))
+        assert m.stash_bytes() == rep["stash_bytes"], (name, m.stash_bytes(), rep["stash_bytes"])
+        m._backward(acts)
+        del acts
+        loss = float(m.loss.item())
+        assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"]), (name, loss, ref["loss"])
+        check_grads(m.grads_numpy(), ref["grads"], storage, FRO_ONLY.get((cfg.name, storage), ()), f"{cfg.name}/{name}")
+        res[name] = m.gflat.clone()
+        if name == "echo":
+            m.capture(0.0)
+            m.gflat.zero_()
+            m.replay()
+            torch.cuda.synchronize()
+            assert bits_equal(m.gflat, res[name])
+        del m
+    assert bits_equal(res["stash"], res["echo"]) and bits_equal(res["stash"], res["echo-regen"])

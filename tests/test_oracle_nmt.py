@@ -3,7 +3,7 @@ import numpy as np
 import torch
 
 from oracle import nmt as O
-from synth.configs import C1, SMALL_NMT
+from synth.configs import NMTConfig, C1, SMALL_NMT
 from synth.data import nmt_params, nmt_batch
 
 
@@ -48,15 +48,19 @@ def test_fd_sampled_gradients_c1():
             assert abs(num - ana) <= 1e-7 + 1e-6 * abs(num), (name, i, num, ana)
 
 
-def _torch_nmt_loss(P, b, cfg, ms=None, mt=None):
+def _torch_nmt_loss(P, b, cfg, ms=None, mt=None, hm=None):
     """Same model written with torch.nn.LSTM / LSTMCell + autograd (library routines).  ms / mt:
-    optional embedding-dropout multipliers [Ts,B,E] / [Td,B,E] (keep / (1 - p))."""
+    optional embedding-dropout multipliers [Ts,B,E] / [Td,B,E] (keep / (1 - p)); hm: optional R33
+    multipliers (encoder list, decoder list, output), applied where the layer above / the output
+    layer reads h / a_t."""
     T = {k: torch.from_numpy(v).requires_grad_(True) for k, v in P.items()}
     B, H, E = cfg.B, cfg.H, cfg.E
     x = T["emb_src"][torch.from_numpy(b["src"])].transpose(0, 1)
     if ms is not None:
         x = x * torch.from_numpy(ms)
     for l in range(cfg.enc_layers):
+        if hm is not None and l > 0:
+            x = x * torch.from_numpy(hm[0][l - 1])
         m = torch.nn.LSTM(x.shape[2], H).double()
         x, _ = torch.func.functional_call(m, {"weight_ih_l0": T[f"enc{l}.Wx"], "weight_hh_l0": T[f"enc{l}.Wh"],
                                               "bias_ih_l0": T[f"enc{l}.b"], "bias_hh_l0": torch.zeros(4 * H, dtype=torch.float64)}, (x,))
@@ -77,14 +81,14 @@ def _torch_nmt_loss(P, b, cfg, ms=None, mt=None):
             h[l], c[l] = torch.func.functional_call(cell, {"weight_ih": T[f"dec{l}.Wx"], "weight_hh": T[f"dec{l}.Wh"],
                                                           "bias_ih": T[f"dec{l}.b"], "bias_hh": torch.zeros(4 * H, dtype=torch.float64)},
                                                     (inp, (h[l], c[l])))
-            inp = h[l]
+            inp = h[l] * torch.from_numpy(hm[1][l][t]) if hm is not None and l < cfg.dec_layers - 1 else h[l]
         q = inp
         qp = q @ T["att.Wq"].T + T["att.bq"]
         sc = torch.tanh(qp[:, None, :] + Kp) @ T["att.v"]
         alpha = torch.softmax(sc.masked_fill(~valid, float("-inf")), dim=1)
         ctx = torch.einsum("bs,bsk->bk", alpha, Hs)
         a = torch.tanh(ctx @ T["att.Wcc"].T + q @ T["att.Wch"].T)
-        logits = a @ T["out.Wo"].T + T["out.bo"]
+        logits = (a * torch.from_numpy(hm[2][t]) if hm is not None else a) @ T["out.Wo"].T + T["out.bo"]
         loss = loss + torch.nn.functional.cross_entropy(logits, torch.from_numpy(b["tgt_out"][:, t]), reduction="sum")
     loss = loss / (B * cfg.Td)
     loss.backward()
@@ -140,3 +144,45 @@ def test_embedding_dropout_oracle_pins():
     r0 = O.step(P1, b1, replace(c1, dropout=0.0))
     r00 = O.step(P1, b1, C1)
     assert r0["loss"] == r00["loss"]
+
+
+def test_hidden_dropout_oracle_pins():
+    """R33 hidden dropout (inter-layer LSTM inputs, a_t into the output layer): (1) torch autograd of
+    the same model with the masks applied explicitly at those points, every gradient to 1e-10; (2) the
+    masks keep ~(1 - p) of the elements and are distinct per site; (3) central FD on a 2+2-layer tiny
+    config; (4) p = 0 equals no dropout."""
+    from dataclasses import replace
+    cfg = replace(SMALL_NMT, dropout=0.2, dropout_hidden=0.3)
+    P = _f64(nmt_params(5, cfg))
+    b = nmt_batch(6, cfg, lengths="random")
+    assert len(b["drop_seeds"]) == 2 + cfg.hidden_drop_sites() == 5
+    r = O.step(P, b, cfg)
+    from oracle.dot_softmax import dropout_keep_mask
+    ks, kt = (int(x) for x in b["drop_seeds"][:2])
+    ms = dropout_keep_mask(ks, 0, cfg.Ts * cfg.B * cfg.E, 0.2).reshape(cfg.Ts, cfg.B, cfg.E) / 0.8
+    mt = dropout_keep_mask(kt, 0, cfg.Td * cfg.B * cfg.E, 0.2).reshape(cfg.Td, cfg.B, cfg.E) / 0.8
+    hm = O.hidden_masks(cfg, b)
+    for m in hm[0] + hm[1] + [hm[2]]:
+        assert 0.55 < (m > 0).mean() < 0.85
+    assert not np.array_equal(hm[1][0] > 0, hm[2] > 0)
+    tl, tg = _torch_nmt_loss(P, b, cfg, ms, mt, hm)
+    assert abs(r["loss"] - tl) < 1e-12
+    for k in P:
+        scale = max(np.abs(tg[k]).max(), 1e-30)
+        assert np.abs(r["grads"][k] - tg[k]).max() / scale < 1e-10, k
+    tiny = NMTConfig("tiny2", B=2, Ts=3, Td=3, E=8, H=8, A=8, V=11, enc_layers=2, dec_layers=2, dropout_hidden=0.4)
+    P1 = _f64(nmt_params(3, tiny))
+    b1 = nmt_batch(4, tiny)
+    G = O.step(P1, b1, tiny)["grads"]
+    eps = 1e-6
+    for name in ("enc0.Wx", "enc1.Wx", "dec0.Wh", "dec1.Wx", "out.Wo", "att.Wq"):
+        for i in (0, 5, 17):
+            Pp = {k: v.copy() for k, v in P1.items()}
+            Pm = {k: v.copy() for k, v in P1.items()}
+            Pp[name].reshape(-1)[i] += eps
+            Pm[name].reshape(-1)[i] -= eps
+            num = (O.step(Pp, b1, tiny, False)["loss"] - O.step(Pm, b1, tiny, False)["loss"]) / (2 * eps)
+            assert abs(num - G[name].reshape(-1)[i]) <= 1e-7 + 1e-6 * abs(num), (name, i)
+    assert O.step(P1, b1, replace(tiny, dropout_hidden=0.0))["loss"] == \
+        O.step(P1, {k: v for k, v in b1.items() if k != "drop_seeds"} | {"drop_seeds": b1["drop_seeds"][:2]},
+               replace(tiny, dropout_hidden=0.0))["loss"]
