@@ -396,6 +396,14 @@ echo_status echo_dropout_apply(int64_t n, float p, uint64_t seed, uint64_t offse
                                int32_t mask_kind, int32_t x_dtype, const void* x, int32_t y_dtype, void* y,
                                int32_t accumulate, void* stream);
 
+/* 1-bit feature maps for the automatic fx pass (fx_pass.py; Alg. 1 line 18):
+ * a ReLU's gradient reads only the sign of its output and a dropout's only its keep-mask.
+ * echo_sign_pack:   bits[j] bit k = (x[8j + k] > 0)  (x dtype 0 fp32, 1 bf16, 2 u8 / bool: != 0)
+ * echo_bits_unpack: out[i] = bit i ? 1 : 0  (out dtype 0 fp32, 1 bf16, 2 u8 / bool)
+ *  n elements (> 0); bits [(n + 7) / 8] uint8; device pointers.  Errors: ECHO_ERR_INVALID.          */
+echo_status echo_sign_pack(int64_t n, int32_t dtype, const void* x, uint8_t* bits, void* stream);
+echo_status echo_bits_unpack(int64_t n, const uint8_t* bits, int32_t dtype, void* out, void* stream);
+
 /* Backward of the attention hidden a_t = tanh(pre_t) (reading R7, §2;
  * tanh keeps its output): dpre[i] = da[i] * (1 - a[i]^2), fp32 arithmetic in that
  * order (a read in its storage dtype).  Outside the Echo decision (a_t is kept in both modes).

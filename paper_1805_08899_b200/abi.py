@@ -31,7 +31,7 @@ EXPORTED = NORTH_STAR + (
             "echo_lstm_fwd_tc", "echo_lstm_fwd_tc_supported",
             "echo_attn_bwd_deferred", "echo_attn_bwd_finish", "echo_attn_bwd_accumulate", "echo_tanh_bwd",
             "echo_lstm_fwd_parts", "echo_lstm_cscan_parts", "echo_lstm_bwd_parts",
-            "echo_dropout_fwd", "echo_dropout_apply")
+            "echo_dropout_fwd", "echo_dropout_apply", "echo_sign_pack", "echo_bits_unpack")
 
 
 class EchoError(RuntimeError):
@@ -79,6 +79,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "echo_lstm_fwd": [ctypes.POINTER(LstmDesc)] + [vp] * 9,
         "echo_lstm_cscan": [ctypes.POINTER(LstmDesc), i32, vp, vp, vp, vp, vp],
         "echo_lstm_fwd_tc": [ctypes.POINTER(LstmDesc)] + [vp] * 10,
+        "echo_sign_pack": [ctypes.c_int64, i32, vp, vp, vp],
+        "echo_bits_unpack": [ctypes.c_int64, vp, i32, vp, vp],
         "echo_lstm_fwd_tc_supported": [i32, i32, i32],
         "echo_lstm_bwd_recompute": [ctypes.POINTER(LstmDesc), i32, i32, ctypes.c_uint32] + [vp] * 11,
         "echo_attn_fwd": [ctypes.POINTER(AttnDesc)] + [vp] * 9,
@@ -350,3 +352,20 @@ def echo_footprint_estimate(graph_json: str, config_json: str | None = None) -> 
     buf = ctypes.create_string_buffer(n.value)
     _check(lib.echo_footprint_estimate(g, c, buf, ctypes.byref(n)))
     return buf.value.decode()
+
+
+def _bdt(t):
+    import torch
+    return {torch.float32: 0, torch.bfloat16: 1, torch.uint8: 2, torch.bool: 2}[t.dtype]
+
+
+def echo_sign_pack(x, bits, stream=None):
+    """bits (uint8 [(n+7)/8]) <- sign bits of x (> 0; bool / uint8: != 0)."""
+    LAUNCHES["count"] += 1
+    _check(load().echo_sign_pack(x.numel(), _bdt(x), _p(x), _p(bits), _stream(stream)))
+
+
+def echo_bits_unpack(bits, out, stream=None):
+    """out (fp32 / bf16 / uint8 / bool) <- 0 / 1 from bits."""
+    LAUNCHES["count"] += 1
+    _check(load().echo_bits_unpack(out.numel(), _p(bits), _bdt(out), _p(out), _stream(stream)))

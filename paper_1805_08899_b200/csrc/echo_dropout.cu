@@ -166,3 +166,81 @@ extern "C" echo_status echo_dropout_apply(int64_t n, float p, uint64_t seed, uin
   if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
   return check_launch(fn);
 }
+
+// ================================================================ 1-bit feature maps of the fx pass
+// Binarization (Alg. 1 line 18) of an arbitrary PyTorch graph's ReLU
+// outputs and boolean dropout masks (fx_pass.py): a ReLU's gradient reads only
+// the sign of its output, a dropout's only its keep-mask, so 1 bit per element is kept.
+// pack: bit k of byte j = (x[8 j + k] > 0) (dtype 0 fp32, 1 bf16, 2 u8/bool: != 0)
+// unpack: out[i] = bit i ? 1 : 0 in out's dtype (0 fp32, 1 bf16, 2 u8/bool)
+namespace echo {
+template <typename T>
+__device__ __forceinline__ bool positive(T v) { return to_f(v) > 0.0f; }
+template <>
+__device__ __forceinline__ bool positive<uint8_t>(uint8_t v) { return v != 0; }
+
+template <typename T>
+__global__ void __launch_bounds__(256) sign_pack_kernel(long n, const T* __restrict__ x, uint8_t* __restrict__ bits) {
+  pdl_wait();
+  const long nb = (n + 7) / 8;
+  for (long j = (long)blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += (long)gridDim.x * blockDim.x) {
+    uint32_t b = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long i = 8 * j + k;
+      if (i < n && positive<T>(x[i])) b |= 1u << k;
+    }
+    bits[j] = (uint8_t)b;
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(256) bits_unpack_kernel(long n, const uint8_t* __restrict__ bits, T* __restrict__ out) {
+  pdl_wait();
+  const long nb = (n + 7) / 8;
+  for (long j = (long)blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += (long)gridDim.x * blockDim.x) {
+    const uint32_t b = bits[j];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long i = 8 * j + k;
+      if (i < n) {
+        if constexpr (sizeof(T) == 1) out[i] = (T)((b >> k) & 1u);
+        else out[i] = from_f<T>((b >> k) & 1u ? 1.0f : 0.0f);
+      }
+    }
+  }
+}
+static int sp_grid(long n) {
+  long g = ((n + 7) / 8 + 255) / 256;
+  return (int)(g < 148L * 16 ? (g > 0 ? g : 1) : 148L * 16);
+}
+}  // namespace echo
+
+extern "C" echo_status echo_sign_pack(int64_t n, int32_t dtype, const void* x, uint8_t* bits, void* stream) {
+  using namespace echo;
+  const char* fn = "echo_sign_pack";
+  if (n <= 0 || !x || !bits) return fail(ECHO_ERR_INVALID, "%s: n=%lld, x / bits NULL", fn, (long long)n);
+  cudaError_t e;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == 0) e = launch(sign_pack_kernel<float>, dim3(sp_grid(n)), dim3(256), 0, st, 1, (long)n, (const float*)x, bits);
+  else if (dtype == 1)
+    e = launch(sign_pack_kernel<__nv_bfloat16>, dim3(sp_grid(n)), dim3(256), 0, st, 1, (long)n, (const __nv_bfloat16*)x, bits);
+  else if (dtype == 2) e = launch(sign_pack_kernel<uint8_t>, dim3(sp_grid(n)), dim3(256), 0, st, 1, (long)n, (const uint8_t*)x, bits);
+  else return fail(ECHO_ERR_INVALID, "%s: bad dtype %d", fn, dtype);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
+}
+
+extern "C" echo_status echo_bits_unpack(int64_t n, const uint8_t* bits, int32_t dtype, void* out, void* stream) {
+  using namespace echo;
+  const char* fn = "echo_bits_unpack";
+  if (n <= 0 || !out || !bits) return fail(ECHO_ERR_INVALID, "%s: n=%lld, bits / out NULL", fn, (long long)n);
+  cudaError_t e;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == 0) e = launch(bits_unpack_kernel<float>, dim3(sp_grid(n)), dim3(256), 0, st, 1, (long)n, bits, (float*)out);
+  else if (dtype == 1)
+    e = launch(bits_unpack_kernel<__nv_bfloat16>, dim3(sp_grid(n)), dim3(256), 0, st, 1, (long)n, bits, (__nv_bfloat16*)out);
+  else if (dtype == 2) e = launch(bits_unpack_kernel<uint8_t>, dim3(sp_grid(n)), dim3(256), 0, st, 1, (long)n, bits, (uint8_t*)out);
+  else return fail(ECHO_ERR_INVALID, "%s: bad dtype %d", fn, dtype);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
+}

@@ -1,0 +1,71 @@
+"""The automatic fx pass on the host: tracing into the estimator's schema, the
+plan's decisions, and refusals (no GPU needed; the GPU run is tests/test_gpu_fx_pass.py)."""
+import json
+
+import pytest
+import torch
+import torch.nn as nn
+
+from tests.fx_models import GatedNet, ResMLP, ReluTaps
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_1805_08899_b200 import build, abi
+    build.build()
+    abi.load()
+
+
+def test_plan_of_gated_net():
+    from paper_1805_08899_b200 import fx_pass as X
+    m = GatedNet(16, 2)
+    x = torch.randn(8, 16)
+    p = X.EchoPlan(m, (x,))
+    ops = [n["op"] for n in p.doc["nodes"]]
+    assert ops.count("fully_connected") == 7 and ops.count("dropout") == 2 and ops.count("mul") == 2
+    assert sum(1 for q in p.doc["placeholders"] if q["trainable"]) == 14          # 7 weights + 7 biases
+    b = X.EchoPlan(m, (x,), strategy="baseline")
+    assert p.stash_bytes() < b.stash_bytes()
+    kinds = set(p.decision.values())
+    assert "recompute" in kinds and "bit" in kinds                # mirrored maps and 1-bit dropout masks
+    # the plan is the estimator's: the same document through the C ABI gives the same bytes
+    from paper_1805_08899_b200 import abi
+    r = json.loads(abi.echo_footprint_estimate(json.dumps(p.doc), json.dumps({"strategy": "echo"})))
+    assert r["stash_bytes"] == p.stash_bytes()
+
+
+def test_plan_recomputes_relu_maps():
+    """ReLU outputs between FCs: Echo keeps the FC outputs the FCs need anyway and regenerates the ReLU
+    maps (mirrored, Fig. 4) instead of keeping them -- here better than 1-bit signs (0 extra bytes);
+    never worse than the Baseline on a residual MLP either."""
+    from paper_1805_08899_b200 import fx_pass as X
+    m = ReluTaps(16, 3)
+    x = torch.randn(4, 16)
+    p = X.EchoPlan(m, (x,))
+    b = X.EchoPlan(m, (x,), strategy="baseline")
+    relu_ids = [n["id"] for n in p.doc["nodes"] if n["op"] == "relu"]
+    assert all(p.decision.get((i, 0)) == "recompute" for i in relu_ids)
+    assert all(b.decision.get((i, 0)) == "stash" for i in relu_ids if (i, 0) in b.decision)
+    assert b.stash_bytes() - p.stash_bytes() == 2 * 4 * 16 * 4
+    r = ResMLP(16, 3)
+    assert X.EchoPlan(r, (x,)).stash_bytes() <= X.EchoPlan(r, (x,), strategy="baseline").stash_bytes()
+
+
+def test_unsupported_ops_raise():
+    from paper_1805_08899_b200 import fx_pass as X
+
+    class Conv(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.c = nn.Conv1d(2, 2, 3)
+
+        def forward(self, x):
+            return self.c(x).sum()
+
+    class Bcast(nn.Module):
+        def forward(self, x):
+            return (x + x[:1]).sum()
+    with pytest.raises(X.Unsupported):
+        X.EchoPlan(Conv(), (torch.randn(1, 2, 8),))
+    with pytest.raises(X.Unsupported):
+        X.EchoPlan(Bcast(), (torch.randn(4, 8),))
