@@ -165,7 +165,7 @@ class _Run(fx.Interpreter):
     def run_node(self, n):
         self.o.current = n
         out = super().run_node(n)
-        if isinstance(out, torch.Tensor):
+        if isinstance(out, torch.Tensor) and n in self.o.plan.node_id:
             self.o._record(n, out)
         return out
 
@@ -289,6 +289,9 @@ class EchoModule(nn.Module):
         if _kind(gm, n) == "dropout":                         # mirrored dropout: re-apply the kept mask
             m = gm.get_submodule(n.target) if n.op == "call_module" else None
             p = m.p if m is not None else kwargs.get("p", args[1] if len(args) > 1 else 0.5)
+            training = m.training if m is not None else kwargs.get("training", True)
+            if p == 0.0 or not training:                      # identity: no mask was drawn
+                return args[0]
             mask = self._value((self.plan.node_id[n], 1))
             return args[0] * mask * (1.0 / (1.0 - p))
         if n.op == "call_module":
