@@ -605,6 +605,33 @@ __device__ __forceinline__ float score_partial_r(const T* kz_row, const float (&
   return warp_sum(acc);
 }
 
+// score_partial_r for bf16 storage with z = qp + Kp formed by packed bf16x2 adds (add.rn.bf16x2:
+// the exact sum rounded once to bf16).  Equal to z_of<bf16> = round_bf16(fp32(qp) + fp32(kz)): both
+// operands are bf16, so their fp32 sum is exact unless the exponents differ by more than 15, and then
+// the smaller one is below 2^-15 of the larger, far from any bf16 rounding midpoint -- both round to
+// the larger operand.  Same E, same FMA order: bit-identical, 2.5 fewer instructions per element.
+__device__ __forceinline__ float score_partial_bf2(const __nv_bfloat16* kz_row, const uint2& q2, const float (&vr)[4],
+                                                   bool act, int c4, __nv_bfloat16* z_out) {
+  float acc = 0.0f;
+  if (act) {
+    const uint2 k2 = *reinterpret_cast<const uint2*>(kz_row + c4 * 4);
+    const __nv_bfloat162 za = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&q2.x),
+                                      *reinterpret_cast<const __nv_bfloat162*>(&k2.x));
+    const __nv_bfloat162 zb = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&q2.y),
+                                      *reinterpret_cast<const __nv_bfloat162*>(&k2.y));
+    const float z[4] = {__low2float(za), __high2float(za), __low2float(zb), __high2float(zb)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc = __fmaf_rn(att_tanh<__nv_bfloat16>(z[k]), vr[k], acc);
+    if (z_out) {
+      uint2 u;
+      *reinterpret_cast<__nv_bfloat162*>(&u.x) = za;
+      *reinterpret_cast<__nv_bfloat162*>(&u.y) = zb;
+      *reinterpret_cast<uint2*>(z_out + c4 * 4) = u;
+    }
+  }
+  return warp_sum(acc);
+}
+
 // Per-lane partials of GR row slots -> full warp sums with log2(GR) halving exchanges (each lane
 // keeps the half of its slots picked by one lane bit) and 5 - log2(GR) butterflies: GR - 1 + 5 -
 // log2(GR) shuffles instead of 5 GR.  Every slot's sum is formed by the SAME pairwise tree as
@@ -881,9 +908,11 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
   mbar_wait(&bar[0], 0);                                      // chunk 0 + the qp / v slices
   const bool act = lane < W / 4;                              // W <= 128: one column group per lane
   float qr[4] = {0.0f, 0.0f, 0.0f, 0.0f}, vr[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  uint2 q2 = make_uint2(0u, 0u);                              // bf16: the lane's qp slice, packed
   if (act) {
     lds4(qps + lane * 4, qr);
     lds4(vs + lane * 4, vr);
+    if constexpr (sizeof(T) == 2) q2 = *reinterpret_cast<const uint2*>(qps + lane * 4);
   }
   cluster_wait();                                             // every CTA's xbar is initialised
   // lane c < C delivers the warp's partial to cluster CTA c (row `rank` of its receive buffer)
@@ -895,7 +924,12 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
     mbar_wait(&bar[k], 0);
     for (; s < s1; s += ATT_WARPS) {
       T* z_out = Z_st ? Z_st + ((long)b * Ts + s) * A + g.a0 : nullptr;
-      const float p = score_partial_r<T>(kz + (size_t)s * Wb, qr, vr, act, lane, true, z_out, nullptr);
+      float p;
+      if constexpr (sizeof(T) == 2)
+        p = score_partial_bf2(reinterpret_cast<const __nv_bfloat16*>(kz) + (size_t)s * Wb, q2, vr, act, lane,
+                              reinterpret_cast<__nv_bfloat16*>(z_out));
+      else
+        p = score_partial_r<T>(kz + (size_t)s * Wb, qr, vr, act, lane, true, z_out, nullptr);
       if (C > 1) {
         if (lane < C) st_async_f32(dst_row + 4u * (uint32_t)s, p, dst_bar);
       } else if (lane == 0) {
@@ -1038,6 +1072,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
         if (WH > 0) tma_prefetch_3d(&mdH, g.h0, b, k * R, pol);
       }
     ECHO_PHASE(12);
+  }
+  if (tid == 32 && dKp && q.pf == 3) {                        // dKp / dH_s into L2 from a second thread at
+    prefetch_tmap(&mdK);                                       // kernel start, alongside the stage-in issue
+    prefetch_tmap(&mdH);
+    for (int k = 0; k * R < n; ++k) {
+      if (W > 0) tma_prefetch_3d(&mdK, g.a0, b, k * R, pol);
+      if (WH > 0) tma_prefetch_3d(&mdH, g.h0, b, k * R, pol);
+    }
   }
   // values only the epilogue / softmax need are fetched now so their latency hides under the
   // staging wait (W <= 128 < ATT_THREADS: one column per thread, see tma_cluster)
@@ -1374,7 +1416,7 @@ static size_t bwd_smem(const echo_attn_desc* d) {
 static int a6_prefetch_mode() {
   static const int m = [] {
     const char* e = getenv("ECHO_A6_PREFETCH");
-    return e && *e >= '0' && *e <= '2' ? *e - '0' : 1;
+    return e && *e >= '0' && *e <= '3' ? *e - '0' : 1;
   }();
   return m;
 }
