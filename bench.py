@@ -41,7 +41,7 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms from just before the timed region to its end."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -54,7 +54,7 @@ class ClockSampler:
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
@@ -447,9 +447,17 @@ def run_ours(args):
         ms, launches = timed(model, False, args.steps, args.warmup)
     sampler = ClockSampler(local)
     sampler.start()
-    # clocks are sampled over a second identical timed region (the first one followed the capture)
+    # clocks are sampled over a second identical timed region (the first one followed the capture);
+    # the sampler starts before that region's own W warm-up steps so that a short region (bf16: K
+    # steps of ~7 ms) still gets samples taken under the same load
     run = runner(model, use_graph)
-    torch.cuda.synchronize()
+    t_w = time.perf_counter()
+    while True:
+        for _ in range(args.warmup):
+            run()
+        torch.cuda.synchronize()
+        if time.perf_counter() - t_w > 0.5:
+            break
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(args.steps):
