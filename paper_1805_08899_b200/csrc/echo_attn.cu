@@ -1416,7 +1416,7 @@ static size_t bwd_smem(const echo_attn_desc* d) {
 static int a6_prefetch_mode() {
   static const int m = [] {
     const char* e = getenv("ECHO_A6_PREFETCH");
-    return e && *e >= '0' && *e <= '3' ? *e - '0' : 1;
+    return e && *e >= '0' && *e <= '3' ? *e - '0' : 3;
   }();
   return m;
 }
