@@ -56,16 +56,30 @@ __device__ unsigned long long g_echo_phase[16][8192];
 // approximations (absolute error <= 1.8e-7 over all floats, scripts/micro/tanh_err.cu: 20000x
 // below the bf16 rounding of z) in 7 instructions instead of 16.  Every kernel that evaluates E
 // for a given storage type uses this function, so STASH and RECOMPUTE stay bit-identical.
+// Round 2: E = 1 - 2 / (2^(2 log2(e) z) + 1) without the |z| / copysign (large negative z: ex2
+// flushes to 0 -> -1; large positive: inf -> 1), so two elements can be evaluated with the packed
+// fp32x2 FMUL2 / FADD2 / FFMA2 of sm_100 (att_tanh2_bf16: the same IEEE operations per lane, hence
+// the same bits as this scalar form).  Max abs error over all floats: scripts/micro/tanh_err.cu.
 template <typename T>
 __device__ __forceinline__ float att_tanh(float z) {
   if constexpr (sizeof(T) == 4) {
     return tanhf(z);
   } else {
     float e, r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(z) * 2.8853900817779268f));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
-    return copysignf(__fmaf_rn(-2.0f, r, 1.0f), z);
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmul_rn(z, 2.8853900817779268f)));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fadd_rn(e, 1.0f)));
+    return __fmaf_rn(-2.0f, r, 1.0f);
   }
+}
+__device__ __forceinline__ float2 att_tanh2_bf16(float2 z) {
+  const float2 t = __fmul2_rn(z, make_float2(2.8853900817779268f, 2.8853900817779268f));
+  float2 e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(t.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(t.y));
+  const float2 d = __fadd2_rn(e, make_float2(1.0f, 1.0f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(d.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(d.y));
+  return __ffma2_rn(r, make_float2(-2.0f, -2.0f), make_float2(1.0f, 1.0f));
 }
 
 constexpr int ATT_THREADS = 256;
@@ -619,9 +633,11 @@ __device__ __forceinline__ float score_partial_bf2(const __nv_bfloat16* kz_row, 
                                       *reinterpret_cast<const __nv_bfloat162*>(&k2.x));
     const __nv_bfloat162 zb = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&q2.y),
                                       *reinterpret_cast<const __nv_bfloat162*>(&k2.y));
-    const float z[4] = {__low2float(za), __high2float(za), __low2float(zb), __high2float(zb)};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc = __fmaf_rn(att_tanh<__nv_bfloat16>(z[k]), vr[k], acc);
+    const float2 ea = att_tanh2_bf16(__bfloat1622float2(za)), eb = att_tanh2_bf16(__bfloat1622float2(zb));
+    acc = __fmaf_rn(ea.x, vr[0], acc);
+    acc = __fmaf_rn(ea.y, vr[1], acc);
+    acc = __fmaf_rn(eb.x, vr[2], acc);
+    acc = __fmaf_rn(eb.y, vr[3], acc);
     if (z_out) {
       uint2 u;
       *reinterpret_cast<__nv_bfloat162*>(&u.x) = za;
@@ -1120,11 +1136,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 4) attn_bwd_tma(echo_attn_desc d,
           float kzv[4], z[4], e[4];
           lds4(kz + (size_t)s * Wb + lane * 4, kzv);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            z[q] = z_of<T>(recompute ? qr[q] : 0.0f, kzv[q], recompute);
-            e[q] = att_tanh<T>(z[q]);
-            psc[j] = __fmaf_rn(e[q], vr[q], psc[j]);
+          for (int q = 0; q < 4; ++q) z[q] = z_of<T>(recompute ? qr[q] : 0.0f, kzv[q], recompute);
+          if constexpr (sizeof(T) == 2) {                       // packed f32x2 tanh (same bits)
+            const float2 ea = att_tanh2_bf16(make_float2(z[0], z[1])), eb = att_tanh2_bf16(make_float2(z[2], z[3]));
+            e[0] = ea.x; e[1] = ea.y; e[2] = eb.x; e[3] = eb.y;
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) e[q] = att_tanh<T>(z[q]);
           }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) psc[j] = __fmaf_rn(e[q], vr[q], psc[j]);
           *reinterpret_cast<float4*>(E + (size_t)s * Wb + lane * 4) = make_float4(e[0], e[1], e[2], e[3]);
         }
         if (actH) {

@@ -835,31 +835,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) lstm_fwd_tc_kernel(const __grid
                  : "memory");
   }
   __syncwarp();
+  // epilogue: warp w -> TMEM lanes (rows) 32 (w % 4) + lane, units j0 + 4 (w / 4) + 0..3; the
+  // accumulator column of gate g, unit u is g * 16 + u.  The cell's other operands (gx_t, bias,
+  // c_{t-1}) do not depend on the MMA: they are loaded before waiting for it
+  const int lg = w & 3, ug = w >> 2;
+  const int b = 32 * lg + (tid & 31);
+  const int j = j0 + 4 * ug;
+  const long row4 = (long)b * 4 * H;
+  float x[4][4], bb[4][4], cp[4];
+  if (b < B) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      ldv<4>(gx + row4 + g * H + j, x[g]);
+      ldv<4>(bias + g * H + j, bb[g]);
+    }
+    ldv<4>(c_prev + (long)b * H + j, cp);
+  }
   tc_mbar_wait(&done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  // epilogue: warp w -> TMEM lanes (rows) 32 (w % 4) + lane, units j0 + 4 (w / 4) + 0..3; the
-  // accumulator column of gate g, unit u is g * 16 + u
-  const int lg = w & 3, ug = w >> 2;
   float acc[4][4];
 #pragma unroll
   for (int g = 0; g < 4; ++g) tc_ld4(tmem + ((uint32_t)(32 * lg) << 16) + (uint32_t)(g * TC_U + 4 * ug), acc[g]);
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-  const int b = 32 * lg + (tid & 31);
-  const int j = j0 + 4 * ug;
   if (b < B) {
-    const long row4 = (long)b * 4 * H;
     float a[4][4];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      float x[4], bb[4];
-      ldv<4>(gx + row4 + g * H + j, x);
-      ldv<4>(bias + g * H + j, bb);
+    for (int g = 0; g < 4; ++g)
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        a[g][u] = __fadd_rn(St<T>::round(__fadd_rn(x[u], acc[g][u])), bb[u]);   // G = round(gx + gh); A = G + b
-    }
-    float cp[4];
-    ldv<4>(c_prev + (long)b * H + j, cp);
+        a[g][u] = __fadd_rn(St<T>::round(__fadd_rn(x[g][u], acc[g][u])), bb[g][u]);   // G = round(gx + gh); A = G + b
     float gi[4], gf[4], gg[4], go[4], c[4], tc[4], h[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
