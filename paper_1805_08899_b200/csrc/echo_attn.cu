@@ -934,6 +934,59 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
   // lane c < C delivers the warp's partial to cluster CTA c (row `rank` of its receive buffer)
   const uint32_t dst_row = C > 1 ? mapa_u32(smem_u32(xpart + rank * Tp), lane < C ? lane : 0) : 0u;
   const uint32_t dst_bar = C > 1 ? mapa_u32(smem_u32(&xbar), lane < C ? lane : 0) : 0u;
+  if (!Z_st && W == 4 * 32) {
+    // RECOMPUTE with a full 128-column slice (every lane active): two positions per iteration, the K row
+    // addressed with 32-bit shared addresses, no per-lane branch -- the same per-position arithmetic
+    // (z, tanh, FMA order, warp_sum tree) as score_partial_bf2 / score_partial_r, fewer instructions
+    const uint32_t kz_s = smem_u32(kz) + (uint32_t)(lane * 4 * sizeof(T)), rowb = (uint32_t)(Wb * sizeof(T));
+    auto part = [&](int s) -> float {
+      float acc = 0.0f;
+      if constexpr (sizeof(T) == 2) {
+        uint32_t k0, k1;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(k0), "=r"(k1) : "r"(kz_s + (uint32_t)s * rowb));
+        const __nv_bfloat162 za = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&q2.x),
+                                          *reinterpret_cast<const __nv_bfloat162*>(&k0));
+        const __nv_bfloat162 zb = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&q2.y),
+                                          *reinterpret_cast<const __nv_bfloat162*>(&k1));
+        const float2 ea = att_tanh2_bf16(__bfloat1622float2(za)), eb = att_tanh2_bf16(__bfloat1622float2(zb));
+        acc = __fmaf_rn(ea.x, vr[0], acc);
+        acc = __fmaf_rn(ea.y, vr[1], acc);
+        acc = __fmaf_rn(eb.x, vr[2], acc);
+        acc = __fmaf_rn(eb.y, vr[3], acc);
+      } else {
+        float4 kv;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(kv.x), "=f"(kv.y), "=f"(kv.z), "=f"(kv.w)
+                     : "r"(kz_s + (uint32_t)s * rowb));
+        const float kz4[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc = __fmaf_rn(att_tanh<T>(z_of<T>(qr[q], kz4[q], true)), vr[q], acc);
+      }
+      return acc;
+    };
+    auto send = [&](int s, float p) {
+      if (C > 1) {
+        if (lane < C) st_async_f32(dst_row + 4u * (uint32_t)s, p, dst_bar);
+      } else if (lane == 0) {
+        xpart[s] = p;
+        mbar_arrive(&xbar);
+      }
+    };
+    for (int k = 0, s = w; k * R < n; ++k) {
+      const int s1 = min(n, (k + 1) * R);
+      if (s >= s1) continue;
+      mbar_wait(&bar[k], 0);
+      for (; s + ATT_WARPS < s1; s += 2 * ATT_WARPS) {
+        const float a0 = part(s), a1 = part(s + ATT_WARPS);
+        const float p0 = warp_sum(a0), p1 = warp_sum(a1);
+        send(s, p0);
+        send(s + ATT_WARPS, p1);
+      }
+      if (s < s1) {
+        send(s, warp_sum(part(s)));
+        s += ATT_WARPS;
+      }
+    }
+  } else
   for (int k = 0, s = w; k * R < n; ++k) {                   // chunk by chunk: one wait per chunk
     const int s1 = min(n, (k + 1) * R);
     if (s >= s1) continue;
