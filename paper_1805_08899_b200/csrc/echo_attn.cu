@@ -1012,7 +1012,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
     for (int s = n + w; s < Ts; s += ATT_WARPS)
       for (int c4 = lane; c4 < W / 4; c4 += 32) stg4(Z_st + ((long)b * Ts + s) * A + g.a0 + c4 * 4, z);
   }
-  const bool ctx_warp = w * 32 < WH;                          // ctx: one thread per column
+  const bool ctx_warp = w * 64 < WH;                          // ctx: one thread per column pair
   if (!ctx_warp && !(alpha_st && rank == 0 && w == 0)) return;
   mbar_wait(&xbar, 0);                                        // all C partial rows received
   // scores (rank-ordered sum, = gather_sum) and softmax (= softmax_row_warp) for s = lane + 32 k
@@ -1044,12 +1044,18 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
       if (lane + 32 * k < Ts) alpha_st[(long)b * Ts + lane + 32 * k] = sc[k];
   if (!ctx_warp) return;
   for (int k = 0; k * R < n; ++k) mbar_wait(&bar[k], 0);     // every H_s chunk landed
-  // ctx_columns with alpha_s taken from lane s % 32 of register sc[s / 32]: the same FMAs into the
-  // same four accumulators (s mod 4) in the same order, so ctx is bit-identical to ctx_columns'
-  const int c = tid;
-  const bool cok = c < WH;
+  // ctx_columns with alpha_s taken from lane s % 32 of register sc[s / 32], two adjacent columns per
+  // thread (one 2-element shared load and one shuffle per position serve both): per column the same
+  // FMAs into the same four accumulators (s mod 4) in the same order, so ctx is bit-identical to
+  // ctx_columns'
+  const int c = 2 * tid;
+  const bool cok = c < WH;                                    // WH is even (a multiple of 8)
   const T* hcol = hs + c;
-  float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+  float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f, b0 = 0.0f, b1 = 0.0f, b2 = 0.0f, b3 = 0.0f;
+  auto h2 = [&](int s) -> float2 {
+    if constexpr (sizeof(T) == 2) return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(hcol + s * WHb));
+    else return *reinterpret_cast<const float2*>(hcol + s * WHb);
+  };
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     if (32 * k >= n) break;
@@ -1060,14 +1066,22 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, Tm
       const float al0 = __shfl_sync(0xffffffffu, ak, j), al1 = __shfl_sync(0xffffffffu, ak, j + 1);
       const float al2 = __shfl_sync(0xffffffffu, ak, j + 2), al3 = __shfl_sync(0xffffffffu, ak, j + 3);
       if (cok) {
-        a0 = __fmaf_rn(al0, to_f(hcol[s0 * WHb]), a0);
-        if (s0 + 1 < n) a1 = __fmaf_rn(al1, to_f(hcol[(s0 + 1) * WHb]), a1);
-        if (s0 + 2 < n) a2 = __fmaf_rn(al2, to_f(hcol[(s0 + 2) * WHb]), a2);
-        if (s0 + 3 < n) a3 = __fmaf_rn(al3, to_f(hcol[(s0 + 3) * WHb]), a3);
+        float2 x = h2(s0);
+        a0 = __fmaf_rn(al0, x.x, a0);
+        b0 = __fmaf_rn(al0, x.y, b0);
+        if (s0 + 1 < n) { x = h2(s0 + 1); a1 = __fmaf_rn(al1, x.x, a1); b1 = __fmaf_rn(al1, x.y, b1); }
+        if (s0 + 2 < n) { x = h2(s0 + 2); a2 = __fmaf_rn(al2, x.x, a2); b2 = __fmaf_rn(al2, x.y, b2); }
+        if (s0 + 3 < n) { x = h2(s0 + 3); a3 = __fmaf_rn(al3, x.x, a3); b3 = __fmaf_rn(al3, x.y, b3); }
       }
     }
   }
-  if (cok) ctx[(long)b * Hk + g.h0 + c] = from_f<T>(St<T>::round(__fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3))));
+  if (cok) {
+    const float ya = St<T>::round(__fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3)));
+    const float yb = St<T>::round(__fadd_rn(__fadd_rn(b0, b1), __fadd_rn(b2, b3)));
+    T* o = ctx + (long)b * Hk + g.h0 + c;
+    o[0] = from_f<T>(ya);
+    o[1] = from_f<T>(yb);
+  }
 }
 
 // phase-4 work split: G = (W + WH)/4 column groups of four; P = ATT_THREADS / G position phases
