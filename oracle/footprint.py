@@ -49,7 +49,7 @@ GRAD_DEPS = {
     "tanh": (set(), {0}, 1), "relu": (set(), {0}, 1), "dropout": (set(), {1}, 2),
     "dot_last": ({0, 1}, set(), 1), "masked_softmax": ({1}, {0}, 1), "weighted_sum": ({0, 1}, set(), 1),
     "softmax_ce_loss": (set(), {1}, 2), "softmax": (set(), {0}, 1), "to_heads": (set(), set(), 1),
-    "from_heads": (set(), set(), 1),
+    "from_heads": (set(), set(), 1), "conv2d": ({0, 1}, set(), 1),
 }
 
 
@@ -90,6 +90,9 @@ class Graph:
         elif op == "from_heads":
             Hh = a["heads"]
             out = [[S[0][0] // Hh * S[0][1], Hh * S[0][2]]]
+        elif op == "conv2d":                                # x [N,C,H,W], W [O,C,kh,kw]; stride, padding
+            st, pd = a.get("stride", 1), a.get("padding", 0)
+            out = [[S[0][0], S[1][0], (S[0][2] + 2 * pd - S[1][2]) // st + 1, (S[0][3] + 2 * pd - S[1][3]) // st + 1]]
         elif op == "embedding":
             out = [S[0] + [S[1][1]]]
         elif op == "slice":
@@ -174,6 +177,9 @@ class Graph:
         o = (i, 0)
         if op == "fully_connected":
             return 2 * self.numel(o) * self.shape[ins[0]][-1]
+        if op == "conv2d":
+            w = self.shape[ins[1]]
+            return 2 * self.numel(o) * w[1] * w[2] * w[3]
         if op == "matmul":
             return 2 * self.shape[ins[0]][0] * self.shape[ins[0]][1] * self.shape[ins[1]][1]
         if op == "batched_dot":

@@ -156,7 +156,7 @@ std::string jstr(const std::string& s) {
 // ============================================================================ graph model
 enum Op {
   FC, MATMUL, BDOT, EMBED, SLICE, ADD, BADD, STACK, CONCAT, SUM, MUL, SIGMOID, TANH, RELU, DROPOUT, DOTLAST,
-  MSOFTMAX, WSUM, CE, SOFTMAX, TO_HEADS, FROM_HEADS, N_OPS
+  MSOFTMAX, WSUM, CE, SOFTMAX, TO_HEADS, FROM_HEADS, CONV2D, N_OPS
 };
 struct OpInfo {
   const char* name;
@@ -173,6 +173,7 @@ const OpInfo OPS[N_OPS] = {
     {"dot_last", 2, 2, 1, 0b11, 0},        {"masked_softmax", 2, 2, 1, 0b10, 0b1},
     {"weighted_sum", 2, 2, 1, 0b11, 0},    {"softmax_ce_loss", 2, 2, 2, 0, 0b10},
     {"softmax", 1, 1, 1, 0, 0b1},          {"to_heads", 1, 1, 1, 0, 0},    {"from_heads", 1, 1, 1, 0, 0},
+    {"conv2d", 2, 3, 1, 0b11, 0},          // like an FC: its gradient reads its input and weight (Eq. 2)
 };
 
 double dtype_width(const std::string& d) {
@@ -271,6 +272,16 @@ void infer(Graph& g, Node& n) {
       const int64_t Hh = attr_int(n, "heads", 1);
       need(I[0]->shape.size() == 3 && Hh > 0 && I[0]->shape[0] % Hh == 0, "[B*H, L, dh]");
       out.push_back({I[0]->shape[0] / Hh * I[0]->shape[1], Hh * I[0]->shape[2]});
+      break;
+    }
+    case CONV2D: {   // x [N,C,H,W], W [O,C,kh,kw] (+ bias [O]); attrs stride, padding (dilation 1, groups 1)
+      need(I[0]->shape.size() == 4 && I[1]->shape.size() == 4 && I[0]->shape[1] == I[1]->shape[1], "x[N,C,H,W] W[O,C,kh,kw]");
+      const int64_t st = attr_int(n, "stride", 1), pd = attr_int(n, "padding", 0);
+      need(st > 0 && pd >= 0, "stride > 0, padding >= 0");
+      const int64_t oh = (I[0]->shape[2] + 2 * pd - I[1]->shape[2]) / st + 1;
+      const int64_t ow = (I[0]->shape[3] + 2 * pd - I[1]->shape[3]) / st + 1;
+      need(oh > 0 && ow > 0, "output size");
+      out.push_back({I[0]->shape[0], I[1]->shape[0], oh, ow});
       break;
     }
     case EMBED: {
@@ -486,6 +497,7 @@ int64_t flops(const Graph& g, const Node& n) {
   const Edge& o = g.edges[n.out[0]];
   switch (n.op) {
     case FC: return 2 * o.numel() * E(0).shape.back();
+    case CONV2D: return 2 * o.numel() * E(1).shape[1] * E(1).shape[2] * E(1).shape[3];
     case MATMUL: return 2 * E(0).shape[0] * E(0).shape[1] * E(1).shape[1];
     case BDOT: return 2 * E(0).shape[0] * E(0).shape[1] * E(0).shape[2] * (o.numel() / (E(0).shape[0] * E(0).shape[1]));
     case DOTLAST: return 2 * E(0).numel();

@@ -7,7 +7,7 @@ Echo is an automatic graph pass that needs no model changes).
 1. `torch.fx` traces the model (its forward must return the scalar training loss) and ShapeProp
    records every tensor's shape / dtype.
 2. The traced graph is written in the estimator's graph schema (the op set of
-   oracle/footprint.py) -- Linear / F.linear -> fully_connected, relu / tanh / sigmoid, elementwise
+   oracle/footprint.py) -- Linear / F.linear -> fully_connected, Conv2d -> conv2d, relu / tanh / sigmoid, elementwise
    add / mul, matmul, softmax, dropout (two outputs: y, keep-mask), sum -> sum_reduce -- and
    echo_footprint_estimate (a8, Alg. 1) decides per feature map: stash, 1-bit, or
    recompute (mirrored) -- dead FC mirrors are never recomputed.
@@ -50,6 +50,8 @@ def _kind(gm, n):
         m = gm.get_submodule(n.target)
         if isinstance(m, nn.Linear):
             return "fully_connected"
+        if isinstance(m, nn.Conv2d):
+            return "conv2d"
         if isinstance(m, nn.ReLU):
             return "relu"
         if isinstance(m, nn.Tanh):
@@ -132,6 +134,16 @@ class EchoPlan:
                     ins = [[ids[n.args[0]], 0], param(f"{n.target}.weight", m.weight)]
                     if m.bias is not None:
                         ins.append(param(f"{n.target}.bias", m.bias))
+                elif op == "conv2d":
+                    m = gm.get_submodule(n.target)
+                    st, pd = m.stride, m.padding
+                    if (m.groups != 1 or m.dilation != (1, 1) or isinstance(pd, str) or st[0] != st[1] or pd[0] != pd[1]
+                            or m.padding_mode != "zeros"):
+                        raise Unsupported(f"{n.name}: conv2d needs groups 1, dilation 1, square stride / zero padding")
+                    ins = [[ids[n.args[0]], 0], param(f"{n.target}.weight", m.weight)]
+                    if m.bias is not None:
+                        ins.append(param(f"{n.target}.bias", m.bias))
+                    attrs.update(stride=int(st[0]), padding=int(pd[0]))
                 elif op == "dropout":
                     m = gm.get_submodule(n.target) if n.op == "call_module" else None
                     attrs["p"] = m.p if m is not None else n.kwargs.get("p", n.args[1] if len(n.args) > 1 else 0.5)

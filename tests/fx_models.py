@@ -60,3 +60,21 @@ class ReluTaps(nn.Module):
             s = torch.relu(x).sum()
             loss = s if loss is None else loss + s
         return loss
+
+
+class ResConvNet(nn.Module):
+    """ResNet-style convolution blocks x + conv(relu(conv(relu(x)))) with a strided stem (§7
+    ResNet case; no batch norm): convolutions are compute-heavy (never recomputed), the ReLU maps are
+    the cheap feature maps."""
+
+    def __init__(self, c=16, blocks=2):
+        super().__init__()
+        self.stem = nn.Conv2d(3, c, 3, stride=2, padding=1)
+        self.c1 = nn.ModuleList([nn.Conv2d(c, c, 3, padding=1) for _ in range(blocks)])
+        self.c2 = nn.ModuleList([nn.Conv2d(c, c, 3, padding=1, bias=False) for _ in range(blocks)])
+
+    def forward(self, x):
+        x = self.stem(x)
+        for a, b in zip(self.c1, self.c2):
+            x = x + b(torch.relu(a(torch.relu(x))))
+        return torch.relu(x).sum()

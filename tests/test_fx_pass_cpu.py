@@ -6,7 +6,7 @@ import pytest
 import torch
 import torch.nn as nn
 
-from tests.fx_models import GatedNet, ResMLP, ReluTaps
+from tests.fx_models import GatedNet, ResMLP, ReluTaps, ResConvNet
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -69,3 +69,23 @@ def test_unsupported_ops_raise():
         X.EchoPlan(Conv(), (torch.randn(1, 2, 8),))
     with pytest.raises(X.Unsupported):
         X.EchoPlan(Bcast(), (torch.randn(4, 8),))
+
+
+def test_conv2d_graph_cpp_equals_oracle():
+    """conv2d (compute-heavy, its gradient reads input and weight): the traced ResNet-style CNN through
+    the C++ estimator equals the Python oracle (bytes, timeline, recompute flops) for every plan; Echo
+    never keeps more than the Baseline; the unmodified model's autograd keeps exactly the Baseline bytes."""
+    from oracle import footprint as F
+    from paper_1805_08899_b200 import fx_pass as X
+    m = ResConvNet(8, 2)
+    x = torch.randn(2, 3, 16, 16)
+    for st in ("baseline", "echo", "mirror"):
+        p = X.EchoPlan(m, (x,), strategy=st)
+        o = F.analyze(p.doc, {"strategy": st})
+        assert p.stash_bytes() == o["stash_bytes"] and p.report["timeline"] == o["timeline"], st
+        assert p.report["recompute_flops"] == o["recompute_flops"], st
+    e = X.EchoPlan(m, (x,)).stash_bytes()
+    b = X.EchoPlan(m, (x,), strategy="baseline").stash_bytes()
+    assert e <= b
+    _, saved = X.baseline_saved_bytes(m, x)
+    assert saved == b
