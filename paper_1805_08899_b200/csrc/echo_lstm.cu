@@ -89,8 +89,11 @@ static int step_vec(long elems, bool bf) {
 }
 
 static int grid_for(long threads, int block) {
+  static const long cap = [] {                 // grid-stride loops above the cap (ECHO_LSTM_GRIDCAP, CTAs)
+    const char* e = getenv("ECHO_LSTM_GRIDCAP");
+    return e && atol(e) > 0 ? atol(e) : 148L * 16;
+  }();
   long g = (threads + block - 1) / block;
-  const long cap = 148L * 16;
   return (int)(g < cap ? (g > 0 ? g : 1) : cap);
 }
 
