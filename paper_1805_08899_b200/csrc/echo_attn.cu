@@ -880,7 +880,7 @@ __device__ __forceinline__ void st_async_v2(uint32_t remote_addr, float x, float
 // identical to the backward's regenerated ones, with no __syncthreads / cluster barrier after the
 // start-up one that publishes the mbarrier initialisation.
 template <typename T>
-__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_tma(echo_attn_desc d, TmaGeo q,
+__global__ void __launch_bounds__(ATT_THREADS, sizeof(T) == 2 ? 8 : 1) attn_fwd_tma(echo_attn_desc d, TmaGeo q,
                                                             const __grid_constant__ CUtensorMap mK,
                                                             const __grid_constant__ CUtensorMap mH,
                                                             const T* __restrict__ qp, const T* __restrict__ v,
