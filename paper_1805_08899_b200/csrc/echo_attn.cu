@@ -1084,6 +1084,337 @@ __global__ void __launch_bounds__(ATT_THREADS, sizeof(T) == 2 ? 8 : 1) attn_fwd_
   }
 }
 
+// ---- a5, persistent row-streaming variant (large B).  One CTA (two per SM)
+// walks rows b = blockIdx.x, + gridDim.x, ...; a producer warp streams each row's Kp positions and
+// then its H_s positions through a ring of shared stages (TMA, R positions x all C column slices
+// per stage, full / empty mbarriers), so HBM reads run continuously under the score, softmax and
+// ctx phases of the previous stages -- no cluster, no DSMEM, no per-row launch / start-up latency.
+// The arithmetic is attn_fwd_tma's, element for element: lane l of a warp evaluates the same four
+// columns r*Wb + 4l of every slice r with the same FMA order, the slice partials are the same
+// warp_sum trees (reduce_scatter, bitwise equal), added in rank order from 0; the softmax and the
+// s-mod-4 ctx accumulators are the same code -- so ctx / Z / alpha are bit-identical to the cluster
+// kernel's and to a6's regenerated ones (tests/test_gpu_attention.py checks both).
+constexpr int ROWS_CWARPS = 8;                                // consumer warps
+constexpr int ROWS_THREADS = (ROWS_CWARPS + 1) * 32;          // + one producer warp
+constexpr int ROWS_MAXST = 8;
+struct RowGeo {
+  int C, Wb, WHb, R, nst;       // slices (as TmaGeo), positions per stage (8 | 16 | 32), ring stages
+  uint32_t sub, stage;          // bytes per slice sub-tile (128-aligned) and per stage (+ the qp row)
+};
+__device__ __forceinline__ void bar_sync_consumers() { asm volatile("bar.sync 1, %0;\n" ::"n"(ROWS_CWARPS * 32) : "memory"); }
+
+// (with a suspend-time hint: a waiting thread sleeps until the phase completes instead of re-polling)
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+// bf16x2 word -> two floats (exact: a bf16 is the high half of its fp32)
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+// ring position: slot and phase advance together (no division by the stage count)
+struct RingPos {
+  int slot;
+  uint32_t phase;
+  __device__ __forceinline__ void next(int nst) {
+    if (++slot == nst) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+template <typename T, int CT, bool STASH>
+__global__ void __launch_bounds__(ROWS_THREADS, 2) attn_fwd_rows(echo_attn_desc d, RowGeo q,
+                                                                   const __grid_constant__ CUtensorMap mK,
+                                                                   const __grid_constant__ CUtensorMap mH,
+                                                                   const T* __restrict__ qp, const T* __restrict__ v,
+                                                                   const int32_t* __restrict__ src_len, T* __restrict__ ctx,
+                                                                   T* __restrict__ Z_st, float* __restrict__ alpha_st) {
+  pdl_wait();
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t full[ROWS_MAXST], empty[ROWS_MAXST];
+  __shared__ float xs[256 * CT];                              // slice partials [s][slice] of the current row
+  __shared__ __align__(16) float al_s[260];                   // alpha of the current row (+ tail-read pad)
+  const int A = d.A, Ts = d.Ts, Hk = d.Hk, Wb = q.Wb, WHb = q.WHb, R = q.R, NST = q.nst;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    for (int k = 0; k < NST; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], ROWS_CWARPS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty), sm0 = smem_u32(smraw);
+  if (w == ROWS_CWARPS) {                                     // ---- producer (one thread)
+    if (lane) return;
+    prefetch_tmap(&mK);
+    prefetch_tmap(&mH);
+    const uint64_t pol = l2_policy(false);
+    RingPos rp{0, 0u};
+    for (int b = blockIdx.x; b < d.B; b += gridDim.x) {
+      const int n = row_len(src_len, b, Ts), nch = (n + R - 1) / R;
+      for (int pass = 0; pass < 2; ++pass) {
+        const int X = pass ? Hk : A, Wx = pass ? WHb : Wb;
+        const CUtensorMap* m = pass ? &mH : &mK;
+        for (int k = 0; k < nch; ++k, rp.next(NST)) {
+          mbar_wait_u32(empty0 + 8u * rp.slot, rp.phase ^ 1u);
+          unsigned char* st = smraw + (size_t)rp.slot * q.stage;
+          const bool first = pass == 0 && k == 0;
+          uint32_t bytes = first ? (uint32_t)(A * sizeof(T)) : 0u;
+#pragma unroll
+          for (int r = 0; r < CT; ++r)
+            if (r * Wx < X) bytes += (uint32_t)(R * Wx * sizeof(T));
+          mbar_expect_tx(&full[rp.slot], bytes);
+#pragma unroll
+          for (int r = 0; r < CT; ++r)
+            if (r * Wx < X) tma_load_3d_hint(st + r * q.sub, m, r * Wx, b, k * R, &full[rp.slot], pol);
+          if (first) bulk_load(st + CT * q.sub, qp + (long)b * A, (uint32_t)(A * sizeof(T)), &full[rp.slot]);
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers (warps 0..7)
+  bool act[CT];
+  uint32_t lk[CT];                                            // lane byte offset in a slice row (0 if inactive)
+  float vr[CT][4];
+#pragma unroll
+  for (int r = 0; r < CT; ++r) {
+    const int a0 = min(A, r * Wb), W = min(A, a0 + Wb) - a0;
+    act[r] = lane < W / 4;
+    lk[r] = act[r] ? (uint32_t)(lane * 4 * sizeof(T)) : 0u;
+    if (act[r]) lds4(v + a0 + lane * 4, vr[r]);              // (lds4: a plain 4-element load, here from global)
+    else vr[r][0] = vr[r][1] = vr[r][2] = vr[r][3] = 0.0f;
+  }
+  constexpr int LG = CT == 1 ? 0 : CT == 2 ? 1 : CT == 4 ? 2 : 3;
+  constexpr bool PAIRS = CT <= 4;                             // two positions per reduce_scatter (<= 8 slots)
+  const uint32_t rowK = (uint32_t)(Wb * sizeof(T)), rowH = (uint32_t)(WHb * sizeof(T));
+  // ctx: thread t owns column pairs t and t + 256 (two adjacent columns each)
+  const int NPJ = (Hk / 2 + ROWS_CWARPS * 32 - 1) / (ROWS_CWARPS * 32);   // <= 2
+  uint32_t off[2];
+  bool pok[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int c = 2 * (tid + j * ROWS_CWARPS * 32);
+    pok[j] = j < NPJ && c < Hk;
+    const int r = pok[j] ? c / WHb : 0, cc = pok[j] ? c - r * WHb : 0;
+    off[j] = (uint32_t)r * q.sub + (uint32_t)(cc * sizeof(T));
+  }
+  RingPos rp{0, 0u};
+  // xs / al_s reuse across rows: a warp writes row b+1's xs only after the second barrier of row b (warp
+  // 0's softmax has read row b's xs), and warp 0 writes row b+1's alpha only after the first barrier of
+  // row b+1 (every warp has finished row b's ctx)
+  for (int b = blockIdx.x; b < d.B; b += gridDim.x) {
+    const int n = row_len(src_len, b, Ts), nch = (n + R - 1) / R;
+    uint2 q2[CT];
+    float qr[CT][4];
+    // slice partial of position i of the stage at sb: attn_fwd_tma's per-lane arithmetic, evaluated
+    // branch-free (an inactive lane reads its slice's first element and contributes 0, as it does there)
+    auto part = [&](uint32_t sb, int r, int i, int s) -> float {
+      const uint32_t a = sb + (uint32_t)r * q.sub + (uint32_t)i * rowK + lk[r];
+      float acc = 0.0f;
+      if constexpr (sizeof(T) == 2) {
+        uint32_t k0, k1;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(k0), "=r"(k1) : "r"(a));
+        const __nv_bfloat162 za = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&q2[r].x),
+                                          *reinterpret_cast<const __nv_bfloat162*>(&k0));
+        const __nv_bfloat162 zb = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&q2[r].y),
+                                          *reinterpret_cast<const __nv_bfloat162*>(&k1));
+        const uint32_t ua = *reinterpret_cast<const uint32_t*>(&za), ub = *reinterpret_cast<const uint32_t*>(&zb);
+        const float2 ea = att_tanh2_bf16(bf2_to_f2(ua)), eb = att_tanh2_bf16(bf2_to_f2(ub));
+        acc = __fmaf_rn(ea.x, vr[r][0], acc);
+        acc = __fmaf_rn(ea.y, vr[r][1], acc);
+        acc = __fmaf_rn(eb.x, vr[r][2], acc);
+        acc = __fmaf_rn(eb.y, vr[r][3], acc);
+        if constexpr (STASH) {
+          if (act[r]) *reinterpret_cast<uint2*>(Z_st + ((long)b * Ts + s) * A + r * Wb + lane * 4) = make_uint2(ua, ub);
+        }
+      } else {
+        float4 kv;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(kv.x), "=f"(kv.y), "=f"(kv.z), "=f"(kv.w) : "r"(a));
+        const float kz4[4] = {kv.x, kv.y, kv.z, kv.w};
+        float z[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          z[c] = z_of<T>(qr[r][c], kz4[c], true);
+          acc = __fmaf_rn(att_tanh<T>(z[c]), vr[r][c], acc);
+        }
+        if constexpr (STASH) {
+          if (act[r]) stg4(Z_st + ((long)b * Ts + s) * A + r * Wb + lane * 4, z);
+        }
+      }
+      return act[r] ? acc : 0.0f;
+    };
+    // phase 1: per-slice warp sums (reduce_scatter: bitwise warp_sum) into xs[s][r]
+    for (int k = 0; k < nch; ++k, rp.next(NST)) {
+      mbar_wait_u32(full0 + 8u * rp.slot, rp.phase);
+      const uint32_t sb = sm0 + (uint32_t)rp.slot * q.stage;
+      if (k == 0) {
+        const T* qrow = reinterpret_cast<const T*>(smraw + (size_t)rp.slot * q.stage + CT * q.sub);
+#pragma unroll
+        for (int r = 0; r < CT; ++r) {
+          if (act[r]) {
+            lds4(qrow + r * Wb + lane * 4, qr[r]);
+            if constexpr (sizeof(T) == 2) q2[r] = *reinterpret_cast<const uint2*>(qrow + r * Wb + lane * 4);
+          } else {
+            q2[r] = make_uint2(0u, 0u);
+            qr[r][0] = qr[r][1] = qr[r][2] = qr[r][3] = 0.0f;
+          }
+        }
+      }
+      const int s1 = min(n, (k + 1) * R);
+      int s = k * R + w;
+      if constexpr (PAIRS) {
+        for (; s + ROWS_CWARPS < s1; s += 2 * ROWS_CWARPS) {
+          float p[2 * CT];
+#pragma unroll
+          for (int r = 0; r < CT; ++r) {
+            p[r] = part(sb, r, s - k * R, s);
+            p[CT + r] = part(sb, r, s + ROWS_CWARPS - k * R, s + ROWS_CWARPS);
+          }
+          const float ps = reduce_scatter<2 * CT>(p, lane);
+          constexpr int LG2 = LG + 1;
+          const int g = lane >> (5 - LG2);                    // slot g = position (g / CT), slice g % CT
+          if ((lane & ((32 >> LG2) - 1)) == 0) xs[(s + (g / CT) * ROWS_CWARPS) * CT + g % CT] = ps;
+        }
+      }
+      for (; s < s1; s += ROWS_CWARPS) {
+        float p[CT];
+#pragma unroll
+        for (int r = 0; r < CT; ++r) p[r] = part(sb, r, s - k * R, s);
+        if constexpr (CT == 1) {
+          const float ps = warp_sum(p[0]);
+          if (lane == 0) xs[s] = ps;
+        } else {
+          const float ps = reduce_scatter<CT>(p, lane);
+          if ((lane & ((32 >> LG) - 1)) == 0) xs[s * CT + (lane >> (5 - LG))] = ps;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_u32(empty0 + 8u * rp.slot);
+    }
+    if constexpr (STASH) {                                    // masked positions: zeros
+      float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int s = n + w; s < Ts; s += ROWS_CWARPS)
+        for (int c4 = lane; c4 < A / 4; c4 += 32) stg4(Z_st + ((long)b * Ts + s) * A + c4 * 4, z);
+    }
+    bar_sync_consumers();                                     // every partial of row b is in xs
+    // warp 0: scores in rank order from 0 (the xpart gather) and the softmax (attn_fwd_tma's register
+    // code, same operations and order) -> al_s; the other warps wait at the second barrier
+    if (w == 0) {
+      float scr[8];
+      float m = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int s = lane + 32 * k;
+        float x = 0.0f;
+        if (s < n) {
+#pragma unroll
+          for (int r = 0; r < CT; ++r) x = __fadd_rn(x, xs[s * CT + r]);
+          m = fmaxf(m, x);
+        }
+        scr[k] = x;
+      }
+      m = warp_max(m);
+      float l = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int s = lane + 32 * k;
+        scr[k] = s < n ? expf(__fsub_rn(scr[k], m)) : 0.0f;
+        if (s < n) l = __fadd_rn(l, scr[k]);
+      }
+      l = warp_sum(l);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int s = lane + 32 * k;
+        const float a = s < n ? __fdiv_rn(scr[k], l) : 0.0f;
+        al_s[s] = a;
+        if (STASH && s < Ts) alpha_st[(long)b * Ts + s] = a;
+      }
+    }
+    bar_sync_consumers();                                     // alpha of row b is in al_s
+    // ctx (ctx_columns' accumulators: one per s mod 4 and column, combined (a0 + a1) + (a2 + a3));
+    // FFMA2 on the column pair = the two scalar FMAs
+    float2 acc[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][e] = make_float2(0.0f, 0.0f);
+    auto hld = [&](uint32_t a) -> float2 {
+      if constexpr (sizeof(T) == 2) {
+        uint32_t u;
+        asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(u) : "r"(a));
+        return bf2_to_f2(u);
+      } else {
+        float2 x;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(x.x), "=f"(x.y) : "r"(a));
+        return x;
+      }
+    };
+    const uint32_t al0 = smem_u32(al_s);
+    {
+      for (int s0 = 0; s0 < n; s0 += R, rp.next(NST)) {       // one stage per s0
+        mbar_wait_u32(full0 + 8u * rp.slot, rp.phase);
+        const uint32_t sb = sm0 + (uint32_t)rp.slot * q.stage;
+        const int ie = min(R, n - s0);
+        if (ie == R) {                                        // full stage: no per-position guards
+#pragma unroll 2
+          for (int i = 0; i < R; i += 4) {
+            float al[4];
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(al[0]), "=f"(al[1]), "=f"(al[2]), "=f"(al[3])
+                         : "r"(al0 + 4u * (uint32_t)(s0 + i)));
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              if (pok[j]) {
+                float2 x[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x[e] = hld(sb + off[j] + (uint32_t)(i + e) * rowH);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[j][e] = __ffma2_rn(make_float2(al[e], al[e]), x[e], acc[j][e]);
+              }
+          }
+        } else {
+          for (int i = 0; i < ie; i += 4) {
+            float al[4];
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(al[0]), "=f"(al[1]), "=f"(al[2]), "=f"(al[3])
+                         : "r"(al0 + 4u * (uint32_t)(s0 + i)));
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              if (pok[j]) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (i + e < ie) acc[j][e] = __ffma2_rn(make_float2(al[e], al[e]), hld(sb + off[j] + (uint32_t)(i + e) * rowH), acc[j][e]);
+              }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(empty0 + 8u * rp.slot);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (pok[j]) {
+        const float ya = St<T>::round(__fadd_rn(__fadd_rn(acc[j][0].x, acc[j][1].x), __fadd_rn(acc[j][2].x, acc[j][3].x)));
+        const float yb = St<T>::round(__fadd_rn(__fadd_rn(acc[j][0].y, acc[j][1].y), __fadd_rn(acc[j][2].y, acc[j][3].y)));
+        T* o = ctx + (long)b * Hk + 2 * (tid + j * ROWS_CWARPS * 32);
+        o[0] = from_f<T>(ya);
+        o[1] = from_f<T>(yb);
+      }
+  }
+}
+
 // phase-4 work split: G = (W + WH)/4 column groups of four; P = ATT_THREADS / G position phases
 static __host__ __device__ __forceinline__ int tma_phases(int W, int WH) { return ATT_THREADS / ((W + WH) / 4); }
 
@@ -1549,6 +1880,43 @@ static bool tma_params(const echo_attn_desc* d, int* C, int* rows, size_t* smem_
   return true;
 }
 
+// a5 row-streaming variant (attn_fwd_rows): ECHO_A5_ROWS=0 never, 1 always (where the shape fits),
+// default: when the launch has at least two rows per SM.  Read on every call (tests switch it).
+static int a5_rows_mode() {
+  const char* e = getenv("ECHO_A5_ROWS");
+  return e && (*e == '0' || *e == '1') ? *e - '0' : 2;
+}
+static int sm_count() {
+  static const int n = [] {
+    int dev = 0, s = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    return s > 0 ? s : 148;
+  }();
+  return n;
+}
+// stage = R positions x every column slice (R in {8, 16, 32}: R | 32 keeps a stage inside one
+// 32-position softmax register) + the row's qp vector; 16-32 KB per stage, ~100 KB of ring
+static bool rows_params(const echo_attn_desc* d, RowGeo* g, size_t* smem) {
+  if (d->A > 1024 || d->Hk > 1024 || d->Ts > 256) return false;
+  const size_t es = d->dtype == ECHO_FP32 ? 4 : 2;
+  const int C = tma_cluster(d->A, d->Hk);
+  const int Wb = tma_width(d->A, C), WHb = tma_width(d->Hk, C);
+  const size_t mw = (size_t)(Wb > WHb ? Wb : WHb);
+  int R = (size_t)C * al128h(16 * mw * es) <= 32768 ? 16 : 8;   // 16 positions per stage where <= 32 KB
+  if ((size_t)C * al128h(32 * mw * es) <= 16384) R = 32;
+  g->C = C;
+  g->Wb = Wb;
+  g->WHb = WHb;
+  g->R = R;
+  g->sub = (uint32_t)al128h((size_t)R * mw * es);
+  g->stage = (uint32_t)((size_t)C * g->sub + al128h((size_t)d->A * es));
+  int nst = (int)((100 * 1024) / g->stage);
+  g->nst = nst < 2 ? 2 : (nst > ROWS_MAXST ? ROWS_MAXST : nst);
+  *smem = (size_t)g->nst * g->stage;
+  return *smem <= 200 * 1024;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1616,6 +1984,24 @@ static echo_status set_smem(const void* kern, size_t bytes, const char* fn) {
   return ECHO_OK;
 }
 
+template <typename T>
+static echo_status launch_rows(const char* fn, const echo_attn_desc* d, const RowGeo& g, size_t smem,
+                               const CUtensorMap& mK, const CUtensorMap& mH, const void* qp, const void* v,
+                               const int32_t* src_len, void* ctx, void* E_st, float* alpha_st, cudaStream_t st) {
+  decltype(&attn_fwd_rows<T, 1, false>) k;
+  if (E_st) k = g.C == 1 ? attn_fwd_rows<T, 1, true> : g.C == 2 ? attn_fwd_rows<T, 2, true>
+              : g.C == 4 ? attn_fwd_rows<T, 4, true> : attn_fwd_rows<T, 8, true>;
+  else k = g.C == 1 ? attn_fwd_rows<T, 1, false> : g.C == 2 ? attn_fwd_rows<T, 2, false>
+         : g.C == 4 ? attn_fwd_rows<T, 4, false> : attn_fwd_rows<T, 8, false>;
+  echo_status s = set_smem((const void*)k, smem, fn);
+  if (s) return s;
+  const int grid = d->B < 2 * sm_count() ? d->B : 2 * sm_count();
+  cudaError_t e = launch(k, dim3(grid, 1, 1), dim3(ROWS_THREADS, 1, 1), smem, st, 0, *d, g, mK, mH, (const T*)qp,
+                         (const T*)v, src_len, (T*)ctx, (T*)E_st, alpha_st);
+  if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
+  return check_launch(fn);
+}
+
 }  // namespace echo
 
 using namespace echo;
@@ -1645,6 +2031,14 @@ extern "C" echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, co
   TmaGeo geo;
   CUtensorMap mK, mH;
   const bool bfd = d->dtype == ECHO_BF16;
+  RowGeo rg;
+  size_t rsm;
+  const int rmode = a5_rows_mode();
+  if (rmode && (rmode == 1 || d->B >= 2 * sm_count()) && rows_params(d, &rg, &rsm) &&
+      map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, rg.Wb, rg.R) &&
+      map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, rg.WHb, rg.R))
+    return bfd ? launch_rows<__nv_bfloat16>(fn, d, rg, rsm, mK, mH, qp, v, src_len, ctx, E_st, alpha_st, st)
+               : launch_rows<float>(fn, d, rg, rsm, mK, mH, qp, v, src_len, ctx, E_st, alpha_st, st);
   if (tma_params(d, &tC, &tR, &sf, &sb, &geo) &&
       map3d(&mK, Kp, bfd, d->A, d->B, d->Ts, d->kp_stride_b, d->kp_stride_s, tma_width(d->A, tC), tR) &&
       map3d(&mH, Hs, bfd, d->Hk, d->B, d->Ts, d->hs_stride_b, d->hs_stride_s, tma_width(d->Hk, tC), tR)) {

@@ -56,7 +56,9 @@ def _run_attn(abi, d, storage, mode, layout):
                                                (128, 50, 512, 512, "sbk"), (3, 700, 256, 64, "bsk"),
                                                (1, 1, 8, 8, "bsk"), (2, 256, 64, 32, "sbk"), (2, 257, 64, 32, "sbk"),
                                                (3, 13, 1024, 1024, "sbk"), (4, 9, 24, 1000, "bsk")])
-def test_attention_parity_and_bit_identity(storage, B, Ts, A, Hk, layout, cuda_dev):
+@pytest.mark.parametrize("rows", ["0", "1"], ids=["a5-cluster", "a5-rows"])
+def test_attention_parity_and_bit_identity(storage, B, Ts, A, Hk, layout, rows, cuda_dev, monkeypatch):
+    monkeypatch.setenv("ECHO_A5_ROWS", rows)                      # both a5 kernels (same arithmetic)
     abi = _abi()
     d = mlp_attn_inputs(31, B, Ts, A, Hk, storage, lengths="random")
     ref = OA.backward(*(np.asarray(d[k], np.float64) for k in ("qp", "Kp", "v", "Hs", "dctx")), src_len=d["src_len"])
@@ -72,6 +74,41 @@ def test_attention_parity_and_bit_identity(storage, B, Ts, A, Hk, layout, cuda_d
     assert bits_equal(s["ctx"], r["ctx"])
     for k in ("dqp", "dKp", "dHs", "dv"):
         assert bits_equal(s[k], r[k]), k
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("B,Ts,A,Hk", [(600, 50, 512, 512), (333, 3, 512, 512), (300, 256, 64, 32), (297, 13, 1024, 1024),
+                                       (400, 9, 24, 1000), (1, 1, 8, 8)])
+def test_a5_rows_equals_cluster_bitwise(storage, B, Ts, A, Hk, cuda_dev, monkeypatch):
+    """The persistent row-streaming a5 (attn_fwd_rows, several rows per CTA through the stage ring) and
+    the cluster a5 (attn_fwd_tma) give the same ctx / Z / alpha bits, in both modes, ragged lengths."""
+    abi = _abi()
+    dt = abi.FP32 if storage == "fp32" else abi.BF16
+    sd = torch.float32 if storage == "fp32" else torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(B * 3 + Ts)
+    Kp = (torch.randn(Ts, B, A, device="cuda", generator=g) * 0.5).to(sd)
+    Hs = torch.randn(Ts, B, Hk, device="cuda", generator=g).to(sd)
+    qp = (torch.randn(B, A, device="cuda", generator=g) * 0.5).to(sd)
+    v = (torch.randn(A, device="cuda", generator=g) * 0.2).to(sd)
+    sl = torch.randint(1, Ts + 1, (B,), device="cuda", generator=g).to(torch.int32)
+    for mode in (abi.STASH, abi.RECOMPUTE):
+        st = mode == abi.STASH
+        desc = abi.AttnDesc(B, Ts, A, Hk, dt, mode, A, B * A, Hk, B * Hk)
+        out = {}
+        for rows in ("0", "1"):
+            monkeypatch.setenv("ECHO_A5_ROWS", rows)
+            ctx = torch.full((B, Hk), float("nan"), device="cuda").to(sd)
+            Z = torch.full((B, Ts, A), float("nan"), device="cuda").to(sd) if st else None
+            al = torch.full((B, Ts), float("nan"), device="cuda") if st else None
+            abi.echo_attn_fwd(desc, qp, Kp, v, Hs, sl, ctx, Z, al)
+            torch.cuda.synchronize()
+            out[rows] = (ctx, Z, al)
+        for x, y in zip(out["0"], out["1"]):
+            if x is not None:
+                assert bits_equal(x, y)
+        if st:
+            rs = out["1"][2].sum(1)
+            assert torch.allclose(rs, torch.ones_like(rs), atol=1e-5)
 
 
 def test_attention_masked_rows_untouched(cuda_dev):
