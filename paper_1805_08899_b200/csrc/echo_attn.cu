@@ -1094,13 +1094,21 @@ __global__ void __launch_bounds__(ATT_THREADS, sizeof(T) == 2 ? 8 : 1) attn_fwd_
 // warp_sum trees (reduce_scatter, bitwise equal), added in rank order from 0; the softmax and the
 // s-mod-4 ctx accumulators are the same code -- so ctx / Z / alpha are bit-identical to the cluster
 // kernel's and to a6's regenerated ones (tests/test_gpu_attention.py checks both).
-constexpr int ROWS_CWARPS = 8;                                // consumer warps
+#ifndef ECHO_ROWS_CWARPS
+#define ECHO_ROWS_CWARPS 4
+#endif
+constexpr int ROWS_CWARPS = ECHO_ROWS_CWARPS;                 // consumer warps
 constexpr int ROWS_THREADS = (ROWS_CWARPS + 1) * 32;          // + one producer warp
+constexpr int ROWS_PER_SM = ROWS_CWARPS == 4 ? 4 : 2;         // resident CTAs per SM
+constexpr int ROWS_MAXPJ = 4;                                 // ctx column pairs per thread (Hk <= 8 * 32 * CWARPS)
 constexpr int ROWS_MAXST = 8;
 struct RowGeo {
   int C, Wb, WHb, R, nst;       // slices (as TmaGeo), positions per stage (8 | 16 | 32), ring stages
   uint32_t sub, stage;          // bytes per slice sub-tile (128-aligned) and per stage (+ the qp row)
 };
+static __host__ __device__ __forceinline__ size_t rows_tail_bytes(int Ts, int C) {   // xs + al_s
+  return 4 * (size_t)(((Ts * C + 3) & ~3) + Ts + 8);
+}
 __device__ __forceinline__ void bar_sync_consumers() { asm volatile("bar.sync 1, %0;\n" ::"n"(ROWS_CWARPS * 32) : "memory"); }
 
 // (with a suspend-time hint: a waiting thread sleeps until the phase completes instead of re-polling)
@@ -1135,7 +1143,7 @@ struct RingPos {
 };
 
 template <typename T, int CT, bool STASH>
-__global__ void __launch_bounds__(ROWS_THREADS, 2) attn_fwd_rows(echo_attn_desc d, RowGeo q,
+__global__ void __launch_bounds__(ROWS_THREADS, ROWS_PER_SM) attn_fwd_rows(echo_attn_desc d, RowGeo q,
                                                                    const __grid_constant__ CUtensorMap mK,
                                                                    const __grid_constant__ CUtensorMap mH,
                                                                    const T* __restrict__ qp, const T* __restrict__ v,
@@ -1144,8 +1152,9 @@ __global__ void __launch_bounds__(ROWS_THREADS, 2) attn_fwd_rows(echo_attn_desc 
   pdl_wait();
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[ROWS_MAXST], empty[ROWS_MAXST];
-  __shared__ float xs[256 * CT];                              // slice partials [s][slice] of the current row
-  __shared__ __align__(16) float al_s[260];                   // alpha of the current row (+ tail-read pad)
+  // after the ring: slice partials xs[s][slice] and alpha al_s[s] of the current row (+ tail-read pad)
+  float* xs = reinterpret_cast<float*>(smraw + (size_t)q.nst * q.stage);
+  float* al_s = xs + ((d.Ts * CT + 3) & ~3);
   const int A = d.A, Ts = d.Ts, Hk = d.Hk, Wb = q.Wb, WHb = q.WHb, R = q.R, NST = q.nst;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
@@ -1202,11 +1211,11 @@ __global__ void __launch_bounds__(ROWS_THREADS, 2) attn_fwd_rows(echo_attn_desc 
   constexpr bool PAIRS = CT <= 4;                             // two positions per reduce_scatter (<= 8 slots)
   const uint32_t rowK = (uint32_t)(Wb * sizeof(T)), rowH = (uint32_t)(WHb * sizeof(T));
   // ctx: thread t owns column pairs t and t + 256 (two adjacent columns each)
-  const int NPJ = (Hk / 2 + ROWS_CWARPS * 32 - 1) / (ROWS_CWARPS * 32);   // <= 2
-  uint32_t off[2];
-  bool pok[2];
+  const int NPJ = (Hk / 2 + ROWS_CWARPS * 32 - 1) / (ROWS_CWARPS * 32);   // <= ROWS_MAXPJ
+  uint32_t off[ROWS_MAXPJ];
+  bool pok[ROWS_MAXPJ];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < ROWS_MAXPJ; ++j) {
     const int c = 2 * (tid + j * ROWS_CWARPS * 32);
     pok[j] = j < NPJ && c < Hk;
     const int r = pok[j] ? c / WHb : 0, cc = pok[j] ? c - r * WHb : 0;
@@ -1340,16 +1349,16 @@ __global__ void __launch_bounds__(ROWS_THREADS, 2) attn_fwd_rows(echo_attn_desc 
       for (int k = 0; k < 8; ++k) {
         const int s = lane + 32 * k;
         const float a = s < n ? __fdiv_rn(scr[k], l) : 0.0f;
-        al_s[s] = a;
+        if (s < Ts + 8) al_s[s] = a;
         if (STASH && s < Ts) alpha_st[(long)b * Ts + s] = a;
       }
     }
     bar_sync_consumers();                                     // alpha of row b is in al_s
     // ctx (ctx_columns' accumulators: one per s mod 4 and column, combined (a0 + a1) + (a2 + a3));
     // FFMA2 on the column pair = the two scalar FMAs
-    float2 acc[2][4];
+    float2 acc[ROWS_MAXPJ][4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < ROWS_MAXPJ; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[j][e] = make_float2(0.0f, 0.0f);
     auto hld = [&](uint32_t a) -> float2 {
@@ -1376,7 +1385,7 @@ __global__ void __launch_bounds__(ROWS_THREADS, 2) attn_fwd_rows(echo_attn_desc 
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(al[0]), "=f"(al[1]), "=f"(al[2]), "=f"(al[3])
                          : "r"(al0 + 4u * (uint32_t)(s0 + i)));
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < ROWS_MAXPJ; ++j)
               if (pok[j]) {
                 float2 x[4];
 #pragma unroll
@@ -1391,7 +1400,7 @@ __global__ void __launch_bounds__(ROWS_THREADS, 2) attn_fwd_rows(echo_attn_desc 
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(al[0]), "=f"(al[1]), "=f"(al[2]), "=f"(al[3])
                          : "r"(al0 + 4u * (uint32_t)(s0 + i)));
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < ROWS_MAXPJ; ++j)
               if (pok[j]) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
@@ -1404,7 +1413,7 @@ __global__ void __launch_bounds__(ROWS_THREADS, 2) attn_fwd_rows(echo_attn_desc 
       }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < ROWS_MAXPJ; ++j)
       if (pok[j]) {
         const float ya = St<T>::round(__fadd_rn(__fadd_rn(acc[j][0].x, acc[j][1].x), __fadd_rn(acc[j][2].x, acc[j][3].x)));
         const float yb = St<T>::round(__fadd_rn(__fadd_rn(acc[j][0].y, acc[j][1].y), __fadd_rn(acc[j][2].y, acc[j][3].y)));
@@ -1903,17 +1912,22 @@ static bool rows_params(const echo_attn_desc* d, RowGeo* g, size_t* smem) {
   const int C = tma_cluster(d->A, d->Hk);
   const int Wb = tma_width(d->A, C), WHb = tma_width(d->Hk, C);
   const size_t mw = (size_t)(Wb > WHb ? Wb : WHb);
-  int R = (size_t)C * al128h(16 * mw * es) <= 32768 ? 16 : 8;   // 16 positions per stage where <= 32 KB
-  if ((size_t)C * al128h(32 * mw * es) <= 16384) R = 32;
+  // per-CTA shared budget for ROWS_PER_SM resident CTAs (228 KB per SM, 1 KB reserved per CTA)
+  const size_t tail = rows_tail_bytes(d->Ts, C);
+  const size_t budget = 228 * 1024 / ROWS_PER_SM - 1024 - 256 - tail;
+  auto stage_of = [&](int R) { return (size_t)C * al128h((size_t)R * mw * es) + al128h((size_t)d->A * es); };
+  int R = 8;                                                  // largest R in {8, 16, 32} with >= 3 stages
+  if (3 * stage_of(16) <= budget) R = 16;
+  if (3 * stage_of(32) <= budget) R = 32;
   g->C = C;
   g->Wb = Wb;
   g->WHb = WHb;
   g->R = R;
   g->sub = (uint32_t)al128h((size_t)R * mw * es);
-  g->stage = (uint32_t)((size_t)C * g->sub + al128h((size_t)d->A * es));
-  int nst = (int)((100 * 1024) / g->stage);
+  g->stage = (uint32_t)stage_of(R);
+  int nst = (int)(budget / g->stage);
   g->nst = nst < 2 ? 2 : (nst > ROWS_MAXST ? ROWS_MAXST : nst);
-  *smem = (size_t)g->nst * g->stage;
+  *smem = (size_t)g->nst * g->stage + tail;
   return *smem <= 200 * 1024;
 }
 
@@ -1995,7 +2009,12 @@ static echo_status launch_rows(const char* fn, const echo_attn_desc* d, const Ro
          : g.C == 4 ? attn_fwd_rows<T, 4, false> : attn_fwd_rows<T, 8, false>;
   echo_status s = set_smem((const void*)k, smem, fn);
   if (s) return s;
-  const int grid = d->B < 2 * sm_count() ? d->B : 2 * sm_count();
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, ROWS_THREADS, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  const int grid = d->B < occ * sm_count() ? d->B : occ * sm_count();
   cudaError_t e = launch(k, dim3(grid, 1, 1), dim3(ROWS_THREADS, 1, 1), smem, st, 0, *d, g, mK, mH, (const T*)qp,
                          (const T*)v, src_len, (T*)ctx, (T*)E_st, alpha_st);
   if (e != cudaSuccess) return fail(ECHO_ERR_CUDA, "%s: launch: %s", fn, cudaGetErrorString(e));
