@@ -497,17 +497,7 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) { mbar_wait_bounded(smem_u32(bar), phase); }
 
 struct Slice {
   int C, r, a0, a1, h0, h1;   // this CTA's column ranges [a0, a1) of A and [h0, h1) of Hk
@@ -1112,17 +1102,7 @@ static __host__ __device__ __forceinline__ size_t rows_tail_bytes(int Ts, int C)
 __device__ __forceinline__ void bar_sync_consumers() { asm volatile("bar.sync 1, %0;\n" ::"n"(ROWS_CWARPS * 32) : "memory"); }
 
 // (with a suspend-time hint: a waiting thread sleeps until the phase completes instead of re-polling)
-__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(phase)
-      : "memory");
-}
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t phase) { mbar_wait_bounded<10000000>(bar, phase); }
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }

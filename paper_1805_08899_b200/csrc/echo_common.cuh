@@ -44,6 +44,53 @@ inline bool pdl_enabled() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
+// ------------------------------------------------------------------ bounded mbarrier waits
+// Every mbarrier wait in libecho (TMA stage-in, st.async exchange, tcgen05 commit) goes through
+// mbar_wait_bounded: the fast path is one try_wait; a phase still incomplete after ECHO_WAIT_NS of
+// global time (a kernel bug: a lost arrive or a short transaction count) traps (no printf: it would
+// cost registers in the launch-bounded kernels), so the launch fails with cudaErrorLaunchFailure instead of spinning until an external
+// timeout kills the process.  Correct launches never get near the bound (the longest wait is a
+// TMA stage-in or a peer CTA's exchange, microseconds).
+#ifndef ECHO_WAIT_NS
+#define ECHO_WAIT_NS 4000000000ull   // 4 s
+#endif
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+// SUSPEND_NS > 0: try_wait with a suspend-time hint (the thread sleeps until the phase completes or
+// the hint expires instead of re-polling)
+template <uint32_t SUSPEND_NS>
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  if (SUSPEND_NS > 0)
+    asm volatile(
+        "{\n.reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase), "n"(SUSPEND_NS)
+        : "memory");
+  else
+    asm volatile(
+        "{\n.reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  return ok != 0;
+}
+template <uint32_t SUSPEND_NS = 0>
+__device__ __forceinline__ void mbar_wait_bounded(uint32_t bar, uint32_t phase) {
+  if (mbar_try<SUSPEND_NS>(bar, phase)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try<SUSPEND_NS>(bar, phase)) {
+    if (globaltimer_ns() - t0 > ECHO_WAIT_NS) __trap();
+  }
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
                           Args&&... args) {

@@ -723,13 +723,7 @@ __device__ __forceinline__ void tc_mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void tc_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc_smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void tc_mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n}\n" ::"r"(tc_smem_u32(bar)), "r"(phase)
-      : "memory");
-}
+__device__ __forceinline__ void tc_mbar_wait(uint64_t* bar, uint32_t phase) { mbar_wait_bounded(tc_smem_u32(bar), phase); }
 __device__ __forceinline__ void tc_tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
