@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(ATT_THREADS, sizeof(T) == 2 ? 8 : 1) attn_fwd_
   }
 }
 
-// ---- a5, persistent row-streaming variant (large B).  One CTA (two per SM)
+// ---- a5, persistent row-streaming variant (large B).  One CTA (ROWS_PER_SM per SM)
 // walks rows b = blockIdx.x, + gridDim.x, ...; a producer warp streams each row's Kp positions and
 // then its H_s positions through a ring of shared stages (TMA, R positions x all C column slices
 // per stage, full / empty mbarriers), so HBM reads run continuously under the score, softmax and
@@ -1175,7 +1175,7 @@ __global__ void __launch_bounds__(ROWS_THREADS, ROWS_PER_SM) attn_fwd_rows(echo_
     }
     return;
   }
-  // ---- consumers (warps 0..7)
+  // ---- consumers (warps 0 .. ROWS_CWARPS-1)
   bool act[CT];
   uint32_t lk[CT];                                            // lane byte offset in a slice row (0 if inactive)
   float vr[CT][4];
@@ -1190,7 +1190,7 @@ __global__ void __launch_bounds__(ROWS_THREADS, ROWS_PER_SM) attn_fwd_rows(echo_
   constexpr int LG = CT == 1 ? 0 : CT == 2 ? 1 : CT == 4 ? 2 : 3;
   constexpr bool PAIRS = CT <= 4;                             // two positions per reduce_scatter (<= 8 slots)
   const uint32_t rowK = (uint32_t)(Wb * sizeof(T)), rowH = (uint32_t)(WHb * sizeof(T));
-  // ctx: thread t owns column pairs t and t + 256 (two adjacent columns each)
+  // ctx: consumer thread t owns column pairs t, t + 32 ROWS_CWARPS, ... (two adjacent columns each)
   const int NPJ = (Hk / 2 + ROWS_CWARPS * 32 - 1) / (ROWS_CWARPS * 32);   // <= ROWS_MAXPJ
   uint32_t off[ROWS_MAXPJ];
   bool pok[ROWS_MAXPJ];
