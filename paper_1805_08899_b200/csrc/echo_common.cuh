@@ -52,7 +52,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 // timeout kills the process.  Correct launches never get near the bound (the longest wait is a
 // TMA stage-in or a peer CTA's exchange, microseconds).
 #ifndef ECHO_WAIT_NS
-#define ECHO_WAIT_NS 4000000000ull   // 4 s
+#define ECHO_WAIT_NS 10000000000ull  // 10 s (compute-sanitizer and time-sliced contexts stretch waits)
 #endif
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
