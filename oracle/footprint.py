@@ -194,17 +194,6 @@ class Graph:
         return self.numel(o)
 
 
-def edge_use_refs(G):
-    """EdgeUseRef pass: consumers per edge, graph outputs count once more."""
-    refs = {}
-    for i in G.order:
-        for e in G.nodes[i]["inputs"]:
-            refs[tuple(e)] = refs.get(tuple(e), 0) + 1
-    for e in G.outputs:
-        refs[e] = refs.get(e, 0) + 1
-    return refs
-
-
 class Strategy:
     def __init__(self, cfg=None):
         cfg = cfg or {}

@@ -246,3 +246,68 @@ def test_nmt_hidden_dropout_graph_reading_r33(est):
     dropped_layers = (cfg.enc_layers - 1) + (cfg.dec_layers - 1)
     assert est(doc, {"strategy": "baseline"})["stash_bytes"] - plain["baseline"] == \
         sum(n * (4 + 1) for n in sites) - dropped_layers * B * H * 4
+
+
+def _group_removal_graph():
+    """Nine ops over [8, 8] f32 tensors (256 B each); x0, x1 inputs, W a weight.
+    3 = x0 + x1, 4 = x1 + n3, 5 = tanh(n4), 6 = FC(n3, W), 7 = n4 * n6, 8 = sigmoid(n5),
+    9 = x1 * n4, 10 = sigmoid(n8), 11 = sum(n10) -> loss (7 and 9 feed nothing but are in the graph,
+    so their gradients read their inputs)."""
+    g = Gr.GraphBuilder()
+    x0, x1 = g.placeholder("x0", [8, 8]), g.placeholder("x1", [8, 8])
+    W = g.placeholder("W", [8, 8], trainable=True)
+    n3 = g.op("add", [x0, x1])
+    n4 = g.op("add", [x1, n3])
+    n5 = g.op("tanh", [n4])
+    n6 = g.op("fully_connected", [n3, W])
+    g.op("mul", [n4, n6])
+    n8 = g.op("sigmoid", [n5])
+    g.op("mul", [x1, n4])
+    n10 = g.op("sigmoid", [n8])
+    g.output(g.op("sum_reduce", [n10]))
+    return g.doc()
+
+
+def test_trimming_removes_sharers_as_a_group(est):
+    """Alg. 1 forward trimming walked by hand (removing one operator that shares a
+    stashed input 'will cause all the other operators to be removed as well'; remove
+    when the released bytes are >= the allocated ones).  Subgraph {3, 4, 5, 8, 10, 11}, all mirrored
+    at first: stash = {x0, x1 (recompute 3, 4; grad of 9), n3 (FC grad), n6 (grad of 7)} = 1024 B.
+      s = 3: co-removal group = {3, 4} (they share the stashed x1); without them the stash is
+             {x1, n3, n4 (needed to recompute 5; grads of 7, 9), n6}: Rel = x0 = 256 >= Alloc = n4 = 256
+             -> BOTH removed.
+      s = 5: group {5}; Alloc = n5 (its own gradient, sigmoid 8's recompute) 256 > Rel 0 -> kept.
+      s = 8, 10: likewise kept.   s = 11: nothing enters or leaves (0 >= 0) -> removed.
+    Final: mirrored {5, 8, 10}; stash {x1, n3, n4, n6} = 1024 B.  Removing only s = 3 and then
+    re-deciding 4 alone would keep 4 mirrored (768 B): the paper's group rule is what is pinned."""
+    doc = _group_removal_graph()
+    cfg = {"enable_dead_node": False}
+    r = F.analyze(doc, cfg)
+    assert sorted(r["mirrored"]) == [5, 8, 10]
+    assert r["stash"] == {(1, 0): False, (3, 0): False, (4, 0): False, (6, 0): False}
+    assert r["stash_bytes"] == 1024
+    c = est(doc, cfg)
+    assert c["stash_bytes"] == 1024 and c["mirrored"] == 3
+
+
+def test_unmirrored_relu_keeps_sign_bits(est):
+    """Alg. 1 line 18 / PAPER.md:726-727 (reading R26): a ReLU whose gradient reads its output and
+    that is not on a recomputation path keeps that output as a 1-bit sign mask.  Graph over [8, 8]
+    f32 (256 B): r = relu(x1) (outside every subgraph: nothing downstream reaches the loss, but its
+    gradient node exists), s = sigmoid(x1), y = FC(s, W), L = sum(y).  Subgraph {FC, s}: trimming s
+    releases x1 (256 B) and allocates s (256 B): 256 >= 256, so s is kept (FC's gradient reads it).
+    Echo keeps s (256 B) + r's sign bits (64 elements -> 8 B) = 264 B; with binarization disabled
+    r is kept at full width: 512 B."""
+    g = Gr.GraphBuilder()
+    g.placeholder("x0", [8, 8])
+    x1 = g.placeholder("x1", [8, 8])
+    W = g.placeholder("W", [8, 8], trainable=True)
+    g.op("relu", [x1])
+    s = g.op("sigmoid", [x1])
+    g.output(g.op("sum_reduce", [g.op("fully_connected", [s, W])]))
+    doc = g.doc()
+    r = F.analyze(doc, {"strategy": "echo"})
+    assert r["mirrored"] == set() and r["stash"] == {(3, 0): True, (4, 0): False} and r["stash_bytes"] == 264
+    r = F.analyze(doc, {"strategy": "echo", "enable_binarization": False})
+    assert r["stash"] == {(3, 0): False, (4, 0): False} and r["stash_bytes"] == 512
+    assert est(doc, {"strategy": "echo"})["stash_bytes"] == 264

@@ -65,3 +65,22 @@ def test_fd_gradient():
         sm[idx] -= eps
         num[idx] = ((O.forward(sp, 0.7, keep, 0.3)["Pd"] - O.forward(sm, 0.7, keep, 0.3)["Pd"]) * dPd).sum() / (2 * eps)
     assert np.abs(num - bw["dS"]).max() / np.abs(num).max() < 1e-6
+
+
+def test_keep_boundary_from_kat_words():
+    """Reading R19's keep rule at its boundary, from the first Random123 vector: seed 0, offset 0
+    draws elements 0..3 from counter (0, 0, 0, 0) with key (0, 0), i.e. the KAT output words.  At
+    p = (w_k >> 8) / 2^24 the threshold equals element k's 24-bit value, so element k is KEPT
+    (keep iff value >= threshold); one step higher it is dropped.  A '>' keep test (or a wrong word /
+    counter mapping) fails here; random inputs hit this boundary with probability 2^-24."""
+    rows = [l.split() for l in open(GOLD) if l.strip() and not l.startswith("#")]
+    words = [int(x, 16) for x in rows[0][6:10]]
+    assert rows[0][:6] == ["00000000"] * 6
+    for k, w in enumerate(words):
+        u = w >> 8
+        for thr, kept in ((u, True), (u + 1, False)):
+            p = thr / float(1 << 24)                       # exact in fp64
+            assert O.keep_threshold(p) == thr
+            m = O.dropout_keep_mask(0, 0, 4, p)
+            assert bool(m[k]) is kept
+            assert [bool(x) for x in m] == [(x >> 8) >= thr for x in words]
