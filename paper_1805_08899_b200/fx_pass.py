@@ -235,7 +235,9 @@ class EchoModule(nn.Module):
             return ("T", t)
         e = self._edge_of(t)
         d = self.plan.decision.get(e)
-        if d == "bit" and t.is_cuda:
+        if d == "bit" and not t.is_cuda:                      # no host path: the 1-bit pack is a libecho kernel
+            raise RuntimeError(f"EchoModule: edge {e} is kept as 1 bit, which needs a CUDA tensor (got {t.device})")
+        if d == "bit":
             if e in self.bits:
                 bits = self.bits[e][0]
             else:
