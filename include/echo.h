@@ -226,7 +226,11 @@ typedef struct {
 /* a5 — forward.
  *  qp [B,A] s, Kp strided [B,Ts,A] s, v [A] s, Hs strided [B,Ts,Hk] s, src_len [B] int32 in
  *  [1,Ts] or NULL (= Ts), ctx [B,Hk] s OUT, E_st [B,Ts,A] s OUT Z = qp + Kp (STASH) / NULL,
- *  alpha_st [B,Ts] fp32 OUT (STASH) / NULL.  Masked positions get alpha = 0.      */
+ *  alpha_st [B,Ts] fp32 OUT (STASH) / NULL.  Masked positions get alpha = 0.
+ *  src_len lives on the device, so the kernels clamp an out-of-range entry to [1,Ts]; with the
+ *  environment flag ECHO_CHECK_SRC_LEN=1 every attention entry point taking src_len first copies it
+ *  to the host (synchronizing `stream`) and returns ECHO_ERR_INVALID for any entry outside [1,Ts]
+ *  (not while the stream is being captured into a CUDA graph).                     */
 echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, const void* Kp, const void* v,
                           const void* Hs, const int32_t* src_len, void* ctx, void* E_st,
                           float* alpha_st, void* stream);

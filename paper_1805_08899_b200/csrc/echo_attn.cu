@@ -1963,6 +1963,33 @@ static echo_status check_attn(const char* fn, const echo_attn_desc* d) {
   return ECHO_OK;
 }
 
+// ECHO_CHECK_SRC_LEN=1 (read on every call): src_len is a device array, so the kernels clamp it to
+// [1, Ts]; with the flag set the entry points copy it to the host (a stream synchronization) and
+// reject any entry outside [1, Ts] with ECHO_ERR_INVALID before launching.  Skipped while the stream
+// is being captured into a CUDA graph (no synchronization is allowed there).
+static echo_status check_src_len(const char* fn, const echo_attn_desc* d, const int32_t* src_len, cudaStream_t st) {
+  const char* e = getenv("ECHO_CHECK_SRC_LEN");
+  if (!src_len || !e || e[0] != '1') return ECHO_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return ECHO_OK;
+  int32_t* h = (int32_t*)malloc(sizeof(int32_t) * (size_t)d->B);
+  if (!h) return fail(ECHO_ERR_CAPACITY, "%s: host buffer for src_len", fn);
+  cudaError_t ce = cudaMemcpyAsync(h, src_len, sizeof(int32_t) * (size_t)d->B, cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) {
+    free(h);
+    return fail(ECHO_ERR_CUDA, "%s: reading src_len: %s", fn, cudaGetErrorString(ce));
+  }
+  for (int b = 0; b < d->B; ++b)
+    if (h[b] < 1 || h[b] > d->Ts) {
+      const int v = h[b];
+      free(h);
+      return fail(ECHO_ERR_INVALID, "%s: src_len[%d] = %d outside [1, %d]", fn, b, v, d->Ts);
+    }
+  free(h);
+  return ECHO_OK;
+}
+
 #define ECHO_REQ(p, name)                                                                     \
   do {                                                                                        \
     if (!(p)) return fail(ECHO_ERR_INVALID, "%s: required pointer %s is NULL", fn, name);     \
@@ -2023,6 +2050,7 @@ extern "C" echo_status echo_attn_fwd(const echo_attn_desc* d, const void* qp, co
     return fail(ECHO_ERR_INVALID, "%s: E_st / alpha_st must be NULL in RECOMPUTE mode", fn);
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if ((s = check_src_len(fn, d, src_len, st))) return s;
   const int C = att_cluster(d->Ts), chunk = att_chunk(d->Ts, C);
   cudaError_t e;
   int tC, tR;
@@ -2098,6 +2126,7 @@ static echo_status attn_bwd_impl(const char* fn, const echo_attn_desc* d, const 
     if (deferred && !al_out) return fail(ECHO_ERR_INVALID, "%s: alpha_out required in deferred RECOMPUTE", fn);
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if ((s = check_src_len(fn, d, src_len, st))) return s;
   const int C = att_cluster(d->Ts), chunk = att_chunk(d->Ts, C);
   cudaError_t e;
   int tC, tR;
@@ -2199,6 +2228,7 @@ static echo_status finish_impl(const char* fn, const echo_attn_desc* d, int32_t 
   const size_t smem = sizeof(float) * ((size_t)Td * FIN_COLS + (size_t)Td * d->Ts);
   if (smem > 200 * 1024) return fail(ECHO_ERR_CAPACITY, "%s: Td=%d x Ts=%d too large", fn, Td, d->Ts);
   cudaStream_t st = (cudaStream_t)stream;
+  if ((s = check_src_len(fn, d, src_len, st))) return s;
   const bool rec = d->mode == ECHO_RECOMPUTE;
   cudaError_t e;
   if (d->dtype == ECHO_FP32) {

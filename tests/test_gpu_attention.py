@@ -282,3 +282,26 @@ def test_attention_rejects_bad_arguments(cuda_dev):
     desc = abi.AttnDesc(2, 4, 16, 16, abi.FP32, abi.RECOMPUTE, 16, 64, 16, 64)
     with pytest.raises(abi.EchoError):                        # RECOMPUTE must not get a stash buffer
         abi.echo_attn_fwd(desc, x, x, x, x, None, x, x, x)
+
+
+def test_attention_src_len_debug_check(cuda_dev, monkeypatch):
+    """SURVEY §8(b) validation: src_len outside [1, Ts] is clamped by the kernels, and rejected with
+    ECHO_ERR_INVALID by the entry points when ECHO_CHECK_SRC_LEN=1 (host copy of the device array)."""
+    abi = _abi()
+    d = mlp_attn_inputs(3, 4, 6, 16, 16)
+    B, Ts, A = d["Kp"].shape
+    Hk = d["Hs"].shape[2]
+    desc = abi.AttnDesc(B, Ts, A, Hk, abi.FP32, abi.RECOMPUTE, Ts * A, A, Ts * Hk, Hk)
+    qp, Kp, v, Hs = (dev(d[k], "fp32") for k in ("qp", "Kp", "v", "Hs"))
+    ctx = torch.empty(B, Hk, device="cuda")
+    good = torch.tensor([6, 1, 3, 2], dtype=torch.int32, device="cuda")
+    for bad in ([6, 0, 3, 2], [6, 1, 7, 2]):
+        sl = torch.tensor(bad, dtype=torch.int32, device="cuda")
+        monkeypatch.delenv("ECHO_CHECK_SRC_LEN", raising=False)
+        abi.echo_attn_fwd(desc, qp, Kp, v, Hs, sl, ctx, None, None)          # clamped, no error
+        monkeypatch.setenv("ECHO_CHECK_SRC_LEN", "1")
+        with pytest.raises(abi.EchoError) as ei:
+            abi.echo_attn_fwd(desc, qp, Kp, v, Hs, sl, ctx, None, None)
+        assert ei.value.status == 1 and "src_len" in str(ei.value)
+    abi.echo_attn_fwd(desc, qp, Kp, v, Hs, good, ctx, None, None)          # in range: accepted
+    torch.cuda.synchronize()
