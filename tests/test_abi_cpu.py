@@ -91,3 +91,44 @@ def test_host_validation_without_gpu(lib):
     with pytest.raises(abi.EchoError) as e:
         abi.echo_dot_softmax_fwd(dd, None, None, None, None, stream=0)
     assert e.value.status == abi.ECHO_ERR_INVALID
+
+
+def _prototypes():
+    """name -> list of C parameter declarations, from include/echo.h."""
+    src = open(os.path.join(ROOT, "include", "echo.h")).read()
+    src = re.sub(r"/\*.*?\*/", " ", src, flags=re.S)
+    src = re.sub(r"//[^\n]*", " ", src)
+    out = {}
+    for m in re.finditer(r"\b(?:echo_status|int|const char\*|void)\s+(echo_[a-z_0-9]+)\s*\(([^;{]*?)\)\s*;", src, flags=re.S):
+        params = " ".join(m.group(2).split())
+        out[m.group(1)] = [] if params in ("", "void") else [p.strip() for p in params.split(",")]
+    return out
+
+
+def test_binding_argtypes_match_the_header(lib):
+    """Every ctypes signature in abi.py has the header's arity and, position by position, the same kind
+    of argument (pointer / int32 / int64 / uint32 / uint64 / float / size_t): an edited prototype cannot
+    silently drift from the binding."""
+    import ctypes
+    protos = _prototypes()
+    assert len(protos) >= len(NORTH_STAR)
+    scalar = {"int32_t": (ctypes.c_int32, ctypes.c_int), "int": (ctypes.c_int32, ctypes.c_int),
+              "int64_t": (ctypes.c_int64,), "uint32_t": (ctypes.c_uint32,), "uint64_t": (ctypes.c_uint64,),
+              "float": (ctypes.c_float,), "size_t": (ctypes.c_size_t,)}
+    checked = 0
+    for name, params in protos.items():
+        argtypes = getattr(lib, name).argtypes
+        if argtypes is None:                      # echo_last_error / echo_abi_version / debug hooks
+            assert not params or name.startswith("echo_debug"), name
+            continue
+        assert len(argtypes) == len(params), (name, len(argtypes), params)
+        for k, (p, a) in enumerate(zip(params, argtypes)):
+            ctype = re.sub(r"\b(const|restrict)\b", "", p.rsplit(" ", 1)[0] if not p.endswith("*") else p).strip()
+            if "*" in p:
+                ok = a in (ctypes.c_void_p, ctypes.c_char_p) or (hasattr(a, "_type_") and a.__name__.startswith("LP_"))
+            else:
+                base = ctype.split()[-1]
+                ok = a in scalar.get(base, (ctypes.c_int32, ctypes.c_int) if base.startswith("echo_") else ())
+            assert ok, (name, k, p, a)
+        checked += 1
+    assert checked >= 25
