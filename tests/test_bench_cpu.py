@@ -20,8 +20,12 @@ def test_reference_arm_json_and_two_ranks():
     runs it and prints ONE JSON line with impl = reference, a cpu_baseline and a zero-copy e2e; the
     other rank exits 0 without output."""
     import json
+    import socket
+    with socket.socket() as so:                   # a free rendezvous port
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", "29561", os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
            "--steps", "1", "--warmup", "0"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
