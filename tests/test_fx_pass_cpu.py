@@ -89,3 +89,45 @@ def test_conv2d_graph_cpp_equals_oracle():
     assert e <= b
     _, saved = X.baseline_saved_bytes(m, x)
     assert saved == b
+
+
+class _TanhGateMLP(nn.Module):
+    """x <- tanh(W x) * sigmoid(G x) + x: tanh / sigmoid / mul / add maps between FCs."""
+
+    def __init__(self, d=32, depth=3):
+        super().__init__()
+        self.fc = nn.ModuleList([nn.Linear(d, d) for _ in range(depth)])
+        self.g = nn.ModuleList([nn.Linear(d, d) for _ in range(depth)])
+
+    def forward(self, x):
+        for f, g in zip(self.fc, self.g):
+            x = torch.tanh(f(x)) * torch.sigmoid(g(x)) + x
+        return x.sum()
+
+
+@pytest.mark.parametrize("make,shape", [(lambda: ReluTaps(16, 3), (4, 16)), (lambda: ResMLP(16, 3), (4, 16)),
+                                        (lambda: ResConvNet(4, 2), (2, 3, 8, 8)), (lambda: _TanhGateMLP(32, 3), (4, 32))],
+                         ids=["relutaps", "resmlp", "resconv", "tanhgate"])
+def test_echo_module_plan_application_on_host(make, shape):
+    """The saved-tensor-hook machinery of EchoModule on host tensors, for plans without 1-bit edges (the
+    1-bit pack is a libecho kernel; the GPU test covers it): loss and every parameter gradient bitwise
+    those of the unmodified model, the bytes the hooks keep == the estimator's Echo stash bytes, and the
+    unmodified model's autograd keeps exactly the Baseline bytes."""
+    from paper_1805_08899_b200 import fx_pass as X
+    torch.manual_seed(0)
+    m = make().double()
+    x = torch.randn(*shape, dtype=torch.float64)
+    ref, base_bytes = X.baseline_saved_bytes(m, x)
+    ref.backward()
+    g_ref = [p.grad.clone() for p in m.parameters()]
+    m.zero_grad(set_to_none=True)
+    em = X.EchoModule(m, (x,))
+    assert "bit" not in set(em.plan.decision.values())
+    assert base_bytes == X.EchoPlan(m, (x,), strategy="baseline").stash_bytes()
+    loss = em(x)
+    assert em.kept_bytes() == em.plan.stash_bytes() <= base_bytes
+    loss.backward()
+    assert torch.equal(loss.detach(), ref.detach())
+    for p, g in zip(m.parameters(), g_ref):
+        assert torch.equal(p.grad, g)
+
