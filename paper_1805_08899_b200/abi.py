@@ -345,12 +345,15 @@ def echo_footprint_estimate(graph_json: str, config_json: str | None = None) -> 
     lib = load()
     g = graph_json.encode()
     c = config_json.encode() if config_json is not None else None
-    n = ctypes.c_size_t(0)
-    st = lib.echo_footprint_estimate(g, c, None, ctypes.byref(n))
-    if st not in (ECHO_OK, ECHO_ERR_CAPACITY):
-        _check(st)
+    # one analysis in the common case: a buffer the size of the graph text (reports are smaller);
+    # the two-call convention (ECHO_ERR_CAPACITY + the needed size) covers the rest
+    n = ctypes.c_size_t(max(1 << 20, len(g)))
     buf = ctypes.create_string_buffer(n.value)
-    _check(lib.echo_footprint_estimate(g, c, buf, ctypes.byref(n)))
+    st = lib.echo_footprint_estimate(g, c, buf, ctypes.byref(n))
+    if st == ECHO_ERR_CAPACITY:
+        buf = ctypes.create_string_buffer(n.value)
+        st = lib.echo_footprint_estimate(g, c, buf, ctypes.byref(n))
+    _check(st)
     return buf.value.decode()
 
 

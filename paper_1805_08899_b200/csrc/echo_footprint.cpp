@@ -27,11 +27,13 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "../../include/echo.h"
@@ -43,16 +45,33 @@ echo_status fail(echo_status s, const char* fmt, ...);
 namespace {
 
 // ============================================================================ minimal JSON
+// Compact read-only DOM: values live in a JsonDoc's pool (stable addresses), containers point at
+// arena arrays of child pointers (and, for objects, keys), strings are views into the source text
+// (or into the doc when they contain escapes).  The source text must outlive the doc.
 struct Json {
-  enum Kind { NUL, BOOL, NUM, STR, ARR, OBJ } kind = NUL;
+  enum Kind : uint8_t { NUL, BOOL, NUM, STR, ARR, OBJ } kind = NUL;
   bool b = false;
   double num = 0;
-  std::string str;
-  std::vector<Json> arr;
-  std::vector<std::pair<std::string, Json>> obj;
-  const Json* get(const std::string& k) const {
-    for (auto& kv : obj)
-      if (kv.first == k) return &kv.second;
+  std::string_view str;
+  struct Range {                               // ARR elements / OBJ values
+    const Json* const* p = nullptr;
+    uint32_t n = 0;
+    size_t size() const { return n; }
+    const Json& operator[](size_t i) const { return *p[i]; }
+    struct It {
+      const Json* const* q;
+      const Json& operator*() const { return **q; }
+      It& operator++() { ++q; return *this; }
+      bool operator!=(const It& o) const { return q != o.q; }
+    };
+    It begin() const { return {p}; }
+    It end() const { return {p + n}; }
+  } arr;
+  const std::string_view* keys = nullptr;      // OBJ keys, parallel to arr
+  const Json* get(std::string_view k) const {
+    if (kind != OBJ) return nullptr;
+    for (uint32_t i = 0; i < arr.n; ++i)
+      if (keys[i] == k) return arr.p[i];
     return nullptr;
   }
   long long i64() const { return (long long)llround(num); }
@@ -62,86 +81,166 @@ struct ParseError : std::runtime_error {
   explicit ParseError(const std::string& s) : std::runtime_error(s) {}
 };
 
+struct JsonDoc {
+  std::deque<Json> pool;
+  std::deque<std::string> escaped;             // strings that contained escapes
+  std::vector<std::unique_ptr<char[]>> blocks; // arena for child-pointer and key arrays
+  char* cur = nullptr;
+  size_t left = 0;
+  const Json* root = nullptr;
+  template <typename T> T* alloc(size_t n) {
+    const size_t bytes = (n * sizeof(T) + 15) & ~(size_t)15;
+    if (bytes > left) {
+      const size_t sz = bytes > (1u << 20) ? bytes : (1u << 20);
+      blocks.emplace_back(new char[sz]);
+      cur = blocks.back().get();
+      left = sz;
+    }
+    T* r = reinterpret_cast<T*>(cur);
+    cur += bytes;
+    left -= bytes;
+    return r;
+  }
+};
+
+// Recursive-descent parser.  Children of open containers are collected on one shared scratch stack
+// and copied to the arena when the container closes; integers are parsed without strtod.
 struct Parser {
   const char* p;
   const char* end;
+  JsonDoc& doc;
+  std::vector<const Json*> kid_stack;
+  std::vector<std::string_view> key_stack;
   void ws() {
-    while (p < end && isspace((unsigned char)*p)) ++p;
+    while (p < end && (*p == ' ' || *p == '\n' || *p == '\t' || *p == '\r' || *p == '\f' || *p == '\v')) ++p;
   }
   [[noreturn]] void err(const char* what) { throw ParseError(std::string("json: ") + what); }
-  Json value() {
+  std::string_view string_view_at() {          // at the opening quote
+    const char* s0 = ++p;
+    const char* q = p;
+    while (q < end && *q != '"' && *q != '\\') ++q;
+    if (q < end && *q == '"') {                // no escapes: a view into the source
+      p = q + 1;
+      return std::string_view(s0, (size_t)(q - s0));
+    }
+    doc.escaped.emplace_back(s0, q);
+    std::string& out = doc.escaped.back();
+    p = q;
+    for (;;) {
+      if (p >= end) err("unterminated string");
+      if (*p == '"') { ++p; return std::string_view(out); }
+      if (*p == '\\') {
+        ++p;
+        if (p >= end) err("bad escape");
+        const char c = *p++;
+        out.push_back(c == 'n' ? '\n' : c == 't' ? '\t' : c);
+        continue;
+      }
+      q = p;
+      while (q < end && *q != '"' && *q != '\\') ++q;
+      out.append(p, q);
+      p = q;
+    }
+  }
+  void number_into(Json& j) {
+    j.kind = Json::NUM;
+    const char* q = p;
+    bool neg = false;
+    if (q < end && *q == '-') { neg = true; ++q; }
+    const char* d0 = q;
+    long long v = 0;
+    while (q < end && *q >= '0' && *q <= '9' && q - d0 < 18) v = v * 10 + (*q++ - '0');
+    if (q > d0 && (q >= end || (*q != '.' && *q != 'e' && *q != 'E' && !(*q >= '0' && *q <= '9')))) {
+      j.num = (double)(neg ? -v : v);      // plain integer (exact below 10^18)
+      p = q;
+      return;
+    }
+    char* r = nullptr;
+    j.num = strtod(p, &r);
+    if (r == p) err("bad value");
+    p = r;
+  }
+  void close(Json& j, size_t mark, bool obj) {
+    const size_t n = kid_stack.size() - mark;
+    j.arr.n = (uint32_t)n;
+    if (!n) return;
+    const Json** kids = doc.alloc<const Json*>(n);
+    std::copy(kid_stack.begin() + mark, kid_stack.end(), kids);
+    j.arr.p = kids;
+    kid_stack.resize(mark);
+    if (obj) {
+      std::string_view* ks = doc.alloc<std::string_view>(n);
+      std::copy(key_stack.end() - n, key_stack.end(), ks);
+      j.keys = ks;
+      key_stack.resize(key_stack.size() - n);
+    }
+  }
+  const Json* value() {
     ws();
     if (p >= end) err("unexpected end");
-    Json j;
+    doc.pool.emplace_back();
+    Json& j = doc.pool.back();
     if (*p == '{') {
       j.kind = Json::OBJ;
       ++p;
       ws();
-      if (p < end && *p == '}') { ++p; return j; }
+      const size_t mark = kid_stack.size();
+      if (p < end && *p == '}') { ++p; return &j; }
       for (;;) {
         ws();
-        Json k = value();
-        if (k.kind != Json::STR) err("object key must be a string");
+        if (p >= end || *p != '"') {
+          if (p < end) value();                // a non-string key: parse it for the error position
+          err("object key must be a string");
+        }
+        key_stack.push_back(string_view_at());
         ws();
         if (p >= end || *p != ':') err("expected ':'");
         ++p;
-        j.obj.emplace_back(k.str, value());
+        kid_stack.push_back(value());
         ws();
         if (p < end && *p == ',') { ++p; continue; }
         if (p < end && *p == '}') { ++p; break; }
         err("expected ',' or '}'");
       }
+      close(j, mark, true);
     } else if (*p == '[') {
       j.kind = Json::ARR;
       ++p;
       ws();
-      if (p < end && *p == ']') { ++p; return j; }
+      const size_t mark = kid_stack.size();
+      if (p < end && *p == ']') { ++p; return &j; }
       for (;;) {
-        j.arr.push_back(value());
+        kid_stack.push_back(value());
         ws();
         if (p < end && *p == ',') { ++p; continue; }
         if (p < end && *p == ']') { ++p; break; }
         err("expected ',' or ']'");
       }
+      close(j, mark, false);
     } else if (*p == '"') {
       j.kind = Json::STR;
-      ++p;
-      while (p < end && *p != '"') {
-        if (*p == '\\') {
-          ++p;
-          if (p >= end) err("bad escape");
-          char c = *p;
-          j.str.push_back(c == 'n' ? '\n' : c == 't' ? '\t' : c);
-        } else {
-          j.str.push_back(*p);
-        }
-        ++p;
-      }
-      if (p >= end) err("unterminated string");
-      ++p;
-    } else if (!strncmp(p, "true", 4)) {
+      j.str = string_view_at();
+    } else if (end - p >= 4 && !strncmp(p, "true", 4)) {
       j.kind = Json::BOOL; j.b = true; p += 4;
-    } else if (!strncmp(p, "false", 5)) {
+    } else if (end - p >= 5 && !strncmp(p, "false", 5)) {
       j.kind = Json::BOOL; j.b = false; p += 5;
-    } else if (!strncmp(p, "null", 4)) {
+    } else if (end - p >= 4 && !strncmp(p, "null", 4)) {
       j.kind = Json::NUL; p += 4;
     } else {
-      char* q = nullptr;
-      j.kind = Json::NUM;
-      j.num = strtod(p, &q);
-      if (q == p) err("bad value");
-      p = q;
+      number_into(j);
     }
-    return j;
+    return &j;
   }
 };
 
-Json parse_json(const char* s) {
-  Parser ps{s, s + strlen(s)};
-  Json j = ps.value();
+// The returned doc views `s`: keep the text alive while the doc (or anything pointing into it) is used.
+std::unique_ptr<JsonDoc> parse_json(const char* s) {
+  auto doc = std::make_unique<JsonDoc>();
+  Parser ps{s, s + strlen(s), *doc, {}, {}};
+  doc->root = ps.value();
   ps.ws();
   if (ps.p != ps.end) throw ParseError("json: trailing characters");
-  return j;
+  return doc;
 }
 
 std::string jstr(const std::string& s) {
@@ -215,7 +314,12 @@ struct Node {
 struct Graph {
   std::vector<Node> nodes;           // by id (dense)
   std::vector<Edge> edges;
-  std::map<std::pair<int, int>, int> edge_of;
+  std::vector<int> first_out;        // per node id: index of its output 0 (outputs are contiguous), -1 if none yet
+  int edge_of(long long node, long long k) const {   // -1 if (node, k) is not an edge
+    if (node < 0 || node >= (long long)first_out.size() || first_out[node] < 0 || k < 0) return -1;
+    const Node& n = nodes[node];
+    return k < (long long)n.out.size() ? n.out[k] : -1;
+  }
   std::vector<int> order;            // non-placeholder node ids, ascending (topological)
   std::vector<int> outputs;          // edge indices
   std::vector<std::vector<int>> consumers;     // per edge: consumer node ids (with multiplicity per use)
@@ -231,12 +335,13 @@ int64_t attr_int(const Node& n, const char* k, int64_t def) {
 std::string attr_str(const Node& n, const char* k) {
   if (!n.attrs) return "";
   const Json* v = n.attrs->get(k);
-  return v && v->kind == Json::STR ? v->str : "";
+  return v && v->kind == Json::STR ? std::string(v->str) : std::string();
 }
 
 void infer(Graph& g, Node& n) {
   const OpInfo& oi = OPS[n.op];
   std::vector<const Edge*> I;
+  I.reserve(n.in.size());
   for (int e : n.in) I.push_back(&g.edges[e]);
   std::vector<std::vector<int64_t>> out;
   auto need = [&](bool ok, const char* what) {
@@ -349,9 +454,9 @@ void infer(Graph& g, Node& n) {
   for (size_t k = 0; k < out.size(); ++k) {
     Edge e{n.id, (int)k, out[k], n.op == CE ? std::string("f32") : (n.op == DROPOUT && k == 1 ? std::string("u8") : dt)};
     for (auto s : e.shape) need(s >= 1, "non-positive dim");
-    g.edge_of[{n.id, (int)k}] = (int)g.edges.size();
+    if (k == 0) g.first_out[n.id] = (int)g.edges.size();
     n.out.push_back((int)g.edges.size());
-    g.edges.push_back(e);
+    g.edges.push_back(std::move(e));
   }
 }
 
@@ -367,6 +472,7 @@ Graph build_graph(const Json& doc) {
     throw ParseError("graph: needs arrays 'placeholders', 'nodes', 'outputs'");
   const size_t N = phs->arr.size() + nds->arr.size();
   g.nodes.resize(N);
+  g.first_out.assign(N, -1);
   std::vector<const Json*> def(N, nullptr);
   std::vector<char> isph(N, 0);
   for (auto& p : phs->arr) {
@@ -387,7 +493,7 @@ Graph build_graph(const Json& doc) {
     n.id = (int)i;
     const Json& d = *def[i];
     const Json* tag = d.get("tag");
-    n.tag = tag && tag->kind == Json::STR ? tag->str : "";
+    n.tag = tag && tag->kind == Json::STR ? std::string(tag->str) : std::string();
     if (isph[i]) {
       n.placeholder = true;
       const Json* tr = d.get("trainable");
@@ -395,34 +501,39 @@ Graph build_graph(const Json& doc) {
       const Json* sh = d.get("shape");
       const Json* dt = d.get("dtype");
       if (!sh || sh->kind != Json::ARR || !dt || dt->kind != Json::STR) throw ParseError("graph: placeholder needs shape, dtype");
-      Edge e{(int)i, 0, {}, dt->str};
+      Edge e{(int)i, 0, {}, std::string(dt->str)};
       for (auto& s : sh->arr) {
         if (s.i64() < 1) throw ParseError("graph: non-positive dim");
         e.shape.push_back(s.i64());
       }
       dtype_width(e.dtype);
-      g.edge_of[{(int)i, 0}] = (int)g.edges.size();
+      g.first_out[i] = (int)g.edges.size();
       n.out.push_back((int)g.edges.size());
-      g.edges.push_back(e);
+      g.edges.push_back(std::move(e));
       continue;
     }
     const Json* op = d.get("op");
     if (!op || op->kind != Json::STR) throw ParseError("graph: node needs 'op'");
     n.op = -1;
-    for (int k = 0; k < N_OPS; ++k)
-      if (op->str == OPS[k].name) n.op = k;
-    if (n.op < 0) throw ParseError("graph: unknown op '" + op->str + "'");
+    static const std::vector<std::string_view> op_names = [] {
+      std::vector<std::string_view> v;
+      for (int k = 0; k < N_OPS; ++k) v.emplace_back(OPS[k].name);
+      return v;
+    }();
+    for (int k = 0; k < N_OPS && n.op < 0; ++k)
+      if (op->str == op_names[k]) n.op = k;
+    if (n.op < 0) throw ParseError("graph: unknown op '" + std::string(op->str) + "'");
     const Json* ins = d.get("inputs");
     if (!ins || ins->kind != Json::ARR) throw ParseError("graph: node needs 'inputs'");
     if ((int)ins->arr.size() < OPS[n.op].min_in || (int)ins->arr.size() > OPS[n.op].max_in)
-      throw ParseError("graph: arity mismatch for node " + std::to_string(i) + " (" + op->str + ")");
+      throw ParseError("graph: arity mismatch for node " + std::to_string(i) + " (" + std::string(op->str) + ")");
     for (auto& r : ins->arr) {
       if (r.kind != Json::ARR || r.arr.size() != 2) throw ParseError("graph: input must be [node, out]");
       long long src = r.arr[0].i64(), k = r.arr[1].i64();
       if (src < 0 || src >= (long long)i) throw ParseError("graph: input must reference an earlier id (cycle or forward ref)");
-      auto it = g.edge_of.find({(int)src, (int)k});
-      if (it == g.edge_of.end()) throw ParseError("graph: dangling edge reference");
-      n.in.push_back(it->second);
+      const int e = g.edge_of(src, k);
+      if (e < 0) throw ParseError("graph: dangling edge reference");
+      n.in.push_back(e);
     }
     const Json* at = d.get("attrs");
     n.attrs = at && at->kind == Json::OBJ ? at : nullptr;
@@ -431,9 +542,9 @@ Graph build_graph(const Json& doc) {
   }
   for (auto& o : outs->arr) {
     if (o.kind != Json::ARR || o.arr.size() != 2) throw ParseError("graph: output must be [node, out]");
-    auto it = g.edge_of.find({(int)o.arr[0].i64(), (int)o.arr[1].i64()});
-    if (it == g.edge_of.end()) throw ParseError("graph: dangling output");
-    g.outputs.push_back(it->second);
+    const int e = g.edge_of(o.arr[0].i64(), o.arr[1].i64());
+    if (e < 0) throw ParseError("graph: dangling output");
+    g.outputs.push_back(e);
   }
   g.consumers.assign(g.edges.size(), {});
   g.grad_readers.assign(g.edges.size(), {});
@@ -466,17 +577,18 @@ struct Config {
 Config parse_config(const char* s) {
   Config c;
   if (!s) return c;
-  Json j = parse_json(s);
+  auto doc = parse_json(s);
+  const Json& j = *doc->root;
   if (j.kind != Json::OBJ) throw ParseError("config: must be an object");
-  if (auto* v = j.get("strategy")) c.kind = v->str;
+  if (auto* v = j.get("strategy")) c.kind = std::string(v->str);
   if (c.kind != "echo" && c.kind != "mirror" && c.kind != "baseline") throw ParseError("config: bad strategy");
   if (auto* v = j.get("compute_heavy_ops")) {
     c.heavy.clear();
-    for (auto& x : v->arr) c.heavy.insert(x.str);
+    for (auto& x : v->arr) c.heavy.insert(std::string(x.str));
   }
   if (auto* v = j.get("binarizable_ops")) {
     c.binarizable.clear();
-    for (auto& x : v->arr) c.binarizable.insert(x.str);
+    for (auto& x : v->arr) c.binarizable.insert(std::string(x.str));
   }
   if (auto* v = j.get("enable_dead_node")) c.dead = v->b;
   if (auto* v = j.get("enable_binarization")) c.binarize = v->b;
@@ -774,8 +886,8 @@ Plan plan(const Graph& g, const Analysis& a, const std::vector<int>& st) {
 }
 
 std::string analyze(const char* graph_json, const char* config_json) {
-  Json doc = parse_json(graph_json);
-  Graph g = build_graph(doc);
+  auto doc = parse_json(graph_json);
+  Graph g = build_graph(*doc->root);
   Config cfg = parse_config(config_json);
   Analysis a(g, cfg);
   Result r;
