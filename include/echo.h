@@ -429,12 +429,17 @@ echo_status echo_tanh_bwd(int64_t n, int32_t dtype, const void* a, const float* 
  *               enable_binarization, regenerate_masks, flop_threshold, weight_multiplier};
  *               NULL = echo defaults.  regenerate_masks (default false, echo / mirror only;
  *               DESIGN.md R30): dropout keep-masks come from a counter-based generator, so a
- *               mirrored dropout regenerates its mask instead of keeping it (0 bytes)
+ *               mirrored dropout regenerates its mask instead of keeping it (0 bytes).
+ *               self_verify (default false): after planning, check that every edge a gradient
+ *               reads is kept or regenerable from kept edges (SPEC.md:632-639 `verify`);
+ *               debug_unstash_edge [node, out]: test hook that drops that edge from the plan
+ *               first (a corrupted plan; implies self_verify)
  *  report_json  caller buffer for the NUL-terminated report; may be NULL to query
  *  report_len   IN capacity of report_json; OUT bytes needed (including the NUL).
  *               Returns ECHO_ERR_CAPACITY (with *report_len set) if too small.
  * Errors: ECHO_ERR_INVALID (parse / schema / unknown op / arity / shape),
- *         ECHO_ERR_GRAPH (cycle or pipeline failure).                              */
+ *         ECHO_ERR_GRAPH (cycle or pipeline failure),
+ *         ECHO_ERR_MISMATCH (self_verify: the plan leaves a gradient input unavailable). */
 echo_status echo_footprint_estimate(const char* graph_json, const char* config_json,
                                     char* report_json, size_t* report_len);
 

@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <set>
@@ -572,6 +573,8 @@ struct Config {
   bool has_threshold = false;
   double threshold = 0;
   double weight_multiplier = 1;
+  bool self_verify = false;    // check the plan is sufficient for the backward (ECHO_ERR_MISMATCH if not)
+  int unstash_node = -1, unstash_out = 0;   // test hook: drop this edge from the plan before verifying
 };
 
 Config parse_config(const char* s) {
@@ -593,6 +596,13 @@ Config parse_config(const char* s) {
   if (auto* v = j.get("enable_dead_node")) c.dead = v->b;
   if (auto* v = j.get("enable_binarization")) c.binarize = v->b;
   if (auto* v = j.get("regenerate_masks")) c.regen = v->b;
+  if (auto* v = j.get("self_verify")) c.self_verify = v->b;
+  if (auto* v = j.get("debug_unstash_edge"))                 // [node, out]: a corrupted plan (negative control)
+    if (v->kind == Json::ARR && v->arr.size() == 2) {
+      c.unstash_node = (int)v->arr[0].i64();
+      c.unstash_out = (int)v->arr[1].i64();
+      c.self_verify = true;
+    }
   if (auto* v = j.get("flop_threshold"))
     if (v->kind == Json::NUM) { c.has_threshold = true; c.threshold = v->num; }
   if (auto* v = j.get("weight_multiplier"))
@@ -885,6 +895,61 @@ Plan plan(const Graph& g, const Analysis& a, const std::vector<int>& st) {
   return p;
 }
 
+// ============================================================================ plan self-check
+struct MismatchError : std::runtime_error {
+  explicit MismatchError(const std::string& s) : std::runtime_error(s) {}
+};
+
+// The plan is sufficient iff every forward edge a gradient step reads can be produced in the backward:
+// a weight; stashed at full precision (or inside a stashed stack); or regenerated by its mirrored
+// producer from inputs that are themselves available (a mirrored dropout also needs its mask).  A heavy
+// op that reads its ORIGINAL inputs (dead mirrors disabled) needs them stashed; a binarizable op that is
+// not mirrored may read its own output as a 1-bit mask; a keep-mask may be kept as bits or (R30)
+// regenerated from its Philox counter.  (SPEC.md:632-639 `verify`, here as a structural check.)
+void verify_plan(const Graph& g, const Analysis& a, const std::vector<int>& st) {
+  std::vector<signed char> memo(g.edges.size(), -1);
+  auto mask_ok = [&](int e) { return st[e] != 0 || a.cfg.regen; };
+  std::function<bool(int)> full = [&](int e) -> bool {
+    if (memo[e] >= 0) return memo[e];
+    memo[e] = 0;                                             // (a cycle cannot occur: ids are topological)
+    bool ok = a.trainable(e) || st[e] == 1 || (g.stacked_into[e] >= 0 && st[g.stacked_into[e]] == 1);
+    const int p = g.edges[e].node;
+    if (!ok && !g.nodes[p].placeholder && a.mirrored[p] && !a.is_random(e)) {
+      ok = true;
+      for (int q : g.nodes[p].in) ok = ok && full(q);
+      if (ok && g.nodes[p].op == DROPOUT) ok = mask_ok(g.nodes[p].out[1]);
+    }
+    memo[e] = ok;
+    return ok;
+  };
+  auto fail_at = [&](int r, int e, const char* why) {
+    throw MismatchError("plan self-check: gradient of node " + std::to_string(r) + " (" + OPS[g.nodes[r].op].name +
+                        ") reads edge [" + std::to_string(g.edges[e].node) + "," + std::to_string(g.edges[e].out) +
+                        "], " + why);
+  };
+  for (int r : g.order) {
+    const Node& n = g.nodes[r];
+    std::vector<int> refs;
+    for (size_t k = 0; k < n.in.size(); ++k)
+      if (k < 32 && (OPS[n.op].needs_in >> k) & 1u) refs.push_back(n.in[k]);
+    for (size_t k = 0; k < n.out.size(); ++k)
+      if ((OPS[n.op].needs_out >> k) & 1u) refs.push_back(n.out[k]);
+    for (int e : refs) {
+      if (a.trainable(e)) continue;
+      if (a.is_random(e)) {
+        if (!mask_ok(e)) fail_at(r, e, "a keep-mask that is neither kept nor regenerable");
+      } else if (a.heavy_orig[r]) {
+        if (!(st[e] == 1 || (g.stacked_into[e] >= 0 && st[g.stacked_into[e]] == 1)))
+          fail_at(r, e, "an original input that is not kept");
+      } else if (g.edges[e].node == r && a.binz[r] && !a.mirrored[r]) {
+        if (st[e] == 0) fail_at(r, e, "its own output, kept neither as bits nor in full");
+      } else if (!full(e)) {
+        fail_at(r, e, "which is neither kept nor regenerable from kept edges");
+      }
+    }
+  }
+}
+
 std::string analyze(const char* graph_json, const char* config_json) {
   auto doc = parse_json(graph_json);
   Graph g = build_graph(*doc->root);
@@ -895,6 +960,12 @@ std::string analyze(const char* graph_json, const char* config_json) {
   else if (cfg.kind == "mirror") run_mirror(g, a);
   std::vector<int> st(g.edges.size(), 0);
   for (size_t e = 0; e < g.edges.size(); ++e) st[e] = a.status((int)e);
+  if (cfg.unstash_node >= 0) {
+    const int e = g.edge_of(cfg.unstash_node, cfg.unstash_out);
+    if (e < 0) throw ParseError("config: debug_unstash_edge is not an edge");
+    st[e] = 0;
+  }
+  if (cfg.self_verify) verify_plan(g, a, st);
   // stash bytes (a stashed stack output covers its view inputs)
   int64_t stash = 0, weights = 0;
   std::map<std::string, int64_t> by_tag;
@@ -964,6 +1035,8 @@ extern "C" echo_status echo_footprint_estimate(const char* graph_json, const cha
   std::string rep;
   try {
     rep = analyze(graph_json, config_json);
+  } catch (const MismatchError& e) {
+    return echo::fail(ECHO_ERR_MISMATCH, "echo_footprint_estimate: %s", e.what());
   } catch (const ParseError& e) {
     return echo::fail(ECHO_ERR_INVALID, "echo_footprint_estimate: %s", e.what());
   } catch (const std::exception& e) {

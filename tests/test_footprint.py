@@ -325,3 +325,48 @@ def test_unmirrored_relu_keeps_sign_bits(est):
     r = F.analyze(doc, {"strategy": "echo", "enable_binarization": False})
     assert r["stash"] == {(3, 0): False, (4, 0): False} and r["stash_bytes"] == 512
     assert est(doc, {"strategy": "echo"})["stash_bytes"] == 264
+
+
+def _self_check_docs():
+    from synth.configs import SMALL_TX, SMALL_DS2, SMALL_NMT_DROP
+    from dataclasses import replace
+    docs = {"add_tanh": Gr.add_tanh(64), "bcast": Gr.broadcast_attn(8, 16), "tanh_fc": Gr.tanh_fc(),
+            "chain4": Gr.chain4(), "lstm3": Gr.lstm_layer(3, 2, 8, 8), "c1": Gr.nmt(C1), "small": Gr.nmt(SMALL_NMT),
+            "small_drop": Gr.nmt(SMALL_NMT_DROP), "small_hdrop": Gr.nmt(replace(SMALL_NMT, dropout_hidden=0.2)),
+            "ds2": Gr.ds2(SMALL_DS2), "tx": Gr.transformer(SMALL_TX), "c2": Gr.nmt(C2)}
+    for seed in range(40):
+        docs[f"rand{seed}"] = Gr.random_graph(seed)
+    return docs
+
+
+def test_plan_self_check_passes_on_every_plan(est):
+    """self_verify (SPEC.md:632-639 'verify', as a structural check): every edge a gradient reads is kept
+    or regenerable from kept edges, for every strategy / option on the workload graphs and 40 random
+    graphs; the self-check changes nothing in the report."""
+    cfgs = [{"strategy": "baseline"}, {"strategy": "mirror"}, {"strategy": "echo"},
+            {"strategy": "echo", "enable_dead_node": False}, {"strategy": "echo", "enable_binarization": False},
+            {"strategy": "echo", "regenerate_masks": True}, {"strategy": "mirror", "regenerate_masks": True}]
+    for name, doc in _self_check_docs().items():
+        for cfg in cfgs:
+            r = est(doc, dict(cfg, self_verify=True))
+            assert r == est(doc, cfg), (name, cfg)
+
+
+def test_plan_self_check_catches_a_corrupted_plan(est):
+    """Negative control (SPEC.md:639 'verify with corrupted plan -> fail, exit 4'): dropping any one
+    kept, non-weight edge from Echo's plan makes the self-check fail with ECHO_ERR_MISMATCH."""
+    from paper_1805_08899_b200 import abi
+    docs = _self_check_docs()
+    n_checked = 0
+    for name in ("add_tanh", "lstm3", "c1", "small_drop", "tx", "rand3", "rand7"):
+        doc = docs[name]
+        r = est(doc, {"strategy": "echo"})
+        for node, out, d in r["decisions"]:
+            if d not in ("stash", "bit"):
+                continue
+            with pytest.raises(abi.EchoError) as ei:
+                est(doc, {"strategy": "echo", "debug_unstash_edge": [node, out]})
+            assert ei.value.status == abi.ECHO_ERR_MISMATCH, (name, node, out)
+            assert "plan self-check" in str(ei.value)
+            n_checked += 1
+    assert n_checked >= 50
