@@ -50,6 +50,9 @@ GRAD_DEPS = {
     "dot_last": ({0, 1}, set(), 1), "masked_softmax": ({1}, {0}, 1), "weighted_sum": ({0, 1}, set(), 1),
     "softmax_ce_loss": (set(), {1}, 2), "softmax": (set(), {0}, 1), "to_heads": (set(), set(), 1),
     "from_heads": (set(), set(), 1), "conv2d": ({0, 1}, set(), 1),
+    # reading R11b (the fx pass's elementwise ops): gelu'(x) and silu'(x) are functions of x, so
+    # their gradients read the input; y = c * x with a constant c reads nothing (dx = c dy)
+    "gelu": ({0}, set(), 1), "silu": ({0}, set(), 1), "scale": (set(), set(), 1),
 }
 
 
@@ -103,7 +106,7 @@ class Graph:
             else:
                 shp[ax] = a["end"] - a["begin"]
             out = [shp]
-        elif op in ("add", "mul", "sigmoid", "tanh", "relu"):
+        elif op in ("add", "mul", "sigmoid", "tanh", "relu", "gelu", "silu", "scale"):
             out = [list(S[0])]
         elif op == "dropout":
             out = [list(S[0]), list(S[0])]                  # y, keep-mask (u8)

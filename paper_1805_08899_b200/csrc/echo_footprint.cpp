@@ -256,7 +256,7 @@ std::string jstr(const std::string& s) {
 // ============================================================================ graph model
 enum Op {
   FC, MATMUL, BDOT, EMBED, SLICE, ADD, BADD, STACK, CONCAT, SUM, MUL, SIGMOID, TANH, RELU, DROPOUT, DOTLAST,
-  MSOFTMAX, WSUM, CE, SOFTMAX, TO_HEADS, FROM_HEADS, CONV2D, N_OPS
+  MSOFTMAX, WSUM, CE, SOFTMAX, TO_HEADS, FROM_HEADS, CONV2D, GELU, SILU, SCALE, N_OPS
 };
 struct OpInfo {
   const char* name;
@@ -274,6 +274,9 @@ const OpInfo OPS[N_OPS] = {
     {"weighted_sum", 2, 2, 1, 0b11, 0},    {"softmax_ce_loss", 2, 2, 2, 0, 0b10},
     {"softmax", 1, 1, 1, 0, 0b1},          {"to_heads", 1, 1, 1, 0, 0},    {"from_heads", 1, 1, 1, 0, 0},
     {"conv2d", 2, 3, 1, 0b11, 0},          // like an FC: its gradient reads its input and weight (Eq. 2)
+    {"gelu", 1, 1, 1, 0b1, 0},             // gelu'(x), silu'(x) are functions of x: the input is read
+    {"silu", 1, 1, 1, 0b1, 0},
+    {"scale", 1, 1, 1, 0, 0},              // y = c x (constant c): dx = c dy reads nothing
 };
 
 double dtype_width(const std::string& d) {
@@ -410,7 +413,7 @@ void infer(Graph& g, Node& n) {
       need(I[0]->shape == I[1]->shape, "equal shapes");
       out.push_back(I[0]->shape);
       break;
-    case SIGMOID: case TANH: case RELU: out.push_back(I[0]->shape); break;
+    case SIGMOID: case TANH: case RELU: case GELU: case SILU: case SCALE: out.push_back(I[0]->shape); break;
     case DROPOUT: out.push_back(I[0]->shape); out.push_back(I[0]->shape); break;
     case BADD:
       need(I[1]->shape.size() == I[0]->shape.size() + 1 &&

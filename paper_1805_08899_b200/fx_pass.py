@@ -7,8 +7,9 @@ Echo is an automatic graph pass that needs no model changes).
 1. `torch.fx` traces the model (its forward must return the scalar training loss) and ShapeProp
    records every tensor's shape / dtype.
 2. The traced graph is written in the estimator's graph schema (the op set of
-   oracle/footprint.py) -- Linear / F.linear -> fully_connected, Conv2d -> conv2d, relu / tanh / sigmoid, elementwise
-   add / mul, matmul, softmax, dropout (two outputs: y, keep-mask), sum -> sum_reduce -- and
+   oracle/footprint.py) -- Linear / F.linear -> fully_connected, Conv2d -> conv2d, relu / tanh / sigmoid / gelu /
+   silu, elementwise add / mul, multiplication or division by a constant -> scale, matmul, softmax, dropout
+   (two outputs: y, keep-mask), sum -> sum_reduce -- and
    echo_footprint_estimate (a8, Alg. 1) decides per feature map: stash, 1-bit, or
    recompute (mirrored) -- dead FC mirrors are never recomputed.
 3. The model runs through an fx Interpreter inside torch.autograd.graph.saved_tensors_hooks: every
@@ -60,13 +61,23 @@ def _kind(gm, n):
             return "sigmoid"
         if isinstance(m, nn.Dropout):
             return "dropout"
+        if isinstance(m, nn.GELU):
+            return "gelu"
+        if isinstance(m, nn.SiLU):
+            return "silu"
         raise Unsupported(f"module {type(m).__name__}")
     if n.op == "call_function":
         t = n.target
+        if t in (operator.mul, torch.mul, operator.truediv, torch.div) and len(n.args) == 2 and not n.kwargs:
+            a, b = n.args
+            scalar = lambda x: isinstance(x, (int, float)) and not isinstance(x, bool)
+            if isinstance(a, fx.Node) and scalar(b) or (t in (operator.mul, torch.mul) and scalar(a) and isinstance(b, fx.Node)):
+                return "scale"                                  # y = c x: a constant factor (or divisor)
         table = {F.linear: "fully_connected", torch.relu: "relu", F.relu: "relu", torch.tanh: "tanh",
                  torch.sigmoid: "sigmoid", operator.add: "add", torch.add: "add", operator.mul: "mul",
                  torch.mul: "mul", torch.matmul: "matmul", operator.matmul: "matmul", F.softmax: "softmax",
-                 torch.softmax: "softmax", torch.sum: "sum_reduce", F.dropout: "dropout"}
+                 torch.softmax: "softmax", torch.sum: "sum_reduce", F.dropout: "dropout", F.gelu: "gelu",
+                 F.silu: "silu"}
         if t in table:
             return table[t]
         raise Unsupported(f"function {getattr(t, '__name__', t)}")
@@ -152,7 +163,7 @@ class EchoPlan:
                     for a in n.args:
                         if isinstance(a, fx.Node):
                             ins.append([ids[a], 0])
-                        elif op not in ("softmax", "sum_reduce"):
+                        elif op not in ("softmax", "sum_reduce", "scale"):
                             raise Unsupported(f"{n.name}: non-tensor operand {a!r}")
                     if op in ("add", "mul"):
                         shapes = [self._meta(a)[0] for a in n.args if isinstance(a, fx.Node)]

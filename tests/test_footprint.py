@@ -370,3 +370,35 @@ def test_plan_self_check_catches_a_corrupted_plan(est):
             assert "plan self-check" in str(ei.value)
             n_checked += 1
     assert n_checked >= 50
+
+
+def test_gelu_silu_scale_rules(est):
+    """Reading R11b (gelu / silu gradients read their input; y = c x reads nothing), by hand over [8, 8]
+    f32 tensors (256 B):  L = sum(gelu(gelu(x))): the Baseline keeps both gelu inputs (x, g1: 512 B);
+    Echo keeps x alone (256 B): trimming keeps g1 and g2 mirrored (Alloc 256 > Rel 0 each), removes the
+    sum (0 >= 0), and dead-node elimination then drops g2 (no backward step reads its output), so g1 is
+    the one regenerated node.  L = sum(tanh(2 x)): the Baseline keeps tanh's output (256 B); Echo's trimming
+    removes the scale (Rel x 256 >= Alloc y 256) and then the tanh (Rel y 256 >= Alloc t 256): 256 B.
+    C++ == oracle on both and on a mixed graph."""
+    g = Gr.GraphBuilder()
+    x = g.placeholder("x", [8, 8])
+    g.output(g.op("sum_reduce", [g.op("gelu", [g.op("gelu", [x])])]))
+    doc = g.doc()
+    b, e = F.analyze(doc, {"strategy": "baseline"}), F.analyze(doc, {"strategy": "echo"})
+    assert b["stash"] == {(0, 0): False, (1, 0): False} and b["stash_bytes"] == 512
+    assert e["stash"] == {(0, 0): False} and sorted(e["mirrored"]) == [1] and e["stash_bytes"] == 256
+    _compare(est, doc)
+    g = Gr.GraphBuilder()
+    x = g.placeholder("x", [8, 8])
+    g.output(g.op("sum_reduce", [g.op("tanh", [g.op("scale", [x])])]))
+    doc = g.doc()
+    b, e = F.analyze(doc, {"strategy": "baseline"}), F.analyze(doc, {"strategy": "echo"})
+    assert b["stash"] == {(2, 0): False} and e["stash"] == {(2, 0): False} and e["mirrored"] == set()
+    _compare(est, doc)
+    g = Gr.GraphBuilder()
+    x = g.placeholder("x", [8, 8])
+    W = g.placeholder("W", [8, 8], trainable=True)
+    h = g.op("silu", [g.op("fully_connected", [x, W])])
+    y = g.op("gelu", [g.op("scale", [g.op("fully_connected", [h, W])])])
+    g.output(g.op("sum_reduce", [g.op("mul", [y, g.op("sigmoid", [h])])]))
+    _compare(est, g.doc())

@@ -105,9 +105,26 @@ class _TanhGateMLP(nn.Module):
         return x.sum()
 
 
+class _GeluSiluMLP(nn.Module):
+    """x <- x + W2 gelu(W1 x) * 0.5, then silu taps, F.gelu and a division by a constant."""
+
+    def __init__(self, d=32, depth=2):
+        super().__init__()
+        self.w1 = nn.ModuleList([nn.Linear(d, 2 * d) for _ in range(depth)])
+        self.w2 = nn.ModuleList([nn.Linear(2 * d, d) for _ in range(depth)])
+        self.act = nn.GELU()
+        self.tap = nn.SiLU()
+
+    def forward(self, x):
+        for a, b in zip(self.w1, self.w2):
+            x = x + b(self.act(a(x))) * 0.5
+        return (self.tap(x) / 4.0).sum() + torch.nn.functional.gelu(2.0 * x).sum()
+
+
 @pytest.mark.parametrize("make,shape", [(lambda: ReluTaps(16, 3), (4, 16)), (lambda: ResMLP(16, 3), (4, 16)),
-                                        (lambda: ResConvNet(4, 2), (2, 3, 8, 8)), (lambda: _TanhGateMLP(32, 3), (4, 32))],
-                         ids=["relutaps", "resmlp", "resconv", "tanhgate"])
+                                        (lambda: ResConvNet(4, 2), (2, 3, 8, 8)), (lambda: _TanhGateMLP(32, 3), (4, 32)),
+                                        (lambda: _GeluSiluMLP(32, 2), (4, 32))],
+                         ids=["relutaps", "resmlp", "resconv", "tanhgate", "gelusilu"])
 def test_echo_module_plan_application_on_host(make, shape):
     """The saved-tensor-hook machinery of EchoModule on host tensors, for plans without 1-bit edges (the
     1-bit pack is a libecho kernel; the GPU test covers it): loss and every parameter gradient bitwise
