@@ -105,6 +105,8 @@ MUTATIONS = [
     ("nmt", "x = s[\"h\"] * md[l][t] if l < L - 1 else s[\"h\"]", "x = s[\"h\"]", "decoder hidden dropout (R33) not applied"),
     # ---- oracle/footprint.py (Alg. 1; liveness SPEC:422-433)
     ("footprint", "if rel >= alloc:", "if rel > alloc:", "trimming tie rule (PAPER.md:549 'greater than or equal')"),
+    ("footprint", '"gelu": ({0}, set(), 1)', '"gelu": (set(), {0}, 1)', "gelu gradient reads its output instead of its input"),
+    ("footprint", '"scale": (set(), set(), 1)', '"scale": ({0}, set(), 1)', "scale gradient reads its input"),
     ("footprint", "M -= group", "M -= {s}", "trimming removes the node, not its sharer group"),
     ("footprint", "for c in G.consumers.get(e, []):\n                            if c in M and c not in group and not binz(c):",
      "for c in G.consumers.get(e, [])[:1]:\n                            if c in M and c not in group and not binz(c):",
