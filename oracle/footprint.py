@@ -53,6 +53,9 @@ GRAD_DEPS = {
     # reading R11b (the fx pass's elementwise ops): gelu'(x) and silu'(x) are functions of x, so
     # their gradients read the input; y = c * x with a constant c reads nothing (dx = c dy)
     "gelu": ({0}, set(), 1), "silu": ({0}, set(), 1), "scale": (set(), set(), 1),
+    # layer_norm(x, weight, bias) -> (y, mean, rstd): its gradient reads x and the row statistics
+    # (torch's native_layer_norm saves exactly those besides the weights), not y
+    "layer_norm": ({0}, {1, 2}, 3),
 }
 
 
@@ -93,6 +96,10 @@ class Graph:
         elif op == "from_heads":
             Hh = a["heads"]
             out = [[S[0][0] // Hh * S[0][1], Hh * S[0][2]]]
+        elif op == "layer_norm":                            # stats over the last norm_ndim dims, kept per row
+            k = a.get("norm_ndim", 1)
+            st = list(S[0][:-k]) + [1] * k
+            out = [list(S[0]), st, st]
         elif op == "conv2d":                                # x [N,C,H,W], W [O,C,kh,kw]; stride, padding
             st, pd = a.get("stride", 1), a.get("padding", 0)
             out = [[S[0][0], S[1][0], (S[0][2] + 2 * pd - S[1][2]) // st + 1, (S[0][3] + 2 * pd - S[1][3]) // st + 1]]
@@ -140,6 +147,8 @@ class Graph:
                 d = "f32"
             if op == "dropout" and k == 1:
                 d = "u8"
+            if op == "layer_norm" and k > 0 and D[0] == "bf16":
+                d = "f32"                                   # the statistics are kept in fp32 for bf16 inputs
             self.dtype[(n["id"], k)] = d
 
     # -------------------------------------------------------------- helpers
@@ -192,6 +201,8 @@ class Graph:
             return 2 * self.numel(ins[1] if op == "weighted_sum" else ins[0])
         if op == "dropout":
             return 2 * self.numel(o)
+        if op == "layer_norm":
+            return 5 * self.numel(o)
         if op == "sum_reduce":
             return self.numel(ins[0])
         return self.numel(o)

@@ -256,7 +256,7 @@ std::string jstr(const std::string& s) {
 // ============================================================================ graph model
 enum Op {
   FC, MATMUL, BDOT, EMBED, SLICE, ADD, BADD, STACK, CONCAT, SUM, MUL, SIGMOID, TANH, RELU, DROPOUT, DOTLAST,
-  MSOFTMAX, WSUM, CE, SOFTMAX, TO_HEADS, FROM_HEADS, CONV2D, GELU, SILU, SCALE, N_OPS
+  MSOFTMAX, WSUM, CE, SOFTMAX, TO_HEADS, FROM_HEADS, CONV2D, GELU, SILU, SCALE, LAYERNORM, N_OPS
 };
 struct OpInfo {
   const char* name;
@@ -277,6 +277,7 @@ const OpInfo OPS[N_OPS] = {
     {"gelu", 1, 1, 1, 0b1, 0},             // gelu'(x), silu'(x) are functions of x: the input is read
     {"silu", 1, 1, 1, 0b1, 0},
     {"scale", 1, 1, 1, 0, 0},              // y = c x (constant c): dx = c dy reads nothing
+    {"layer_norm", 1, 3, 3, 0b1, 0b110},   // (y, mean, rstd): the gradient reads x and the row statistics
 };
 
 double dtype_width(const std::string& d) {
@@ -414,6 +415,16 @@ void infer(Graph& g, Node& n) {
       out.push_back(I[0]->shape);
       break;
     case SIGMOID: case TANH: case RELU: case GELU: case SILU: case SCALE: out.push_back(I[0]->shape); break;
+    case LAYERNORM: {   // statistics over the last norm_ndim dims, one per row
+      const int64_t k = attr_int(n, "norm_ndim", 1);
+      need(k >= 1 && k <= (int64_t)I[0]->shape.size(), "norm_ndim");
+      std::vector<int64_t> st(I[0]->shape.begin(), I[0]->shape.end() - k);
+      st.insert(st.end(), (size_t)k, 1);
+      out.push_back(I[0]->shape);
+      out.push_back(st);
+      out.push_back(st);
+      break;
+    }
     case DROPOUT: out.push_back(I[0]->shape); out.push_back(I[0]->shape); break;
     case BADD:
       need(I[1]->shape.size() == I[0]->shape.size() + 1 &&
@@ -456,7 +467,9 @@ void infer(Graph& g, Node& n) {
   if (dt.empty()) dt = n.op == EMBED ? I[1]->dtype : I[0]->dtype;
   dtype_width(dt);
   for (size_t k = 0; k < out.size(); ++k) {
-    Edge e{n.id, (int)k, out[k], n.op == CE ? std::string("f32") : (n.op == DROPOUT && k == 1 ? std::string("u8") : dt)};
+    std::string dk = n.op == CE ? std::string("f32") : (n.op == DROPOUT && k == 1 ? std::string("u8") : dt);
+    if (n.op == LAYERNORM && k > 0 && I[0]->dtype == "bf16") dk = "f32";   // fp32 statistics for bf16 inputs
+    Edge e{n.id, (int)k, out[k], dk};
     for (auto s : e.shape) need(s >= 1, "non-positive dim");
     if (k == 0) g.first_out[n.id] = (int)g.edges.size();
     n.out.push_back((int)g.edges.size());
@@ -628,6 +641,7 @@ int64_t flops(const Graph& g, const Node& n) {
     case DOTLAST: return 2 * E(0).numel();
     case WSUM: return 2 * E(1).numel();
     case DROPOUT: return 2 * o.numel();
+    case LAYERNORM: return 5 * o.numel();
     case SUM: return E(0).numel();
     default: return o.numel();
   }

@@ -8,8 +8,9 @@ Echo is an automatic graph pass that needs no model changes).
    records every tensor's shape / dtype.
 2. The traced graph is written in the estimator's graph schema (the op set of
    oracle/footprint.py) -- Linear / F.linear -> fully_connected, Conv2d -> conv2d, relu / tanh / sigmoid / gelu /
-   silu, elementwise add / mul, multiplication or division by a constant -> scale, matmul, softmax, dropout
-   (two outputs: y, keep-mask), sum -> sum_reduce -- and
+   silu, LayerNorm / F.layer_norm -> layer_norm (three outputs: y, mean, rstd), elementwise add / mul,
+   multiplication or division by a constant -> scale, matmul, softmax, dropout (two outputs: y,
+   keep-mask), sum -> sum_reduce -- and
    echo_footprint_estimate (a8, Alg. 1) decides per feature map: stash, 1-bit, or
    recompute (mirrored) -- dead FC mirrors are never recomputed.
 3. The model runs through an fx Interpreter inside torch.autograd.graph.saved_tensors_hooks: every
@@ -65,6 +66,8 @@ def _kind(gm, n):
             return "gelu"
         if isinstance(m, nn.SiLU):
             return "silu"
+        if isinstance(m, nn.LayerNorm):
+            return "layer_norm"
         raise Unsupported(f"module {type(m).__name__}")
     if n.op == "call_function":
         t = n.target
@@ -77,7 +80,7 @@ def _kind(gm, n):
                  torch.sigmoid: "sigmoid", operator.add: "add", torch.add: "add", operator.mul: "mul",
                  torch.mul: "mul", torch.matmul: "matmul", operator.matmul: "matmul", F.softmax: "softmax",
                  torch.softmax: "softmax", torch.sum: "sum_reduce", F.dropout: "dropout", F.gelu: "gelu",
-                 F.silu: "silu"}
+                 F.silu: "silu", F.layer_norm: "layer_norm"}
         if t in table:
             return table[t]
         raise Unsupported(f"function {getattr(t, '__name__', t)}")
@@ -155,6 +158,21 @@ class EchoPlan:
                     if m.bias is not None:
                         ins.append(param(f"{n.target}.bias", m.bias))
                     attrs.update(stride=int(st[0]), padding=int(pd[0]))
+                elif op == "layer_norm":
+                    if n.op == "call_module":
+                        m = gm.get_submodule(n.target)
+                        shape = tuple(m.normalized_shape)
+                        ins = [[ids[n.args[0]], 0]]
+                        if m.weight is not None:
+                            ins.append(param(f"{n.target}.weight", m.weight))
+                        if m.bias is not None:
+                            ins.append(param(f"{n.target}.bias", m.bias))
+                    else:
+                        shape = n.args[1] if len(n.args) > 1 else n.kwargs["normalized_shape"]
+                        if any(isinstance(a, fx.Node) for a in list(n.args[2:]) + list(n.kwargs.values())):
+                            raise Unsupported(f"{n.name}: functional layer_norm with weight / bias tensors")
+                        ins = [[ids[n.args[0]], 0]]
+                    attrs["norm_ndim"] = len(shape) if isinstance(shape, (tuple, list)) else 1
                 elif op == "dropout":
                     m = gm.get_submodule(n.target) if n.op == "call_module" else None
                     attrs["p"] = m.p if m is not None else n.kwargs.get("p", n.args[1] if len(n.args) > 1 else 0.5)
@@ -187,6 +205,7 @@ class _Run(fx.Interpreter):
 
     def run_node(self, n):
         self.o.current = n
+        self.o.ln_stat = 0
         out = super().run_node(n)
         if isinstance(out, torch.Tensor) and n in self.o.plan.node_id:
             self.o._record(n, out)
@@ -236,8 +255,12 @@ class EchoModule(nn.Module):
         for a in n.all_input_nodes:
             if self.ptr_of.get(a) == k:
                 return (self.plan.node_id[a], 0)
-        if _kind(self.plan.gm, n) == "dropout" and t.dtype == torch.bool:
+        kind = _kind(self.plan.gm, n)
+        if kind == "dropout" and t.dtype == torch.bool:
             return (self.plan.node_id[n], 1)
+        if kind == "layer_norm":                               # native_layer_norm saves x, then mean, rstd
+            self.ln_stat = getattr(self, "ln_stat", 0) + 1
+            return (self.plan.node_id[n], self.ln_stat)
         return (self.plan.node_id[n], 0)
 
     def _pack(self, t):
@@ -257,9 +280,9 @@ class EchoModule(nn.Module):
                 self.bits[e] = (bits, t.shape, t.dtype)
                 self._keep(bits, bits.numel())
             return ("B", bits, t.shape, t.dtype)
-        if e[1] == 1 and d != "bit":                           # a kept (byte) mask is also a frontier
+        if e[1] >= 1 and d not in ("bit", "recompute"):      # a kept (byte) mask / statistic is a frontier too
             self.env[e] = t
-        if d == "recompute" and e[1] == 0:
+        if d == "recompute":                                  # (never a keep-mask: masks are random, R26)
             return ("R", e, t.shape, t.stride(), t.storage_offset())
         self._keep(t)
         return ("T", t)
@@ -295,6 +318,10 @@ class EchoModule(nn.Module):
         else:
             with torch.no_grad():
                 v = self._rerun(n)
+            if isinstance(v, tuple):                           # layer_norm: (y, mean, rstd), all cached
+                for k, x in enumerate(v):
+                    self.cache[(e[0], k)] = x
+                v = v[e[1]]
         self.cache[e] = v
         return v
 
@@ -319,6 +346,13 @@ class EchoModule(nn.Module):
                 return args[0]
             mask = self._value((self.plan.node_id[n], 1))
             return args[0] * mask * (1.0 / (1.0 - p))
+        if _kind(gm, n) == "layer_norm":                      # all three outputs (the same kernel as the forward)
+            if n.op == "call_module":
+                m = gm.get_submodule(n.target)
+                return tuple(torch.native_layer_norm(args[0], m.normalized_shape, m.weight, m.bias, m.eps))
+            shape = args[1] if len(args) > 1 else kwargs["normalized_shape"]
+            eps = kwargs.get("eps", args[4] if len(args) > 4 else 1e-5)
+            return tuple(torch.native_layer_norm(args[0], list(shape), None, None, eps))
         if n.op == "call_module":
             return gm.get_submodule(n.target)(*args, **kwargs)
         if n.op == "call_method":

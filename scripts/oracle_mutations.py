@@ -107,6 +107,8 @@ MUTATIONS = [
     ("footprint", "if rel >= alloc:", "if rel > alloc:", "trimming tie rule (PAPER.md:549 'greater than or equal')"),
     ("footprint", '"gelu": ({0}, set(), 1)', '"gelu": (set(), {0}, 1)', "gelu gradient reads its output instead of its input"),
     ("footprint", '"scale": (set(), set(), 1)', '"scale": ({0}, set(), 1)', "scale gradient reads its input"),
+    ("footprint", '"layer_norm": ({0}, {1, 2}, 3)', '"layer_norm": ({0}, {0}, 3)', "layer-norm gradient reads y, not the statistics"),
+    ("footprint", 'if op == "layer_norm" and k > 0 and D[0] == "bf16":', 'if False:', "bf16 layer-norm statistics kept in bf16"),
     ("footprint", "M -= group", "M -= {s}", "trimming removes the node, not its sharer group"),
     ("footprint", "for c in G.consumers.get(e, []):\n                            if c in M and c not in group and not binz(c):",
      "for c in G.consumers.get(e, [])[:1]:\n                            if c in M and c not in group and not binz(c):",

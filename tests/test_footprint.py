@@ -402,3 +402,25 @@ def test_gelu_silu_scale_rules(est):
     y = g.op("gelu", [g.op("scale", [g.op("fully_connected", [h, W])])])
     g.output(g.op("sum_reduce", [g.op("mul", [y, g.op("sigmoid", [h])])]))
     _compare(est, g.doc())
+
+
+def test_layer_norm_rule(est):
+    """layer_norm(x, w, b) -> (y, mean, rstd), gradient reads x and the row statistics (torch's
+    native_layer_norm saves exactly those besides the weights).  By hand, x [4, 8], z = FC(LN(x)),
+    L = sum(z):  Baseline keeps x, mean, rstd (LN's gradient) and y (the FC's input): f32
+    128 + 16 + 16 + 128 = 288 B; bf16 (fp32 statistics) 64 + 16 + 16 + 64 = 160 B.  Echo mirrors the LN
+    (trimming it would allocate y, mean, rstd and release nothing) and keeps x alone: 128 / 64 B.
+    C++ == oracle for every plan."""
+    for dt, base, echo in (("f32", 288, 128), ("bf16", 160, 64)):
+        g = Gr.GraphBuilder()
+        x = g.placeholder("x", [4, 8], dt)
+        w, b = g.placeholder("w", [8], dt, trainable=True), g.placeholder("b", [8], dt, trainable=True)
+        W = g.placeholder("W", [8, 8], dt, trainable=True)
+        y = g.op("layer_norm", [x, w, b], nout=3, norm_ndim=1)[0]
+        g.output(g.op("sum_reduce", [g.op("fully_connected", [y, W])]))
+        doc = g.doc()
+        rb, re_ = F.analyze(doc, {"strategy": "baseline"}), F.analyze(doc, {"strategy": "echo"})
+        assert rb["stash_bytes"] == base and re_["stash_bytes"] == echo, dt
+        assert re_["mirrored"] == {4} and re_["stash"] == {(0, 0): False}
+        assert rb["graph"].dtype[(4, 1)] == "f32" and rb["graph"].shape[(4, 1)] == [4, 1]
+        _compare(est, doc)

@@ -121,10 +121,28 @@ class _GeluSiluMLP(nn.Module):
         return (self.tap(x) / 4.0).sum() + torch.nn.functional.gelu(2.0 * x).sum()
 
 
+class _PreLNBlock(nn.Module):
+    """Transformer-style MLP blocks x <- x + W2 gelu(W1 LN(x)), a final F.layer_norm (no affine) and a
+    linear head."""
+
+    def __init__(self, d=32, depth=2):
+        super().__init__()
+        self.ln = nn.ModuleList([nn.LayerNorm(d) for _ in range(depth)])
+        self.w1 = nn.ModuleList([nn.Linear(d, 4 * d) for _ in range(depth)])
+        self.w2 = nn.ModuleList([nn.Linear(4 * d, d) for _ in range(depth)])
+        self.head = nn.Linear(d, d)
+        self.d = d
+
+    def forward(self, x):
+        for n, a, b in zip(self.ln, self.w1, self.w2):
+            x = x + b(torch.nn.functional.gelu(a(n(x))))
+        return self.head(torch.nn.functional.layer_norm(x, (self.d,))).sum()
+
+
 @pytest.mark.parametrize("make,shape", [(lambda: ReluTaps(16, 3), (4, 16)), (lambda: ResMLP(16, 3), (4, 16)),
                                         (lambda: ResConvNet(4, 2), (2, 3, 8, 8)), (lambda: _TanhGateMLP(32, 3), (4, 32)),
-                                        (lambda: _GeluSiluMLP(32, 2), (4, 32))],
-                         ids=["relutaps", "resmlp", "resconv", "tanhgate", "gelusilu"])
+                                        (lambda: _GeluSiluMLP(32, 2), (4, 32)), (lambda: _PreLNBlock(32, 2), (6, 32))],
+                         ids=["relutaps", "resmlp", "resconv", "tanhgate", "gelusilu", "preln"])
 def test_echo_module_plan_application_on_host(make, shape):
     """The saved-tensor-hook machinery of EchoModule on host tensors, for plans without 1-bit edges (the
     1-bit pack is a libecho kernel; the GPU test covers it): loss and every parameter gradient bitwise
