@@ -529,6 +529,14 @@ def run_ours(args):
                 print(f"[bench] mirror plan failed: {ex}", file=sys.stderr)
         out["ms_other"] = ms_other
         out["mem"] = mem
+        if ws == 1 and use_graph:                                # the same step without the CUDA graph
+            try:
+                m4 = build(mode)
+                out["eager"], _ = timed(m4, False, max(3, args.steps // 2), args.warmup)
+                del m4
+                torch.cuda.empty_cache()
+            except Exception as ex:
+                print(f"[bench] eager timing failed: {ex}", file=sys.stderr)
         out["kern"] = time_attn_bwd(cfg, dtype)
         out["probe"] = probe_kernels(mode, args.steps, args.warmup) if use_graph and mode == abi.RECOMPUTE else None
         out["traffic"] = ncu_traffic(dtype) if cfg.B == 128 else None
@@ -607,6 +615,10 @@ def run_ours(args):
                 "value": samples / (mi["ms_per_step"] / 1e3), "ms_per_step": mi["ms_per_step"],
                 "peak_activation_bytes": mi["mem"][0], "stash_bytes": mi["mem"][1],
                 "stash_reduction_vs_stash": (st[1] / mi["mem"][1]) if st[1] and mi["mem"][1] else None}
+        if out.get("eager"):
+            line["eager_mode"] = {"value": samples / (out["eager"] / 1e3), "ms_per_step": out["eager"],
+                                  "how": "the same step launched from the host without the CUDA graph "
+                                         "(SURVEY 8(d): eager and graph mode reported separately), device-timed"}
         if out["ms_other"]:
             other_name = "stash" if mode == abi.RECOMPUTE else "recompute"
             line[f"{other_name}_mode"] = {"value": samples / (out["ms_other"] / 1e3), "ms_per_step": out["ms_other"]}
