@@ -607,6 +607,19 @@ def run_ours(args):
             "stash_ratio": (st[1] / rc[1]) if st[1] and rc[1] else None,
             "how": "torch max_memory_allocated - memory_allocated at step start (eager), fp32 allocator bytes",
         }
+        try:                                                     # the host estimator's numbers beside them
+            from synth import graphs as Gr
+            gdoc = json.dumps(Gr.nmt(cfg, "f32" if dtype == abi.FP32 else "bf16"))
+            est = {s_: json.loads(abi.echo_footprint_estimate(gdoc, json.dumps({"strategy": s_})))
+                   for s_ in ("baseline", "echo")}
+            line["memory"]["estimator"] = {
+                "stash_bytes": {"stash": est["baseline"]["stash_bytes"], "recompute": est["echo"]["stash_bytes"]},
+                "peak_bytes": {"stash": est["baseline"]["peak_bytes"], "recompute": est["echo"]["peak_bytes"]},
+                "how": "echo_footprint_estimate on the step's graph (synth/graphs.py nmt): stash bytes are exact "
+                       "(== stash_bytes above); peak = its liveness model of feature maps and activation "
+                       "gradients over one schedule (no GEMM workspaces, no allocator rounding)"}
+        except Exception as ex:
+            print(f"[bench] estimator numbers failed: {ex}", file=sys.stderr)
         mi = out.get("mirror")
         if mi:
             line["mirror_mode"] = {
