@@ -14,5 +14,5 @@ for r in $out/r02b_a5rows_*.ncu-rep $out/r02b_a6_c2_fp32.ncu-rep; do
   b=$(basename "$r" .ncu-rep)
   python scripts/ncu_summary.py "$r" > "profiles/${b}_ncu.txt" 2>&1
 done
-[ -s "$out/r02b_launches_fp32.csv" ] && python scripts/summarize_launches.py "$out/r02b_launches_fp32.csv" > profiles/r02b_launches_fp32.txt 2>&1
+[ -s "$out/r02b_launches_fp32.csv" ] && python scripts/summarize_launches.py "$out/r02b_launches_fp32.csv" profiles/r02b_launches_c2_fp32_recompute.csv "C2 fp32 recompute, round 2 closing bundle"
 ls -la profiles | grep r02b
