@@ -325,9 +325,14 @@ CHEAP_UNARY = ["tanh", "sigmoid", "relu"]
 CHEAP_BINARY = ["add", "mul"]
 
 
-def random_graph(seed, max_nodes=40, N=8):
-    """Seeded random DAG mixing cheap / compute-heavy / binarizable ops over [N, N] tensors."""
+CHEAP_UNARY_X = CHEAP_UNARY + ["gelu", "silu", "scale"]
+
+
+def random_graph(seed, max_nodes=40, N=8, extended=False):
+    """Seeded random DAG mixing cheap / compute-heavy / binarizable ops over [N, N] tensors.
+    extended=True also draws the fx pass's gelu / silu / scale and 3-output layer_norm nodes."""
     rng = np.random.default_rng(seed)
+    unary = CHEAP_UNARY_X if extended else CHEAP_UNARY
     g = GraphBuilder()
     edges = [g.placeholder(f"x{i}", [N, N], "f32") for i in range(int(rng.integers(1, 4)))]
     W = g.placeholder("W", [N, N], "f32", trainable=True)
@@ -335,8 +340,10 @@ def random_graph(seed, max_nodes=40, N=8):
     for _ in range(n_ops):
         r = rng.random()
         a = edges[int(rng.integers(0, len(edges)))]
-        if r < 0.35:
-            e = g.op(CHEAP_UNARY[int(rng.integers(0, 3))], [a])
+        if extended and r < 0.08:
+            e = g.op("layer_norm", [a], nout=3, norm_ndim=1)[0]
+        elif r < 0.35:
+            e = g.op(unary[int(rng.integers(0, len(unary)))], [a])
         elif r < 0.65:
             b = edges[int(rng.integers(0, len(edges)))]
             e = g.op(CHEAP_BINARY[int(rng.integers(0, 2))], [a, b])

@@ -424,3 +424,14 @@ def test_layer_norm_rule(est):
         assert re_["mirrored"] == {4} and re_["stash"] == {(0, 0): False}
         assert rb["graph"].dtype[(4, 1)] == "f32" and rb["graph"].shape[(4, 1)] == [4, 1]
         _compare(est, doc)
+
+
+def test_cpp_matches_oracle_random_graphs_extended_ops(est):
+    """Random graphs with the fx pass's gelu / silu / scale / layer_norm (R11b, R11c): C++ == oracle for
+    every plan, the plan self-check passes, and Echo never keeps more than the Baseline."""
+    for seed in range(60):
+        doc = Gr.random_graph(seed, extended=True)
+        _compare(est, doc)
+        for st in ("baseline", "mirror", "echo"):
+            est(doc, {"strategy": st, "self_verify": True})
+        assert est(doc, {"strategy": "echo"})["stash_bytes"] <= est(doc, {"strategy": "baseline"})["stash_bytes"], seed
