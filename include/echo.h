@@ -437,7 +437,8 @@ echo_status echo_tanh_bwd(int64_t n, int32_t dtype, const void* a, const float* 
  *  report_json  caller buffer for the NUL-terminated report; may be NULL to query
  *  report_len   IN capacity of report_json; OUT bytes needed (including the NUL).
  *               Returns ECHO_ERR_CAPACITY (with *report_len set) if too small.
- * Errors: ECHO_ERR_INVALID (parse / schema / unknown op / arity / shape),
+ * Errors: ECHO_ERR_INVALID (parse / schema / unknown op / arity / shape / an unknown or
+ *         wrongly typed config key),
  *         ECHO_ERR_GRAPH (cycle or pipeline failure),
  *         ECHO_ERR_MISMATCH (self_verify: the plan leaves a gradient input unavailable). */
 echo_status echo_footprint_estimate(const char* graph_json, const char* config_json,

@@ -599,6 +599,31 @@ Config parse_config(const char* s) {
   auto doc = parse_json(s);
   const Json& j = *doc->root;
   if (j.kind != Json::OBJ) throw ParseError("config: must be an object");
+  // strict schema: an unknown key or a value of the wrong kind is an error, not silently ignored
+  static const char* const kKeys[] = {"strategy", "compute_heavy_ops", "binarizable_ops", "enable_dead_node",
+                                      "enable_binarization", "regenerate_masks", "flop_threshold",
+                                      "weight_multiplier", "self_verify", "debug_unstash_edge"};
+  for (uint32_t i = 0; i < j.arr.n; ++i) {
+    bool known = false;
+    for (const char* k : kKeys) known = known || j.keys[i] == k;
+    if (!known) throw ParseError("config: unknown key '" + std::string(j.keys[i]) + "'");
+  }
+  auto kind_of = [&](const char* k, Json::Kind want, const char* what) {
+    const Json* v = j.get(k);
+    if (v && v->kind != want) throw ParseError(std::string("config: ") + k + " must be " + what);
+    return v;
+  };
+  for (const char* k : {"enable_dead_node", "enable_binarization", "regenerate_masks", "self_verify"})
+    kind_of(k, Json::BOOL, "a boolean");
+  for (const char* k : {"compute_heavy_ops", "binarizable_ops"}) {
+    if (const Json* v = kind_of(k, Json::ARR, "an array of op names"))
+      for (auto& x : v->arr)
+        if (x.kind != Json::STR) throw ParseError(std::string("config: ") + k + " must be an array of op names");
+  }
+  kind_of("strategy", Json::STR, "a string");
+  kind_of("flop_threshold", Json::NUM, "a number");
+  kind_of("weight_multiplier", Json::NUM, "a number");
+  kind_of("debug_unstash_edge", Json::ARR, "[node, out]");
   if (auto* v = j.get("strategy")) c.kind = std::string(v->str);
   if (c.kind != "echo" && c.kind != "mirror" && c.kind != "baseline") throw ParseError("config: bad strategy");
   if (auto* v = j.get("compute_heavy_ops")) {

@@ -201,6 +201,17 @@ def test_error_codes(est):
     buf = ctypes.create_string_buffer(4)
     st = lib.echo_footprint_estimate(json.dumps(Gr.add_tanh(8)).encode(), None, buf, ctypes.byref(n))
     assert st == abi.ECHO_ERR_CAPACITY and n.value > 4
+    # the strategy config is validated strictly: unknown keys and wrongly typed values are errors
+    g = json.dumps(Gr.add_tanh(8))
+    for cfg, what in (({"strategy": "echo", "enable_deadnode": False}, "unknown key"),
+                      ({"strategy": "echo", "enable_dead_node": 0}, "boolean"),
+                      ({"strategy": "echo", "compute_heavy_ops": "fully_connected"}, "array"),
+                      ({"strategy": "echo", "compute_heavy_ops": [1]}, "array"),
+                      ({"strategy": 3}, "string"), ({"strategy": "greedy"}, "bad strategy"),
+                      ({"strategy": "echo", "flop_threshold": "high"}, "number")):
+        with pytest.raises(abi.EchoError) as ex:
+            abi.echo_footprint_estimate(g, json.dumps(cfg))
+        assert ex.value.status == abi.ECHO_ERR_INVALID and what in str(ex.value), (cfg, str(ex.value))
 
 
 def test_regenerated_masks_reading_r30(est):
